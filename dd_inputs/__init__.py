@@ -1,0 +1,338 @@
+"""Seeded synthetic inputs shaped like the paper's 3D DD auxiliary matrices.
+
+This module is the ONLY code shared by the CUDA path's tests/bench and the CPU
+oracle (`oracle/`).  It holds no arithmetic of the method (no factorization, no
+solve): it only draws random numbers and builds the input matrix the paper's
+pipeline would hand to the auxiliary-problem solver.
+
+What is synthesised (BASELINE.json `configs[0..4]`, DESIGN.md
+"Input recipe"):
+
+* A box grid of nx*ny*nz subdomains; an *interface* is an unordered pair {p<q}
+  of touching subdomains (face pairs; for config 2 also edge/corner pairs),
+  subdomain id p = x + nx*(y + ny*z), interface ids sorted by (p, q)
+  (SURVEY.md ledger L13).  Interface I carries s_I dual DoFs.
+* Each subdomain p contributes one dense symmetric clique
+  S_p = G^T diag(d) G + sigma*I over the concatenated DoFs of the interfaces it
+  touches (ascending interface id), G square N(0,1) (ledger L11),
+  d = +-U(0.5, 2) (complex: + i*U(0, 0.1)), sigma = 0.1 (complex 0.1+0.05i),
+  plain transpose (complex *symmetric*, never Hermitian), then symmetrised
+  (S + S^T)/2 (ledger L12) and accumulated additively into the lower blocks.
+  This is the "sparse collection of dense blocks" of PAPER.md:29 (§II): one
+  dense clique per subdomain, as the primal elimination of PAPER.md:27 would
+  produce.
+* Right-hand sides B (n x nrhs) with N(0,1) entries (complex: re and im).
+
+Two random back-ends with the same recipe:
+  backend="numpy": numpy.random.default_rng(seed) (PCG64), draw order per
+      subdomain ascending: G (re, then im), sign, mag, (im_d); then B.
+  backend="torch": a torch.Generator on the target device (used only for the
+      full-size bench configs where numpy would take minutes); same recipe,
+      different stream of numbers.  Both sides of any parity comparison always
+      receive the very same bytes.
+"""
+from __future__ import annotations
+
+import dataclasses
+import itertools
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+__all__ = ["Problem", "grid_interfaces", "build_problem", "config", "CONFIGS", "random_rhs",
+           "dense_expand", "block_pattern_from_cliques"]
+
+
+@dataclasses.dataclass
+class Problem:
+    """Block-sparse symmetric matrix in the C-ABI input format.
+
+    blk_size[nblk]      int64, interface sizes s_I
+    colptr[nblk+1]      int64, block-CSC column pointers of the LOWER pattern
+    rowidx[nnzb]        int32, row block ids (sorted, >= column, diagonal first)
+    values              1-D float64 / complex128: all blocks concatenated, block p
+                        (CSC position) is column-major s_row x s_col at val_offset[p]
+    val_offset[nnzb]    int64 element offsets
+    cliques             list of (subdomain id, interface ids) -- provenance only
+    """
+    blk_size: np.ndarray
+    colptr: np.ndarray
+    rowidx: np.ndarray
+    values: np.ndarray
+    val_offset: np.ndarray
+    cliques: List[Tuple[int, List[int]]]
+    name: str = ""
+
+    @property
+    def nblk(self) -> int:
+        return int(self.blk_size.shape[0])
+
+    @property
+    def n(self) -> int:
+        return int(self.blk_size.sum())
+
+    @property
+    def nnzb(self) -> int:
+        return int(self.rowidx.shape[0])
+
+    @property
+    def is_complex(self) -> bool:
+        return np.iscomplexobj(self.values)
+
+    @property
+    def dof_offset(self) -> np.ndarray:
+        return np.concatenate([[0], np.cumsum(self.blk_size)]).astype(np.int64)
+
+    def block(self, p: int) -> np.ndarray:
+        """Block at CSC position p as an (s_row, s_col) view (column-major storage)."""
+        j = int(np.searchsorted(self.colptr, p, side="right") - 1)
+        i = int(self.rowidx[p])
+        si, sj = int(self.blk_size[i]), int(self.blk_size[j])
+        off = int(self.val_offset[p])
+        return self.values[off:off + si * sj].reshape(sj, si).T
+
+    def blocks(self) -> Dict[Tuple[int, int], np.ndarray]:
+        out = {}
+        for j in range(self.nblk):
+            for p in range(int(self.colptr[j]), int(self.colptr[j + 1])):
+                out[(int(self.rowidx[p]), j)] = self.block(p)
+        return out
+
+
+# --------------------------------------------------------------------------- topology
+def _sid(x, y, z, nx, ny):
+    return x + nx * (y + ny * z)
+
+
+def grid_interfaces(nx: int, ny: int, nz: int) -> List[Tuple[int, int]]:
+    """Face-adjacent subdomain pairs (p<q), sorted by (p, q) (ledger L13)."""
+    pairs = []
+    for z in range(nz):
+        for y in range(ny):
+            for x in range(nx):
+                p = _sid(x, y, z, nx, ny)
+                if x + 1 < nx:
+                    pairs.append((p, _sid(x + 1, y, z, nx, ny)))
+                if y + 1 < ny:
+                    pairs.append((p, _sid(x, y + 1, z, nx, ny)))
+                if z + 1 < nz:
+                    pairs.append((p, _sid(x, y, z + 1, nx, ny)))
+    return sorted(pairs)
+
+
+def _edge_corner_pairs(nx, ny, nz):
+    out = []
+    for z, y, x in itertools.product(range(nz), range(ny), range(nx)):
+        p = _sid(x, y, z, nx, ny)
+        for dx, dy, dz in itertools.product((-1, 0, 1), repeat=3):
+            if abs(dx) + abs(dy) + abs(dz) < 2:
+                continue
+            X, Y, Z = x + dx, y + dy, z + dz
+            if 0 <= X < nx and 0 <= Y < ny and 0 <= Z < nz:
+                q = _sid(X, Y, Z, nx, ny)
+                if p < q:
+                    out.append((p, q))
+    return sorted(out)
+
+
+def unstructured_interfaces(nx, ny, nz, rng: np.random.Generator, drop=0.3, dmin=4, dmax=14):
+    """Config 2 topology, reading L9.
+
+    Drop 30% of face pairs at random; each subdomain draws a target degree
+    t_p ~ U{dmin..dmax}; shuffled edge/corner pairs are added while both ends are
+    below target; then a fix-up pass adds pairs (faces first) until every
+    subdomain touches >= dmin interfaces.
+    """
+    nsub = nx * ny * nz
+    faces = grid_interfaces(nx, ny, nz)
+    keep = rng.random(len(faces)) >= drop
+    pairs = {f for f, k in zip(faces, keep) if k}
+    target = rng.integers(dmin, dmax + 1, nsub)
+    deg = np.zeros(nsub, dtype=np.int64)
+    for p, q in pairs:
+        deg[p] += 1
+        deg[q] += 1
+    cand = _edge_corner_pairs(nx, ny, nz)
+    order = rng.permutation(len(cand))
+    for t in order:
+        p, q = cand[t]
+        if deg[p] < target[p] and deg[q] < target[q] and deg[p] < dmax and deg[q] < dmax:
+            pairs.add((p, q))
+            deg[p] += 1
+            deg[q] += 1
+    # fix-up: every subdomain touches >= dmin interfaces
+    allc = [f for f in faces if f not in pairs] + [c for c in cand if c not in pairs]
+    for p in range(nsub):
+        for (a, b) in allc:
+            if deg[p] >= dmin:
+                break
+            if p in (a, b) and (a, b) not in pairs and deg[a] < dmax and deg[b] < dmax:
+                pairs.add((a, b))
+                deg[a] += 1
+                deg[b] += 1
+    return sorted(pairs)
+
+
+def block_pattern_from_cliques(nblk: int, cliques: Sequence[Sequence[int]]):
+    """Lower block pattern = diagonal + union of clique pairs (block-CSC)."""
+    cols: List[set] = [{j} for j in range(nblk)]
+    for members in cliques:
+        ms = sorted(members)
+        for a in range(len(ms)):
+            for b in range(a + 1, len(ms)):
+                cols[ms[a]].add(ms[b])
+    colptr = np.zeros(nblk + 1, dtype=np.int64)
+    rows = []
+    for j in range(nblk):
+        r = sorted(cols[j])
+        rows.extend(r)
+        colptr[j + 1] = colptr[j] + len(r)
+    return colptr, np.asarray(rows, dtype=np.int32)
+
+
+# --------------------------------------------------------------------------- values
+def _layout(blk_size, colptr, rowidx):
+    nnzb = len(rowidx)
+    off = np.zeros(nnzb, dtype=np.int64)
+    tot = 0
+    for j in range(len(blk_size)):
+        for p in range(int(colptr[j]), int(colptr[j + 1])):
+            off[p] = tot
+            tot += int(blk_size[rowidx[p]]) * int(blk_size[j])
+    return off, tot
+
+
+def build_problem(nx, ny, nz, sizes_fn, *, complex_=False, seed=0, topology="faces",
+                  backend="numpy", device="cpu", name="") -> Problem:
+    """Build the auxiliary matrix of a grid DD model (recipe in the module doc).
+
+    sizes_fn(n_interfaces, rng) -> int array of interface sizes.
+    backend "numpy" draws with default_rng(seed); "torch" with a torch.Generator
+    on `device` (values then produced on that device and copied to host numpy).
+    """
+    rng = np.random.default_rng(seed)
+    if topology == "faces":
+        pairs = grid_interfaces(nx, ny, nz)
+    else:
+        pairs = unstructured_interfaces(nx, ny, nz, rng)
+    nblk = len(pairs)
+    blk_size = np.asarray(sizes_fn(nblk, rng), dtype=np.int64)
+    nsub = nx * ny * nz
+    touch: List[List[int]] = [[] for _ in range(nsub)]
+    for I, (p, q) in enumerate(pairs):
+        touch[p].append(I)
+        touch[q].append(I)
+    cliques = [(p, sorted(touch[p])) for p in range(nsub) if touch[p]]
+    colptr, rowidx = block_pattern_from_cliques(nblk, [c for _, c in cliques])
+    val_offset, total = _layout(blk_size, colptr, rowidx)
+    dtype = np.complex128 if complex_ else np.float64
+    values = np.zeros(total, dtype=dtype)
+    pos = {}
+    for j in range(nblk):
+        for p in range(int(colptr[j]), int(colptr[j + 1])):
+            pos[(int(rowidx[p]), j)] = p
+
+    sigma = (0.1 + 0.05j) if complex_ else 0.1
+    if backend == "torch":
+        import torch
+        gen = torch.Generator(device=device)
+        gen.manual_seed(seed)
+        tdt = torch.complex128 if complex_ else torch.float64
+    for p_sub, members in cliques:
+        m = int(sum(blk_size[I] for I in members))
+        if backend == "numpy":
+            G = rng.standard_normal((m, m))
+            if complex_:
+                G = G + 1j * rng.standard_normal((m, m))
+            sign = 2.0 * rng.integers(0, 2, m) - 1.0
+            mag = rng.uniform(0.5, 2.0, m)
+            d = sign * mag
+            if complex_:
+                d = d + 1j * rng.uniform(0.0, 0.1, m)
+            S = G.T @ (d[:, None] * G)
+            S = S + sigma * np.eye(m)
+            S = 0.5 * (S + S.T)
+        else:
+            import torch
+            G = torch.randn(m, m, generator=gen, device=device, dtype=torch.float64)
+            if complex_:
+                G = torch.complex(G, torch.randn(m, m, generator=gen, device=device, dtype=torch.float64))
+            sign = 2.0 * torch.randint(0, 2, (m,), generator=gen, device=device).double() - 1.0
+            mag = 0.5 + 1.5 * torch.rand(m, generator=gen, device=device, dtype=torch.float64)
+            d = (sign * mag).to(tdt)
+            if complex_:
+                d = d + 1j * (0.1 * torch.rand(m, generator=gen, device=device, dtype=torch.float64))
+            S = G.transpose(0, 1) @ (d[:, None] * G)
+            S = S + sigma * torch.eye(m, dtype=tdt, device=device)
+            S = 0.5 * (S + S.transpose(0, 1))
+            S = S.cpu().numpy()
+        offs = np.concatenate([[0], np.cumsum([blk_size[I] for I in members])])
+        for a, I in enumerate(members):
+            for b, J in enumerate(members):
+                if I < J:
+                    continue
+                blk = S[offs[a]:offs[a + 1], offs[b]:offs[b + 1]]
+                pp = pos[(I, J)]
+                si, sj = int(blk_size[I]), int(blk_size[J])
+                dst = values[val_offset[pp]:val_offset[pp] + si * sj].reshape(sj, si).T
+                dst += blk
+    return Problem(blk_size, colptr, rowidx, values, val_offset, cliques, name)
+
+
+def random_rhs(n: int, nrhs: int, complex_: bool, seed: int) -> np.ndarray:
+    """N(0,1) right-hand sides, (n, nrhs) Fortran-ordered (column-major)."""
+    rng = np.random.default_rng([seed, 7919])
+    B = rng.standard_normal((n, nrhs))
+    if complex_:
+        B = B + 1j * rng.standard_normal((n, nrhs))
+    return np.asfortranarray(B)
+
+
+def dense_expand(prob: Problem) -> np.ndarray:
+    """The full symmetric n x n matrix the blocks define (A^T = A, no conjugation).
+
+    Only the lower triangle of each diagonal block is used, as the C ABI states.
+    """
+    n = prob.n
+    off = prob.dof_offset
+    A = np.zeros((n, n), dtype=prob.values.dtype)
+    for (i, j), blk in prob.blocks().items():
+        if i == j:
+            lo = np.tril(blk)
+            A[off[i]:off[i + 1], off[j]:off[j + 1]] = lo + np.tril(blk, -1).T
+        else:
+            A[off[i]:off[i + 1], off[j]:off[j + 1]] = blk
+            A[off[j]:off[j + 1], off[i]:off[i + 1]] = blk.T
+    return A
+
+
+# --------------------------------------------------------------------------- configs
+def _const(s):
+    return lambda n, rng: np.full(n, s, dtype=np.int64)
+
+
+def _uniform(lo, hi):
+    return lambda n, rng: rng.integers(lo, hi + 1, n)
+
+
+# name -> (grid, sizes, complex, topology, nrhs, order)   (BASELINE.json configs[i])
+CONFIGS = {
+    "cfg0": dict(grid=(2, 2, 1), sizes=_const(32), complex_=False, topology="faces", nrhs=4, order="auto"),
+    "cfg1": dict(grid=(4, 4, 4), sizes=_const(256), complex_=False, topology="faces", nrhs=64, order="nd"),
+    "cfg2": dict(grid=(6, 6, 6), sizes=_uniform(128, 1024), complex_=False, topology="unstructured", nrhs=256,
+                 order="auto"),
+    "cfg3": dict(grid=(8, 8, 4), sizes=_const(512), complex_=True, topology="faces", nrhs=1000, order="auto"),
+    "cfg3alt": dict(grid=(3, 6, 10), sizes=_const(512), complex_=True, topology="faces", nrhs=1000, order="auto"),
+    "cfg4": dict(grid=(8, 8, 4), sizes=_const(512), complex_=True, topology="faces", nrhs=1000, order="auto",
+                 batches=10),
+}
+
+
+def config(name: str, *, seed: int = 0, backend: str = "numpy", device: str = "cpu",
+           grid: Optional[Tuple[int, int, int]] = None, sizes=None) -> Problem:
+    """Problem for a named BASELINE config; `grid`/`sizes` override for scaled-down variants."""
+    c = CONFIGS[name]
+    g = grid or c["grid"]
+    sz = c["sizes"] if sizes is None else (sizes if callable(sizes) else _const(int(sizes)))
+    return build_problem(*g, sz, complex_=c["complex_"], seed=seed, topology=c["topology"],
+                         backend=backend, device=device, name=name)
