@@ -1,0 +1,162 @@
+/*
+ * dd_aux.h -- C ABI of the B200-native auxiliary-matrix solver (arXiv:2002.05019).
+ *
+ * The operation (§II APPROACH): the auxiliary (interface / dual-DoF)
+ * matrix A of the direct domain-decomposition method is "symmetric ... block-wise
+ * sparse (sparse collection of dense blocks)"; it "is LDL^T factorized via a very
+ * fast symbolic factorization step [on the] attributed clique graph of the
+ * block-wise sparse matrix, followed by a custom block LDL^T with restricted
+ * Bunch-Kaufman pivoting [BUNCH1977]"; the factored auxiliary problem is then solved
+ * for many excitations ("forward/backward substitution ... for
+ * 200 excitations").  The three calls follow the north_star (BASELINE.json):
+ *   dd_aux_analyze  block pattern + interface sizes -> clique-graph symbolic
+ *                   factorization, elimination tree, block storage layout (host only)
+ *   dd_aux_factor   block values -> P A P^T = L D L^T on the GPU
+ *   dd_aux_solve    nrhs right-hand sides -> X = A^{-1} B on the GPU
+ * Readings of the paper (restricted pivoting domain, CABS1, tie rule, explicit L,
+ * refinement, norms) are listed in DESIGN.md "Readings" (L1-L16).
+ *
+ * Scalars: DD_REAL64 = IEEE binary64; DD_COMPLEX128 = (re, im) binary64 pairs,
+ * complex SYMMETRIC (A^T = A, never conjugated anywhere).
+ *
+ * Memory ownership: the handle owns host symbolic data only.  Every device buffer
+ * (values, factor, workspace, right-hand sides) is allocated and owned by the
+ * caller (PyTorch in this repo); the library never calls cudaMalloc/cudaFree.
+ * Pointers named d_* are DEVICE pointers, all others HOST pointers.  Streams are
+ * passed as an opaque `void*` holding a cudaStream_t (NULL = legacy default stream).
+ *
+ * Errors: 0 = DD_OK.  -k = argument k invalid (LAPACK style, 1-based position).
+ * DD_ZERO_PIVOT (+1): factorization completed but D is singular; a later solve
+ * returns DD_ERR_SINGULAR.  Negative DD_ERR_* codes below.  dd_aux_last_error()
+ * returns a thread-local message for the last failing call.  Handles are not
+ * thread-safe; separate handles are independent.
+ */
+#ifndef DD_AUX_H
+#define DD_AUX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dd_aux_handle_s* dd_aux_handle_t;
+
+enum { DD_REAL64 = 0, DD_COMPLEX128 = 1 };
+
+/* Block elimination orders.  AUTO = the lower-flop of ND and MINDEG (reading L8). */
+enum { DD_ORDER_AUTO = 0, DD_ORDER_ND = 1, DD_ORDER_MINDEG = 2, DD_ORDER_NATURAL = 3, DD_ORDER_USER = 4 };
+
+enum {
+  DD_OK = 0,
+  DD_ZERO_PIVOT = 1,
+  DD_ERR_CUDA = -100,          /* message carries the cudaError_t string                 */
+  DD_ERR_WORKSPACE = -101,     /* a buffer size argument is smaller than required        */
+  DD_ERR_NOT_FACTORED = -102,  /* dd_aux_solve before a successful dd_aux_factor         */
+  DD_ERR_SINGULAR = -103,      /* solve with a factor that reported DD_ZERO_PIVOT        */
+  DD_ERR_PATTERN = -104,       /* invalid block pattern (message says which rule)        */
+  DD_ERR_INTERNAL = -105
+};
+
+typedef struct {
+  int32_t order;              /* DD_ORDER_*                                               */
+  const int32_t* user_order;  /* [nblk] block elimination order for DD_ORDER_USER (copied) */
+  int32_t refine_steps;       /* iterative-refinement steps in dd_aux_solve (default 1, L7) */
+  int32_t use_graphs;         /* reserved (CUDA-graph capture of the level loop), default 0 */
+  int32_t reserved[4];
+} dd_aux_options;
+
+typedef struct {
+  int64_t n, nblk, nnzb_in, nnzb_filled, n_levels, max_front; /* max_front = max_k s_k + r_k */
+  int64_t max_level_width;                                    /* max nodes in one level       */
+  double flops_factor;          /* algorithmic: mu*sum_k(s^3/3 + r s^2 + r^2 s), mu=4 complex */
+  double flops_solve_per_rhs;   /* mu*2*sum_k(s^2 + 2 r s)                                     */
+  double factor_value_bytes;    /* sum_k (s^2 + r s) * scalar bytes           */
+  size_t factor_bytes;          /* size of d_factor                                            */
+  size_t work_bytes;            /* size of d_work for dd_aux_factor                            */
+  int32_t dtype, order_used;
+} dd_aux_info;
+
+typedef struct {
+  int64_t npos, nneg, nzero;    /* inertia from D (real only; complex: all zero)  (a6)        */
+  int64_t n2x2, nswaps;         /* 2x2 pivots, symmetric interchanges                          */
+  int64_t first_zero_pivot;     /* 0, or 1 + ORIGINAL global DoF index of the first zero pivot */
+  float ms_load, ms_factor;     /* device time of the load and factor phases (CUDA events)     */
+} dd_aux_factor_info;
+
+/* Default options: AUTO order, 1 refinement step. */
+void dd_aux_default_options(dd_aux_options* opt);
+
+/* Host-only symbolic phase ("very fast symbolic factorization step").
+ *  nblk        number of interfaces (blocks), > 0
+ *  blk_size    [nblk] interface sizes s_I > 0
+ *  colptr      [nblk+1] block-CSC column pointers of the LOWER block pattern
+ *  rowidx      [colptr[nblk]] row block ids: sorted ascending per column, >= column,
+ *              diagonal block present (first), no duplicates
+ *  dtype       DD_REAL64 or DD_COMPLEX128
+ *  opt         options (NULL = defaults); user_order is copied
+ *  out         receives the new handle
+ * All arrays are read during the call only.  Returns DD_ERR_PATTERN on an invalid
+ * pattern (dd_aux_last_error names the rule). */
+int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr, const int32_t* rowidx,
+                   int32_t dtype, const dd_aux_options* opt, dd_aux_handle_t* out);
+
+int dd_aux_get_info(dd_aux_handle_t h, dd_aux_info* info);
+
+/* order[t] = original block id eliminated at position t (host out, [nblk]). */
+int dd_aux_get_order(dd_aux_handle_t h, int32_t* order);
+
+/* Elimination tree by ORIGINAL block id: parent[k] (-1 = root) and level[k] (height, leaves 0);
+ * either pointer may be NULL.  nnz_struct (if non-NULL) receives sum_k |struct(k)|. */
+int dd_aux_get_etree(dd_aux_handle_t h, int32_t* parent, int32_t* level, int64_t* nnz_struct);
+
+/* Bytes of d_work needed by dd_aux_solve for nrhs right-hand sides. */
+int dd_aux_solve_work_bytes(dd_aux_handle_t h, int64_t nrhs, size_t* bytes);
+
+/* Numeric factorization on the GPU.
+ *  d_vals      device; all input blocks concatenated; block p (CSC position) is column-major
+ *              s_row x s_col with leading dimension s_row at element offset val_offset[p];
+ *              complex values interleaved (re, im) like torch.complex128.  Diagonal blocks are
+ *              passed full, only their lower triangle is read.  Never written.  Must stay alive
+ *              and unchanged while dd_aux_solve may refine (it re-reads A for the residual).
+ *  val_offset  host [nnzb_in] element (not byte) offsets; copied into the handle
+ *  d_factor    device, info.factor_bytes, 256-byte aligned; holds L, D, pivots and the
+ *              device descriptor tables; must not be modified between factor and solve
+ *  d_work      device, info.work_bytes, 256-byte aligned; scratch, free after return
+ *  stream      cudaStream_t (as void*); the call enqueues all work on it and synchronizes it
+ *              once at exit to return finfo
+ *  finfo       host out (may be NULL)
+ * Returns DD_OK, DD_ZERO_PIVOT, or an error. */
+int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offset, void* d_factor,
+                  void* d_work, void* stream, dd_aux_factor_info* finfo);
+
+/* Multi-RHS solve X = A^{-1} B (forward L, D^{-1}, backward L^T) plus refine_steps steps of
+ * iterative refinement r = b - A x, x += solve(r) against the ORIGINAL blocks d_vals.
+ *  d_vals      the same buffer passed to dd_aux_factor (may be NULL iff refine_steps == 0)
+ *  nrhs        >= 0 (0 is a no-op)
+ *  d_B         device, n x nrhs column-major, leading dimension ldb >= n, ORIGINAL DoF order
+ *              (DoF = sum_{I'<I} s_I' + local); overwritten by X (like LAPACK ?sytrs)
+ *  d_work      device, dd_aux_solve_work_bytes(nrhs) bytes
+ *  stream      enqueued asynchronously on this stream (no host synchronization) */
+int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, int64_t nrhs, void* d_B,
+                 int64_t ldb, void* d_work, void* stream);
+
+/* Diagnostics (synchronizes): per-position pivots of the factored diagonal blocks, host out.
+ *  ipiv  [n] LAPACK convention, 1-based LOCAL to each block: ipiv = kp+1 (1x1) or -(kp+1) twice (2x2)
+ *  perm  [n] composite in-block permutation, local 0-based: (P_k A_kk P_k^T)[a,b] = A_kk[perm[a], perm[b]]
+ *  d, e  [n] diagonal and 2x2 sub-diagonal of D (scalar type of the handle; e = 0 off 2x2 firsts)
+ * Entries are grouped by elimination position (block order[0] first).  Any pointer may be NULL. */
+int dd_aux_get_pivots(dd_aux_handle_t h, const void* d_factor, int32_t* ipiv, int32_t* perm, void* d, void* e);
+
+int dd_aux_destroy(dd_aux_handle_t h);
+
+const char* dd_aux_last_error(void);
+
+/* Library version string. */
+const char* dd_aux_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DD_AUX_H */

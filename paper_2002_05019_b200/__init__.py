@@ -1,0 +1,283 @@
+"""B200-native auxiliary-matrix solver of arXiv:2002.05019 -- thin Python binding.
+
+The product is the C-ABI library ``libdd_aux.so`` (include/dd_aux.h): hand-written
+sm_100a CUDA kernels for the restricted-Bunch-Kaufman block LDL^T of the
+block-sparse auxiliary matrix (§II) and its multi-RHS solve.  This
+module only marshals arguments to it (same function names as the C ABI); PyTorch
+supplies device memory and streams.  There is no CPU fallback: importing this
+package on a machine without the built library raises ImportError, and every
+compute call needs CUDA device buffers.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+__all__ = ["DD_REAL64", "DD_COMPLEX128", "DD_ORDER_AUTO", "DD_ORDER_ND", "DD_ORDER_MINDEG", "DD_ORDER_NATURAL",
+           "DD_ORDER_USER", "DD_OK", "DD_ZERO_PIVOT", "DDAuxError", "dd_aux_default_options", "dd_aux_analyze",
+           "dd_aux_get_info", "dd_aux_get_order", "dd_aux_get_etree", "dd_aux_solve_work_bytes", "dd_aux_factor",
+           "dd_aux_solve", "dd_aux_get_pivots", "dd_aux_destroy", "dd_aux_last_error", "dd_aux_version",
+           "AuxSolver", "LIB_PATH", "EXPORTED_SYMBOLS"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdd_aux.so")
+
+DD_REAL64, DD_COMPLEX128 = 0, 1
+DD_ORDER_AUTO, DD_ORDER_ND, DD_ORDER_MINDEG, DD_ORDER_NATURAL, DD_ORDER_USER = 0, 1, 2, 3, 4
+DD_OK, DD_ZERO_PIVOT = 0, 1
+DD_ERR_CUDA, DD_ERR_WORKSPACE, DD_ERR_NOT_FACTORED, DD_ERR_SINGULAR, DD_ERR_PATTERN = -100, -101, -102, -103, -104
+
+EXPORTED_SYMBOLS = ["dd_aux_default_options", "dd_aux_analyze", "dd_aux_get_info", "dd_aux_get_order",
+                    "dd_aux_get_etree", "dd_aux_solve_work_bytes", "dd_aux_factor", "dd_aux_solve",
+                    "dd_aux_get_pivots", "dd_aux_destroy", "dd_aux_last_error", "dd_aux_version"]
+
+
+class DDAuxError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"dd_aux error {code}: {msg}")
+        self.code = code
+
+
+class dd_aux_options(ctypes.Structure):
+    _fields_ = [("order", ctypes.c_int32), ("user_order", ctypes.POINTER(ctypes.c_int32)),
+                ("refine_steps", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+
+
+class dd_aux_info(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("nblk", ctypes.c_int64), ("nnzb_in", ctypes.c_int64),
+                ("nnzb_filled", ctypes.c_int64), ("n_levels", ctypes.c_int64), ("max_front", ctypes.c_int64),
+                ("max_level_width", ctypes.c_int64), ("flops_factor", ctypes.c_double),
+                ("flops_solve_per_rhs", ctypes.c_double), ("factor_value_bytes", ctypes.c_double),
+                ("factor_bytes", ctypes.c_size_t), ("work_bytes", ctypes.c_size_t), ("dtype", ctypes.c_int32),
+                ("order_used", ctypes.c_int32)]
+
+
+class dd_aux_factor_info(ctypes.Structure):
+    _fields_ = [("npos", ctypes.c_int64), ("nneg", ctypes.c_int64), ("nzero", ctypes.c_int64),
+                ("n2x2", ctypes.c_int64), ("nswaps", ctypes.c_int64), ("first_zero_pivot", ctypes.c_int64),
+                ("ms_load", ctypes.c_float), ("ms_factor", ctypes.c_float)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    i64, i32 = ctypes.c_int64, ctypes.c_int32
+    pi64 = ctypes.POINTER(ctypes.c_int64)
+    pi32 = ctypes.POINTER(ctypes.c_int32)
+    sig = {
+        "dd_aux_default_options": (None, [ctypes.POINTER(dd_aux_options)]),
+        "dd_aux_analyze": (ctypes.c_int, [i64, pi64, pi64, pi32, i32, ctypes.POINTER(dd_aux_options), ctypes.POINTER(P)]),
+        "dd_aux_get_info": (ctypes.c_int, [P, ctypes.POINTER(dd_aux_info)]),
+        "dd_aux_get_order": (ctypes.c_int, [P, pi32]),
+        "dd_aux_get_etree": (ctypes.c_int, [P, pi32, pi32, pi64]),
+        "dd_aux_solve_work_bytes": (ctypes.c_int, [P, i64, ctypes.POINTER(ctypes.c_size_t)]),
+        "dd_aux_factor": (ctypes.c_int, [P, P, pi64, P, P, P, ctypes.POINTER(dd_aux_factor_info)]),
+        "dd_aux_solve": (ctypes.c_int, [P, P, P, i64, P, i64, P, P]),
+        "dd_aux_get_pivots": (ctypes.c_int, [P, P, pi32, pi32, P, P]),
+        "dd_aux_destroy": (ctypes.c_int, [P]),
+        "dd_aux_last_error": (ctypes.c_char_p, []),
+        "dd_aux_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def _np_ptr(a, ctype):
+    return a.ctypes.data_as(ctypes.POINTER(ctype))
+
+
+def _check(rc, allow=(DD_OK,)):
+    if rc not in allow:
+        raise DDAuxError(rc, dd_aux_last_error())
+    return rc
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(int(getattr(stream, "cuda_stream", stream)))
+
+
+def _dev_ptr(t):
+    if t is None:
+        return None
+    if not getattr(t, "is_cuda", False):
+        raise ValueError("device buffers must be CUDA tensors (there is no CPU path)")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def dd_aux_last_error() -> str:
+    return _lib.dd_aux_last_error().decode()
+
+
+def dd_aux_version() -> str:
+    return _lib.dd_aux_version().decode()
+
+
+def dd_aux_default_options(order=DD_ORDER_AUTO, refine_steps=1, user_order=None) -> dd_aux_options:
+    o = dd_aux_options()
+    _lib.dd_aux_default_options(ctypes.byref(o))
+    o.order = int(order)
+    o.refine_steps = int(refine_steps)
+    if user_order is not None:
+        uo = np.ascontiguousarray(user_order, dtype=np.int32)
+        o._user_order_keepalive = uo
+        o.user_order = _np_ptr(uo, ctypes.c_int32)
+        o.order = DD_ORDER_USER
+    return o
+
+
+def dd_aux_analyze(blk_size, colptr, rowidx, dtype=DD_REAL64, opt: Optional[dd_aux_options] = None):
+    bs = np.ascontiguousarray(blk_size, dtype=np.int64)
+    cp = np.ascontiguousarray(colptr, dtype=np.int64)
+    ri = np.ascontiguousarray(rowidx, dtype=np.int32)
+    h = ctypes.c_void_p()
+    rc = _lib.dd_aux_analyze(len(bs), _np_ptr(bs, ctypes.c_int64), _np_ptr(cp, ctypes.c_int64),
+                             _np_ptr(ri, ctypes.c_int32), int(dtype), ctypes.byref(opt) if opt is not None else None,
+                             ctypes.byref(h))
+    _check(rc)
+    return h
+
+
+def dd_aux_get_info(h) -> dict:
+    info = dd_aux_info()
+    _check(_lib.dd_aux_get_info(h, ctypes.byref(info)))
+    return {f: getattr(info, f) for f, _ in dd_aux_info._fields_}
+
+
+def dd_aux_get_order(h) -> np.ndarray:
+    n = dd_aux_get_info(h)["nblk"]
+    out = np.empty(n, dtype=np.int32)
+    _check(_lib.dd_aux_get_order(h, _np_ptr(out, ctypes.c_int32)))
+    return out
+
+
+def dd_aux_get_etree(h):
+    n = dd_aux_get_info(h)["nblk"]
+    parent = np.empty(n, dtype=np.int32)
+    level = np.empty(n, dtype=np.int32)
+    nnz = ctypes.c_int64()
+    _check(_lib.dd_aux_get_etree(h, _np_ptr(parent, ctypes.c_int32), _np_ptr(level, ctypes.c_int32),
+                                 ctypes.byref(nnz)))
+    return parent, level, int(nnz.value)
+
+
+def dd_aux_solve_work_bytes(h, nrhs: int) -> int:
+    b = ctypes.c_size_t()
+    _check(_lib.dd_aux_solve_work_bytes(h, int(nrhs), ctypes.byref(b)))
+    return int(b.value)
+
+
+def dd_aux_factor(h, d_vals, val_offset, d_factor, d_work, stream=None):
+    """Returns (rc, finfo dict); rc is DD_OK or DD_ZERO_PIVOT, errors raise DDAuxError."""
+    vo = np.ascontiguousarray(val_offset, dtype=np.int64)
+    fi = dd_aux_factor_info()
+    rc = _lib.dd_aux_factor(h, _dev_ptr(d_vals), _np_ptr(vo, ctypes.c_int64), _dev_ptr(d_factor), _dev_ptr(d_work),
+                            _stream_ptr(stream), ctypes.byref(fi))
+    _check(rc, allow=(DD_OK, DD_ZERO_PIVOT))
+    return rc, {f: getattr(fi, f) for f, _ in dd_aux_factor_info._fields_}
+
+
+def dd_aux_solve(h, d_factor, d_vals, d_B, d_work, stream=None, nrhs=None, ldb=None):
+    """d_B: (n, nrhs) column-major CUDA tensor (stride (1, ldb)); overwritten by X."""
+    if nrhs is None:
+        nrhs = d_B.shape[1] if d_B.dim() == 2 else 1
+    if ldb is None:
+        ldb = d_B.stride(1) if d_B.dim() == 2 and d_B.shape[1] > 1 else d_B.shape[0]
+        if d_B.dim() == 2 and d_B.shape[1] > 1 and d_B.stride(0) != 1:
+            raise ValueError("d_B must be column-major (stride(0) == 1)")
+    rc = _lib.dd_aux_solve(h, _dev_ptr(d_factor), _dev_ptr(d_vals), int(nrhs), _dev_ptr(d_B), int(ldb),
+                           _dev_ptr(d_work), _stream_ptr(stream))
+    return _check(rc)
+
+
+def dd_aux_get_pivots(h, d_factor, cplx=False) -> dict:
+    n = dd_aux_get_info(h)["n"]
+    ipiv = np.empty(n, dtype=np.int32)
+    perm = np.empty(n, dtype=np.int32)
+    dt = np.complex128 if cplx else np.float64
+    d = np.empty(n, dtype=dt)
+    e = np.empty(n, dtype=dt)
+    _check(_lib.dd_aux_get_pivots(h, _dev_ptr(d_factor), _np_ptr(ipiv, ctypes.c_int32), _np_ptr(perm, ctypes.c_int32),
+                                  ctypes.c_void_p(d.ctypes.data), ctypes.c_void_p(e.ctypes.data)))
+    return dict(ipiv=ipiv, perm=perm, d=d, e=e)
+
+
+def dd_aux_destroy(h):
+    if h:
+        _lib.dd_aux_destroy(h)
+
+
+class AuxSolver:
+    """Convenience owner of one handle plus its torch-allocated device buffers.
+
+    Marshalling only: analyze -> allocate factor/work with torch -> dd_aux_factor ->
+    dd_aux_solve.  Buffers are uint8 CUDA tensors sized by dd_aux_get_info.
+    """
+
+    def __init__(self, blk_size, colptr, rowidx, complex_=False, order=DD_ORDER_AUTO, refine_steps=1,
+                 user_order=None, device="cuda"):
+        import torch
+        self.torch = torch
+        self.cplx = bool(complex_)
+        self.opt = dd_aux_default_options(order, refine_steps, user_order)
+        self.h = dd_aux_analyze(blk_size, colptr, rowidx, DD_COMPLEX128 if self.cplx else DD_REAL64, self.opt)
+        self.info = dd_aux_get_info(self.h)
+        self.device = device
+        self.factor_buf = None
+        self.work = None
+        self.vals = None
+        self.finfo = None
+
+    @property
+    def n(self):
+        return self.info["n"]
+
+    def order(self):
+        return dd_aux_get_order(self.h)
+
+    def _work(self, nbytes):
+        if self.work is None or self.work.numel() < nbytes:
+            self.work = self.torch.empty(max(nbytes, 256), dtype=self.torch.uint8, device=self.device)
+        return self.work
+
+    def factor(self, d_vals, val_offset, stream=None):
+        torch = self.torch
+        if self.factor_buf is None:
+            self.factor_buf = torch.empty(self.info["factor_bytes"], dtype=torch.uint8, device=self.device)
+        w = self._work(self.info["work_bytes"])
+        self.vals = d_vals
+        rc, self.finfo = dd_aux_factor(self.h, d_vals, val_offset, self.factor_buf, w, stream)
+        return rc, self.finfo
+
+    def solve_(self, d_B, stream=None):
+        """In-place solve of a column-major (n, nrhs) CUDA tensor."""
+        nrhs = d_B.shape[1] if d_B.dim() == 2 else 1
+        w = self._work(dd_aux_solve_work_bytes(self.h, nrhs))
+        dd_aux_solve(self.h, self.factor_buf, self.vals, d_B, w, stream)
+        return d_B
+
+    def pivots(self):
+        return dd_aux_get_pivots(self.h, self.factor_buf, self.cplx)
+
+    def close(self):
+        if self.h:
+            dd_aux_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

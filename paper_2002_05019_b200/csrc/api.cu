@@ -1,0 +1,811 @@
+// C ABI (include/dd_aux.h): host driver of the B200 auxiliary-matrix solver.
+//
+// dd_aux_analyze builds, on the host, everything integer about the factorization
+// ("very fast symbolic factorization step"): the block elimination order,
+// the clique-completion fill, the elimination tree and its levels, the HBM layout of
+// the factor and every per-level descriptor table the kernels consume.  dd_aux_factor
+// and dd_aux_solve only upload tables and enqueue kernels level by level (SURVEY.md
+// §8(a) a5: "Per level, in order: K1 -> K2 -> K3, stream order as the only barrier").
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/dd_aux.h"
+#include "analyze.hpp"
+#include "launch.hpp"
+
+using namespace ddaux;
+using namespace ddk;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                        \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) return fail(DD_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define LAUNCH_CHECK(what)                                                                 \
+  do {                                                                                     \
+    cudaError_t e_ = cudaGetLastError();                                                   \
+    if (e_ != cudaSuccess) return fail(DD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Blob {  // host image of the device table region
+  std::vector<uint8_t> data;
+  template <class T>
+  size_t put(const std::vector<T>& v) {
+    size_t off = align256(data.size());
+    data.resize(off + v.size() * sizeof(T));
+    if (!v.empty()) std::memcpy(data.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+  }
+};
+
+struct LevelRanges {
+  int n0, n1;     // level nodes
+  int s0, s1;     // K2 strips
+  int r0, r1;     // rowperm entries
+  int t0, t1;     // K3 tiles
+  int f0, f1;     // forward-solve tiles
+  int b0, b1;     // backward-solve tiles
+};
+
+}  // namespace
+
+struct dd_aux_handle_s {
+  int dtype = DD_REAL64;
+  bool cplx = false;
+  dd_aux_options opt{};
+  Graph g;
+  Symbolic S;
+  std::vector<int64_t> blk_size, colptr, odof_blk;
+  std::vector<int32_t> rowidx;
+  int64_t n = 0, n_pad = 0, nnzb_in = 0;
+  int order_used = 0;
+  // layout
+  std::vector<NodeDev> nodes;
+  int64_t nA = 0;            // arena elements per plane
+  int64_t d_off = 0, e_off = 0;
+  int64_t nW = 0, nK1 = 0;   // level workspace elements per plane
+  int max_s = 0;
+  // tables
+  Blob blob;
+  size_t off_nodes = 0, off_stpos = 0, off_strow = 0, off_lvlnodes = 0, off_strips = 0, off_rowperm = 0,
+         off_targets = 0, off_contribs = 0, off_tiles = 0, off_ftargets = 0, off_fcontribs = 0, off_btiles = 0,
+         off_sprows = 0, off_blksize = 0, off_odof = 0;
+  size_t off_spsegs = 0;       // SpSeg table (filled at factor time)
+  std::vector<SpSeg> spsegs;   // voff holds the CSC position until factor
+  int n_sprows = 0;
+  std::vector<LevelRanges> lv;
+  // factor buffer offsets (bytes)
+  size_t tables_bytes = 0, off_arena = 0, off_ipiv = 0, off_perm = 0, off_gperm = 0, off_ginv = 0, off_stats = 0,
+         off_totals = 0, factor_bytes = 0;
+  // work buffer offsets (bytes)
+  size_t w_off_W = 0, w_off_K1 = 0, w_off_load = 0, work_bytes = 0;
+  // info
+  double flops_factor = 0, flops_solve = 0, value_bytes = 0;
+  int64_t max_front = 0, max_width = 0;
+  bool factored = false, singular = false;
+  const void* factored_ptr = nullptr;
+};
+
+extern "C" {
+
+void dd_aux_default_options(dd_aux_options* opt) {
+  if (!opt) return;
+  std::memset(opt, 0, sizeof(*opt));
+  opt->order = DD_ORDER_AUTO;
+  opt->refine_steps = 1;
+}
+
+const char* dd_aux_last_error(void) { return g_err.c_str(); }
+const char* dd_aux_version(void) { return "dd_aux 0.1 (sm_100a, FP64 DMMA)"; }
+
+int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr, const int32_t* rowidx,
+                   int32_t dtype, const dd_aux_options* opt_in, dd_aux_handle_t* out) {
+  if (nblk <= 0) return fail(-1, "nblk must be > 0");
+  if (!blk_size) return fail(-2, "blk_size is NULL");
+  if (!colptr) return fail(-3, "colptr is NULL");
+  if (!rowidx) return fail(-4, "rowidx is NULL");
+  if (dtype != DD_REAL64 && dtype != DD_COMPLEX128) return fail(-5, "dtype must be DD_REAL64 or DD_COMPLEX128");
+  if (!out) return fail(-7, "out is NULL");
+  std::string msg = validate_pattern(nblk, blk_size, colptr, rowidx);
+  if (!msg.empty()) return fail(DD_ERR_PATTERN, msg);
+  dd_aux_options opt;
+  dd_aux_default_options(&opt);
+  if (opt_in) opt = *opt_in;
+  if (opt.order < DD_ORDER_AUTO || opt.order > DD_ORDER_USER) return fail(-6, "invalid order option");
+  if (opt.refine_steps < 0) return fail(-6, "refine_steps must be >= 0");
+
+  dd_aux_handle_s* h = new (std::nothrow) dd_aux_handle_s();
+  if (!h) return fail(DD_ERR_INTERNAL, "out of host memory");
+  h->dtype = dtype;
+  h->cplx = dtype == DD_COMPLEX128;
+  h->opt = opt;
+  h->opt.user_order = nullptr;
+  h->blk_size.assign(blk_size, blk_size + nblk);
+  h->colptr.assign(colptr, colptr + nblk + 1);
+  h->rowidx.assign(rowidx, rowidx + colptr[nblk]);
+  h->nnzb_in = colptr[nblk];
+  h->g = graph_from_pattern(nblk, blk_size, colptr, rowidx);
+  const int N = (int)nblk;
+  h->odof_blk.assign(N + 1, 0);
+  for (int i = 0; i < N; ++i) h->odof_blk[i + 1] = h->odof_blk[i] + blk_size[i];
+  h->n = h->odof_blk[N];
+
+  // ---------------------------------------------------------------- ordering (reading L8)
+  std::vector<int> order;
+  if (opt.order == DD_ORDER_USER) {
+    if (!opt.user_order) {
+      delete h;
+      return fail(-6, "DD_ORDER_USER needs user_order");
+    }
+    order.assign(opt.user_order, opt.user_order + N);
+    std::vector<char> seen(N, 0);
+    for (int v : order) {
+      if (v < 0 || v >= N || seen[v]) {
+        delete h;
+        return fail(-6, "user_order is not a permutation");
+      }
+      seen[v] = 1;
+    }
+    h->order_used = DD_ORDER_USER;
+  } else if (opt.order == DD_ORDER_NATURAL) {
+    order.resize(N);
+    for (int i = 0; i < N; ++i) order[i] = i;
+    h->order_used = DD_ORDER_NATURAL;
+  } else if (opt.order == DD_ORDER_MINDEG) {
+    order = order_mindeg(h->g);
+    h->order_used = DD_ORDER_MINDEG;
+  } else if (opt.order == DD_ORDER_ND) {
+    order = order_nd(h->g);
+    h->order_used = DD_ORDER_ND;
+  } else {
+    auto md = order_mindeg(h->g);
+    auto nd = order_nd(h->g);
+    if (order_flops(h->g, nd) < order_flops(h->g, md)) {
+      order = nd;
+      h->order_used = DD_ORDER_ND;
+    } else {
+      order = md;
+      h->order_used = DD_ORDER_MINDEG;
+    }
+  }
+  h->S = symbolic_from_order(h->g, order);
+  const Symbolic& S = h->S;
+
+  // ---------------------------------------------------------------- layout
+  const int64_t mu = h->cplx ? 4 : 1;
+  h->flops_factor = mu * S.flops_factor;
+  h->flops_solve = mu * S.flops_solve;
+  h->nodes.resize(N);
+  std::vector<int32_t> st_pos, st_row;
+  int64_t ydof = 0, panel_off = 0;
+  for (int t = 0; t < N; ++t) {
+    NodeDev& nd = h->nodes[t];
+    const int blk = S.order[t];
+    nd.blk = blk;
+    nd.s = (int32_t)blk_size[blk];
+    nd.sp = (int32_t)pad2(nd.s);
+    nd.st0 = (int32_t)st_pos.size();
+    nd.nst = (int32_t)S.st[t].size();
+    int64_t ro = nd.sp, r = 0;
+    for (int u : S.st[t]) {
+      st_pos.push_back(u);
+      st_row.push_back((int32_t)ro);
+      int64_t su = blk_size[S.order[u]];
+      ro += pad2(su);
+      r += su;
+    }
+    nd.rp = (int32_t)(ro - nd.sp);
+    nd.ld = (int32_t)pad8(ro);
+    nd.ldw = (int32_t)pad8(std::max<int64_t>(nd.rp, 2));
+    nd.panel = panel_off;
+    panel_off += (int64_t)nd.ld * nd.s;
+    nd.ydof = ydof;
+    ydof += nd.sp;
+    nd.odof = h->odof_blk[blk];
+    h->max_front = std::max<int64_t>(h->max_front, nd.s + r);
+    h->max_s = std::max(h->max_s, nd.s);
+    h->value_bytes += (double)(nd.s * (int64_t)nd.s + r * nd.s) * (h->cplx ? 16.0 : 8.0);
+  }
+  h->n_pad = ydof;
+  int64_t off = panel_off;
+  for (int t = 0; t < N; ++t) {
+    NodeDev& nd = h->nodes[t];
+    nd.linv = off;
+    off += (int64_t)((nd.s + TB - 1) / TB) * TB * TB;
+  }
+  h->d_off = off;
+  off += pad8(h->n_pad);
+  h->e_off = off;
+  off += pad8(h->n_pad);
+  h->nA = (off + 31) & ~int64_t(31);
+  // level workspace (W panels and K1 scratch) -- reused by every level
+  for (int l = 0; l < S.nlevels; ++l) {
+    int64_t w = 0, k1 = 0;
+    for (int t : S.level_nodes[l]) {
+      NodeDev& nd = h->nodes[t];
+      nd.w = w;
+      w += (int64_t)nd.ldw * nd.s;
+      nd.k1w = k1;
+      k1 += (int64_t)nd.sp * K1NB;
+    }
+    h->nW = std::max(h->nW, w);
+    h->nK1 = std::max(h->nK1, k1);
+    h->max_width = std::max<int64_t>(h->max_width, (int64_t)S.level_nodes[l].size());
+  }
+  h->nW = (h->nW + 31) & ~int64_t(31);
+  h->nK1 = (h->nK1 + 31) & ~int64_t(31);
+
+  // ---------------------------------------------------------------- per-level tables
+  auto row_in_panel = [&](int j, int i) -> int {  // row offset of block at position i inside panel j
+    if (i == j) return 0;
+    const NodeDev& nj = h->nodes[j];
+    auto b = st_pos.begin() + nj.st0, e = b + nj.nst;
+    auto it = std::lower_bound(b, e, i);
+    return st_row[it - st_pos.begin()];
+  };
+  // reverse index: for node t, the earlier panels k with t in struct(k)
+  std::vector<std::vector<std::pair<int, int>>> appears(N);
+  for (int k = 0; k < N; ++k)
+    for (int q = 0; q < h->nodes[k].nst; ++q) appears[st_pos[h->nodes[k].st0 + q]].push_back({k, st_row[h->nodes[k].st0 + q]});
+
+  std::vector<int32_t> lvl_nodes;
+  std::vector<Strip> strips;
+  std::vector<RowPerm> rowperm;
+  std::vector<UpdTarget> targets;
+  std::vector<UpdContrib> contribs;
+  std::vector<Tile> tiles;
+  std::vector<SolveTarget> ftargets;
+  std::vector<SolveContrib> fcontribs;
+  std::vector<int2> btiles;
+  const int BM3 = k3_bm(h->cplx), BN3 = k3_bn(h->cplx), SBM = solve_bm(h->cplx);
+  const int K2BM = 64;
+  for (int l = 0; l < S.nlevels; ++l) {
+    LevelRanges R{};
+    const auto& L = S.level_nodes[l];
+    R.n0 = (int)lvl_nodes.size();
+    for (int t : L) lvl_nodes.push_back(t);
+    R.n1 = (int)lvl_nodes.size();
+    R.s0 = (int)strips.size();
+    for (int t : L) {
+      const NodeDev& nd = h->nodes[t];
+      for (int r0 = 0; r0 < nd.rp; r0 += K2BM) strips.push_back(Strip{t, r0, std::min(K2BM, nd.rp - r0), 0});
+    }
+    R.s1 = (int)strips.size();
+    R.r0 = (int)rowperm.size();
+    for (int t : L)
+      for (auto& kr : appears[t]) rowperm.push_back(RowPerm{t, kr.first, kr.second, 0});
+    R.r1 = (int)rowperm.size();
+    // K3 targets: (i, j) in struct(k)^2, i at/after j, contributors in ascending position
+    std::unordered_map<int64_t, int> tmap;
+    std::vector<std::vector<UpdContrib>> tcon;
+    std::vector<std::pair<int, int>> tij;
+    for (int k : L) {
+      const NodeDev& nk = h->nodes[k];
+      for (int a = 0; a < nk.nst; ++a)
+        for (int b = 0; b <= a; ++b) {
+          int i = st_pos[nk.st0 + a], j = st_pos[nk.st0 + b];
+          int64_t key = (int64_t)i * N + j;
+          auto it = tmap.find(key);
+          int id;
+          if (it == tmap.end()) {
+            id = (int)tij.size();
+            tmap.emplace(key, id);
+            tij.push_back({i, j});
+            tcon.push_back({});
+          } else {
+            id = it->second;
+          }
+          tcon[id].push_back(UpdContrib{k, st_row[nk.st0 + a] - nk.sp, st_row[nk.st0 + b], 0});
+        }
+    }
+    R.t0 = (int)tiles.size();
+    std::vector<std::pair<int64_t, Tile>> ltiles;
+    for (size_t id = 0; id < tij.size(); ++id) {
+      int i = tij[id].first, j = tij[id].second;
+      UpdTarget tg{};
+      tg.j = j;
+      tg.ro = row_in_panel(j, i);
+      tg.M = h->nodes[i].s;
+      tg.N = h->nodes[j].s;
+      tg.c0 = (int)contribs.size();
+      int64_t kcost = 0;
+      for (auto& c : tcon[id]) {
+        contribs.push_back(c);
+        kcost += h->nodes[c.k].s;
+      }
+      tg.c1 = (int)contribs.size();
+      tg.diag = (i == j);
+      int tid = (int)targets.size();
+      targets.push_back(tg);
+      for (int tm = 0; tm * BM3 < tg.M; ++tm)
+        for (int tn = 0; tn * BN3 < tg.N; ++tn) {
+          if (tg.diag && tn * BN3 > tm * BM3 + BM3 - 1) continue;
+          ltiles.push_back({kcost, Tile{tid, tm, tn, 0}});
+        }
+    }
+    std::stable_sort(ltiles.begin(), ltiles.end(), [](auto& x, auto& y) { return x.first > y.first; });
+    for (auto& x : ltiles) tiles.push_back(x.second);
+    R.t1 = (int)tiles.size();
+    // forward-solve targets: y_i -= L_ik z_k over the level's contributors
+    std::unordered_map<int, std::vector<SolveContrib>> fmap;
+    std::vector<int> fo;
+    for (int k : L) {
+      const NodeDev& nk = h->nodes[k];
+      for (int a = 0; a < nk.nst; ++a) {
+        int i = st_pos[nk.st0 + a];
+        if (!fmap.count(i)) fo.push_back(i);
+        fmap[i].push_back(SolveContrib{k, st_row[nk.st0 + a]});
+      }
+    }
+    R.f0 = (int)ftargets.size();
+    for (int i : fo) {
+      int c0 = (int)fcontribs.size();
+      for (auto& c : fmap[i]) fcontribs.push_back(c);
+      int c1 = (int)fcontribs.size();
+      for (int tm = 0; tm * SBM < h->nodes[i].s; ++tm) ftargets.push_back(SolveTarget{i, tm, c0, c1});
+    }
+    R.f1 = (int)ftargets.size();
+    R.b0 = (int)btiles.size();
+    for (int t : L)
+      if (h->nodes[t].nst > 0)
+        for (int tm = 0; tm * SBM < h->nodes[t].s; ++tm) btiles.push_back(make_int2(t, tm));
+    R.b1 = (int)btiles.size();
+    h->lv.push_back(R);
+  }
+  // K6 residual rows: block row I of the full symmetric A
+  std::vector<std::vector<SpSeg>> rowsegs(N);
+  for (int j = 0; j < N; ++j)
+    for (int64_t p = colptr[j]; p < colptr[j + 1]; ++p) {
+      int i = rowidx[p];
+      if (i == j) rowsegs[i].push_back(SpSeg{p, j, 2});
+      else {
+        rowsegs[i].push_back(SpSeg{p, j, 0});  // stored (i, j)
+        rowsegs[j].push_back(SpSeg{p, i, 1});  // (j, i) = stored^T
+      }
+    }
+  std::vector<SpRow> sprows;
+  const int SPM = spmv_bm();
+  for (int I = 0; I < N; ++I) {
+    std::sort(rowsegs[I].begin(), rowsegs[I].end(), [](const SpSeg& a, const SpSeg& b) { return a.J < b.J; });
+    int c0 = (int)h->spsegs.size();
+    for (auto& sg : rowsegs[I]) h->spsegs.push_back(sg);
+    int c1 = (int)h->spsegs.size();
+    for (int tm = 0; tm * SPM < blk_size[I]; ++tm) sprows.push_back(SpRow{I, tm, c0, c1});
+  }
+  h->n_sprows = (int)sprows.size();
+
+  Blob& B = h->blob;
+  h->off_nodes = B.put(h->nodes);
+  h->off_stpos = B.put(st_pos);
+  h->off_strow = B.put(st_row);
+  h->off_lvlnodes = B.put(lvl_nodes);
+  h->off_strips = B.put(strips);
+  h->off_rowperm = B.put(rowperm);
+  h->off_targets = B.put(targets);
+  h->off_contribs = B.put(contribs);
+  h->off_tiles = B.put(tiles);
+  h->off_ftargets = B.put(ftargets);
+  h->off_fcontribs = B.put(fcontribs);
+  h->off_btiles = B.put(btiles);
+  h->off_sprows = B.put(sprows);
+  h->off_blksize = B.put(h->blk_size);
+  std::vector<int64_t> odof(h->odof_blk.begin(), h->odof_blk.end() - 1);
+  h->off_odof = B.put(odof);
+  h->off_spsegs = B.put(h->spsegs);
+  h->tables_bytes = align256(B.data.size());
+
+  // ---------------------------------------------------------------- buffer sizes
+  const int planes = h->cplx ? 2 : 1;
+  size_t o = h->tables_bytes;
+  h->off_arena = o;
+  o = align256(o + (size_t)h->nA * planes * sizeof(double));
+  h->off_ipiv = o;
+  o = align256(o + (size_t)h->n_pad * 4);
+  h->off_perm = o;
+  o = align256(o + (size_t)h->n_pad * 4);
+  h->off_gperm = o;
+  o = align256(o + (size_t)h->n_pad * 4);
+  h->off_ginv = o;
+  o = align256(o + (size_t)h->n * 4);
+  h->off_stats = o;
+  o = align256(o + (size_t)N * 8 * 8);
+  h->off_totals = o;
+  o = align256(o + 16 * 8);
+  h->factor_bytes = o;
+  size_t w = 0;
+  h->w_off_W = w;
+  w = align256(w + (size_t)h->nW * planes * sizeof(double));
+  h->w_off_K1 = w;
+  w = align256(w + (size_t)h->nK1 * planes * sizeof(double));
+  h->w_off_load = w;
+  w = align256(w + (size_t)h->nnzb_in * sizeof(LoadBlock));
+  h->work_bytes = w;
+  *out = h;
+  return DD_OK;
+}
+
+int dd_aux_get_info(dd_aux_handle_t h, dd_aux_info* info) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (!info) return fail(-2, "info is NULL");
+  std::memset(info, 0, sizeof(*info));
+  info->n = h->n;
+  info->nblk = h->S.nblk;
+  info->nnzb_in = h->nnzb_in;
+  info->nnzb_filled = h->S.nblk + h->S.nnz_struct;
+  info->n_levels = h->S.nlevels;
+  info->max_front = h->max_front;
+  info->max_level_width = h->max_width;
+  info->flops_factor = h->flops_factor;
+  info->flops_solve_per_rhs = h->flops_solve;
+  info->factor_value_bytes = h->value_bytes;
+  info->factor_bytes = h->factor_bytes;
+  info->work_bytes = h->work_bytes;
+  info->dtype = h->dtype;
+  info->order_used = h->order_used;
+  return DD_OK;
+}
+
+int dd_aux_get_order(dd_aux_handle_t h, int32_t* order) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (!order) return fail(-2, "order is NULL");
+  for (int t = 0; t < h->S.nblk; ++t) order[t] = h->S.order[t];
+  return DD_OK;
+}
+
+int dd_aux_get_etree(dd_aux_handle_t h, int32_t* parent, int32_t* level, int64_t* nnz_struct) {
+  if (!h) return fail(-1, "handle is NULL");
+  for (int t = 0; t < h->S.nblk; ++t) {
+    int blk = h->S.order[t];
+    if (parent) parent[blk] = h->S.parent[t] < 0 ? -1 : h->S.order[h->S.parent[t]];
+    if (level) level[blk] = h->S.level[t];
+  }
+  if (nnz_struct) *nnz_struct = h->S.nnz_struct;
+  return DD_OK;
+}
+
+int dd_aux_solve_work_bytes(dd_aux_handle_t h, int64_t nrhs, size_t* bytes) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (nrhs < 0) return fail(-2, "nrhs must be >= 0");
+  if (!bytes) return fail(-3, "bytes is NULL");
+  const int planes = h->cplx ? 2 : 1;
+  const size_t ldy = (size_t)pad8(h->n_pad);
+  size_t w = align256(ldy * (size_t)nrhs * planes * sizeof(double));   // y
+  w += align256((size_t)h->n * (size_t)nrhs * planes * sizeof(double));  // saved B (refinement)
+  *bytes = w;
+  return DD_OK;
+}
+
+int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offset, void* d_factor, void* d_work,
+                  void* stream, dd_aux_factor_info* finfo) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (!d_vals) return fail(-2, "d_vals is NULL");
+  if (!val_offset) return fail(-3, "val_offset is NULL");
+  if (!d_factor || ((uintptr_t)d_factor & 255)) return fail(-4, "d_factor is NULL or not 256-byte aligned");
+  if (!d_work || ((uintptr_t)d_work & 255)) return fail(-5, "d_work is NULL or not 256-byte aligned");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool C = h->cplx;
+  const int N = h->S.nblk;
+  uint8_t* F = (uint8_t*)d_factor;
+  uint8_t* Wb = (uint8_t*)d_work;
+  h->factored = false;
+
+  // ---- tables: fill the value offsets of the K6 segments, upload everything
+  {
+    SpSeg* sp = (SpSeg*)(h->blob.data.data() + h->off_spsegs);
+    for (size_t q = 0; q < h->spsegs.size(); ++q) sp[q].voff = val_offset[h->spsegs[q].voff];
+  }
+  CUDA_TRY(cudaMemcpyAsync(F, h->blob.data.data(), h->blob.data.size(), cudaMemcpyHostToDevice, st));
+  // ---- K0 load list
+  std::vector<LoadBlock> lbs;
+  lbs.reserve(h->nnzb_in);
+  int64_t max_elems = 0;
+  for (int j = 0; j < N; ++j)
+    for (int64_t p = h->colptr[j]; p < h->colptr[j + 1]; ++p) {
+      int i = h->rowidx[p];
+      int pi = h->S.pos[i], pj = h->S.pos[j];
+      LoadBlock L{};
+      L.voff = val_offset[p];
+      L.rows = (int32_t)h->blk_size[i];
+      L.cols = (int32_t)h->blk_size[j];
+      L.diag = (i == j);
+      if (pi >= pj) {  // stored (i,j) in panel pj at the rows of i
+        const NodeDev& nj = h->nodes[pj];
+        int ro = 0;
+        if (i != j) {
+          auto b = h->S.st[pj].begin();
+          auto it = std::lower_bound(b, h->S.st[pj].end(), pi);
+          const int32_t* strow = (const int32_t*)(h->blob.data.data() + h->off_strow);
+          ro = strow[nj.st0 + (it - b)];
+        }
+        L.dst = nj.panel + ro;
+        L.ld = nj.ld;
+        L.trans = 0;
+      } else {  // i eliminated first: block (j, i) = stored^T lives in panel pi at the rows of j
+        const NodeDev& ni = h->nodes[pi];
+        auto b = h->S.st[pi].begin();
+        auto it = std::lower_bound(b, h->S.st[pi].end(), pj);
+        const int32_t* strow = (const int32_t*)(h->blob.data.data() + h->off_strow);
+        L.dst = ni.panel + strow[ni.st0 + (it - b)];
+        L.ld = ni.ld;
+        L.trans = 1;
+      }
+      max_elems = std::max<int64_t>(max_elems, (int64_t)L.rows * L.cols);
+      lbs.push_back(L);
+    }
+  CUDA_TRY(cudaMemcpyAsync(Wb + h->w_off_load, lbs.data(), lbs.size() * sizeof(LoadBlock), cudaMemcpyHostToDevice, st));
+
+  double* arena = (double*)(F + h->off_arena);
+  const int64_t aim = C ? h->nA : 0;
+  double* work = (double*)Wb;
+  const int64_t wim = C ? h->nW : 0;
+  double* k1work = (double*)(Wb + h->w_off_K1);
+  const int64_t k1im = C ? h->nK1 : 0;
+  const NodeDev* dnodes = (const NodeDev*)(F + h->off_nodes);
+
+  cudaEvent_t e0, e1, e2;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreate(&e2);
+  cudaEventRecord(e0, st);
+  // ---- a1: zero the arena, load the caller's blocks
+  CUDA_TRY(cudaMemsetAsync(arena, 0, (size_t)h->nA * (C ? 2 : 1) * sizeof(double), st));
+  launch_load(C, (const double*)d_vals, (const LoadBlock*)(Wb + h->w_off_load), (int)lbs.size(), max_elems, arena,
+              aim, st);
+  LAUNCH_CHECK("k0_load");
+  cudaEventRecord(e1, st);
+
+  K1Args k1{};
+  k1.nd = dnodes;
+  k1.arena = arena;
+  k1.aim = aim;
+  k1.work = k1work;
+  k1.wim = k1im;
+  k1.perm = (int*)(F + h->off_perm);
+  k1.ipiv = (int*)(F + h->off_ipiv);
+  k1.gperm = (int*)(F + h->off_gperm);
+  k1.ginv = (int*)(F + h->off_ginv);
+  k1.d_off = h->d_off;
+  k1.e_off = h->e_off;
+  k1.stats = (int64_t*)(F + h->off_stats);
+  CUDA_TRY(cudaMemsetAsync(k1.ipiv, 0, (size_t)h->n_pad * 4, st));
+  RowpermArgs rp{(const RowPerm*)(F + h->off_rowperm), dnodes, arena, aim, k1.perm};
+  K2Args k2{(const Strip*)(F + h->off_strips), dnodes, arena, aim, work, wim, k1.perm, k1.ipiv, h->d_off, h->e_off};
+  K3Args k3{(const Tile*)(F + h->off_tiles), (const UpdTarget*)(F + h->off_targets),
+            (const UpdContrib*)(F + h->off_contribs), dnodes, arena, aim, work, wim};
+  const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
+  // ---- a2-a5: level-scheduled factorization
+  for (const LevelRanges& R : h->lv) {
+    k1.nodes = lvlnodes + R.n0;
+    launch_k1(C, k1, R.n1 - R.n0, st);
+    LAUNCH_CHECK("k1_diag_bk");
+    RowpermArgs r = rp;
+    r.list = rp.list + R.r0;
+    launch_rowperm(C, r, R.r1 - R.r0, h->max_s, st);
+    LAUNCH_CHECK("k_rowperm");
+    K2Args a2 = k2;
+    a2.strips = k2.strips + R.s0;
+    launch_k2(C, a2, R.s1 - R.s0, st);
+    LAUNCH_CHECK("k2_panel");
+    K3Args a3 = k3;
+    a3.tiles = k3.tiles + R.t0;
+    launch_k3(C, a3, R.t1 - R.t0, st);
+    LAUNCH_CHECK("k3_update");
+  }
+  // ---- a6: statistics
+  int64_t* totals_d = (int64_t*)(F + h->off_totals);
+  launch_k4((const int64_t*)(F + h->off_stats), N, totals_d, st);
+  LAUNCH_CHECK("k4_stats");
+  cudaEventRecord(e2, st);
+  int64_t totals[16] = {0};
+  CUDA_TRY(cudaMemcpyAsync(totals, totals_d, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  float ms_load = 0, ms_fac = 0;
+  cudaEventElapsedTime(&ms_load, e0, e1);
+  cudaEventElapsedTime(&ms_fac, e1, e2);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  if (finfo) {
+    finfo->npos = C ? 0 : totals[0];
+    finfo->nneg = C ? 0 : totals[1];
+    finfo->nzero = C ? 0 : totals[2];
+    finfo->n2x2 = totals[3];
+    finfo->nswaps = totals[4];
+    finfo->first_zero_pivot = totals[5];
+    finfo->ms_load = ms_load;
+    finfo->ms_factor = ms_fac;
+  }
+  h->factored = true;
+  h->factored_ptr = d_factor;
+  h->singular = totals[5] != 0;
+  return h->singular ? DD_ZERO_PIVOT : DD_OK;
+}
+
+static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t yim, int64_t ldy, int nrhs,
+                       cudaStream_t st) {
+  const bool C = h->cplx;
+  SolveArgs a{};
+  a.nd = (const NodeDev*)(F + h->off_nodes);
+  a.arena = (const double*)(F + h->off_arena);
+  a.aim = C ? h->nA : 0;
+  a.y = y;
+  a.yim = yim;
+  a.ldy = ldy;
+  a.nrhs = nrhs;
+  a.ftargets = (const SolveTarget*)(F + h->off_ftargets);
+  a.fcontribs = (const SolveContrib*)(F + h->off_fcontribs);
+  a.btiles = (const int2*)(F + h->off_btiles);
+  a.st_pos = (const int*)(F + h->off_stpos);
+  a.st_row = (const int*)(F + h->off_strow);
+  a.ipiv = (const int*)(F + h->off_ipiv);
+  a.d_off = h->d_off;
+  a.e_off = h->e_off;
+  a.nrows = h->n_pad;
+  const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
+  for (const LevelRanges& R : h->lv) {
+    SolveArgs b = a;
+    b.nodes = lvlnodes + R.n0;
+    launch_fdiag(C, b, R.n1 - R.n0, st);
+    LAUNCH_CHECK("k_fdiag");
+    b.ftargets = a.ftargets + R.f0;
+    launch_fupd(C, b, R.f1 - R.f0, st);
+    LAUNCH_CHECK("k_fupd");
+  }
+  launch_dsolve(C, a, st);
+  LAUNCH_CHECK("k_dsolve");
+  for (int l = (int)h->lv.size() - 1; l >= 0; --l) {
+    const LevelRanges& R = h->lv[l];
+    SolveArgs b = a;
+    b.btiles = a.btiles + R.b0;
+    launch_bupd(C, b, R.b1 - R.b0, st);
+    LAUNCH_CHECK("k_bupd");
+    b.nodes = lvlnodes + R.n0;
+    launch_bdiag(C, b, R.n1 - R.n0, st);
+    LAUNCH_CHECK("k_bdiag");
+  }
+  return DD_OK;
+}
+
+int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, int64_t nrhs, void* d_B, int64_t ldb,
+                 void* d_work, void* stream) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (!d_factor) return fail(-2, "d_factor is NULL");
+  if (nrhs < 0) return fail(-4, "nrhs must be >= 0");
+  if (nrhs == 0) return DD_OK;
+  if (!d_B) return fail(-5, "d_B is NULL");
+  if (ldb < h->n) return fail(-6, "ldb < n");
+  if (!d_work || ((uintptr_t)d_work & 255)) return fail(-7, "d_work is NULL or not 256-byte aligned");
+  if (!h->factored || h->factored_ptr != d_factor) return fail(DD_ERR_NOT_FACTORED, "d_factor holds no factorization of this handle");
+  if (h->singular) return fail(DD_ERR_SINGULAR, "the factorization reported a zero pivot");
+  const int refine = h->opt.refine_steps;
+  if (refine > 0 && !d_vals) return fail(-3, "d_vals is NULL but refine_steps > 0");
+  if (nrhs > (1 << 30)) return fail(-4, "nrhs too large");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool C = h->cplx;
+  const int planes = C ? 2 : 1;
+  const uint8_t* F = (const uint8_t*)d_factor;
+  uint8_t* Wb = (uint8_t*)d_work;
+  const int64_t ldy = pad8(h->n_pad);
+  double* y = (double*)Wb;
+  const int64_t yim = C ? ldy * nrhs : 0;
+  double* Bsave = (double*)(Wb + align256((size_t)ldy * nrhs * planes * sizeof(double)));
+
+  PermArgs pa{};
+  pa.gperm = (const int*)(F + h->off_gperm);
+  pa.nrows = h->n_pad;
+  pa.nrhs = (int)nrhs;
+  pa.y = y;
+  pa.yim = yim;
+  pa.ldy = ldy;
+  if (refine > 0) {
+    launch_copy(C, (const double*)d_B, ldb, Bsave, h->n, h->n, (int)nrhs, st);
+    LAUNCH_CHECK("k_copy");
+  }
+  pa.src = (const double*)d_B;
+  pa.lds = ldb;
+  launch_perm_in(C, pa, st);
+  LAUNCH_CHECK("k_perm_in");
+  int rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st);
+  if (rc) return rc;
+  pa.dst = (double*)d_B;
+  pa.ldd = ldb;
+  pa.accumulate = 0;
+  launch_perm_out(C, pa, st);
+  LAUNCH_CHECK("k_perm_out");
+  for (int r = 0; r < refine; ++r) {
+    SpmvArgs sa{};
+    sa.rows = (const SpRow*)(F + h->off_sprows);
+    sa.segs = (const SpSeg*)(F + h->off_spsegs);
+    sa.blk_size = (const int64_t*)(F + h->off_blksize);
+    sa.odof = (const int64_t*)(F + h->off_odof);
+    sa.vals = (const double*)d_vals;
+    sa.X = (const double*)d_B;
+    sa.ldx = ldb;
+    sa.Bsave = Bsave;
+    sa.ldb = h->n;
+    sa.ginv = (const int*)(F + h->off_ginv);
+    sa.y = y;
+    sa.yim = yim;
+    sa.ldy = ldy;
+    sa.nrhs = (int)nrhs;
+    launch_spmv(C, sa, h->n_sprows, st);
+    LAUNCH_CHECK("k_spmv");
+    rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st);
+    if (rc) return rc;
+    pa.accumulate = 1;
+    launch_perm_out(C, pa, st);
+    LAUNCH_CHECK("k_perm_out");
+  }
+  return DD_OK;
+}
+
+int dd_aux_get_pivots(dd_aux_handle_t h, const void* d_factor, int32_t* ipiv, int32_t* perm, void* d, void* e) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (!d_factor) return fail(-2, "d_factor is NULL");
+  if (!h->factored || h->factored_ptr != d_factor) return fail(DD_ERR_NOT_FACTORED, "not factored");
+  const uint8_t* F = (const uint8_t*)d_factor;
+  const int64_t np = h->n_pad;
+  std::vector<int32_t> ip(np), pm(np);
+  const bool C = h->cplx;
+  std::vector<double> dv(np * (C ? 2 : 1)), ev(np * (C ? 2 : 1));
+  CUDA_TRY(cudaMemcpy(ip.data(), F + h->off_ipiv, np * 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(pm.data(), F + h->off_perm, np * 4, cudaMemcpyDeviceToHost));
+  const double* arena = (const double*)(F + h->off_arena);
+  CUDA_TRY(cudaMemcpy(dv.data(), arena + h->d_off, np * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(ev.data(), arena + h->e_off, np * 8, cudaMemcpyDeviceToHost));
+  if (C) {
+    CUDA_TRY(cudaMemcpy(dv.data() + np, arena + h->nA + h->d_off, np * 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(ev.data() + np, arena + h->nA + h->e_off, np * 8, cudaMemcpyDeviceToHost));
+  }
+  int64_t q = 0;
+  for (int t = 0; t < h->S.nblk; ++t) {
+    const NodeDev& nd = h->nodes[t];
+    for (int m = 0; m < nd.s; ++m, ++q) {
+      int64_t g = nd.ydof + m;
+      if (ipiv) ipiv[q] = ip[g];
+      if (perm) perm[q] = pm[g];
+      if (d) {
+        if (C) {
+          ((double*)d)[2 * q] = dv[g];
+          ((double*)d)[2 * q + 1] = dv[np + g];
+        } else {
+          ((double*)d)[q] = dv[g];
+        }
+      }
+      if (e) {
+        if (C) {
+          ((double*)e)[2 * q] = ev[g];
+          ((double*)e)[2 * q + 1] = ev[np + g];
+        } else {
+          ((double*)e)[q] = ev[g];
+        }
+      }
+    }
+  }
+  return DD_OK;
+}
+
+int dd_aux_destroy(dd_aux_handle_t h) {
+  delete h;
+  return DD_OK;
+}
+
+}  // extern "C"

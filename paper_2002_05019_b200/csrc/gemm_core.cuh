@@ -1,0 +1,260 @@
+// FP64 tensor-core (DMMA) tile engine for sm_100a.
+//
+// On sm_100a the FP64 tensor path is reachable only through warp-level
+// mma.sync ... .f64 (tcgen05.mma has no f64 kind; wgmma is sm_90a-only), which
+// lowers to SASS DMMA.8x8x4.  This engine computes one BM x BN
+// output tile of   C (+)= sum_seg A_seg * B_seg   where the K dimension is the
+// concatenation of a list of segments ("gathered K", SURVEY.md §8(a) a4:
+// owner-computes target tiles summing all contributors of a level in a fixed
+// order -- deterministic, no atomics).  Operands are staged into shared memory by
+// cp.async (LDGSTS, 16-byte chunks, zero-filled outside the logical shape) in a
+// STAGES-deep pipeline and fed to mma.sync.m16n8k4.f64 from registers.
+//
+// Operand layouts (all column-major storage in HBM):
+//   A "MK": A(m,k) = a[m + col(k)*lda]   (m contiguous; optional column gather map)
+//   A "KM": A(m,k) = a[k + m*lda]        (k contiguous; i.e. a transposed view)
+//   B "NK": B(k,n) = b[n + k*ldb]        (n contiguous; B = L^T of a col-major L)
+//   B "KN": B(k,n) = b[k + n*ldb]        (k contiguous; a col-major K x N block)
+// Complex (complex symmetric, no conjugation) is planar: imaginary planes at a
+// fixed element offset; products use the 4M real formulation
+//   Cr += Ar Br - Ai Bi,  Ci += Ar Bi + Ai Br.
+// Alignment contract: every segment base, lda/ldb and row offsets are even
+// (16-byte aligned chunks); the library's layout guarantees it.
+#pragma once
+#include <cstdint>
+
+namespace ddk {
+
+struct Seg {
+  const double* a;   // A(0,0) (re plane)
+  const double* b;   // B(0,0) (re plane)
+  const int* acol;   // MK only: column gather map (k -> column), or nullptr
+  int64_t lda, ldb;
+  int K;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void dmma16x8x4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+__device__ __forceinline__ double dneg(double x) {  // sign flip on the integer pipe (keeps DMMA pipe free)
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ull);
+}
+
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool CPLX, bool A_KM, bool B_KN>
+struct Gemm {
+  static constexpr int NTHR = WARPS_M * WARPS_N * 32;
+  static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
+  static constexpr int MI = WTM / 16, NI = WTN / 8;
+  static constexpr int NPL = CPLX ? 2 : 1;
+  static constexpr int A_LD = A_KM ? (BK + 4) : (BM + 4);
+  static constexpr int A_TILE = A_KM ? BM * (BK + 4) : BK * (BM + 4);
+  static constexpr int B_LD = B_KN ? (BK + 4) : (BN + 4);
+  static constexpr int B_TILE = B_KN ? BN * (BK + 4) : BK * (BN + 4);
+  static constexpr int STAGE = NPL * (A_TILE + B_TILE);
+  static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE * sizeof(double);
+  static_assert(WTM % 16 == 0 && WTN % 8 == 0 && BK % 4 == 0, "tile shape");
+  static_assert((A_LD % 16) == 4 && (B_LD % 16) == 4, "bank-conflict-free padding");
+
+  struct Acc {
+    double r[MI][NI][4];
+    double i[CPLX ? MI : 1][CPLX ? NI : 1][4];
+  };
+
+  __device__ static void zero(Acc& acc) {
+#pragma unroll
+    for (int a = 0; a < MI; ++a)
+#pragma unroll
+      for (int b = 0; b < NI; ++b)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          acc.r[a][b][v] = 0.0;
+          if constexpr (CPLX) acc.i[a][b][v] = 0.0;
+        }
+  }
+
+  // Visit every accumulator element: f(row_in_tile, col_in_tile, re, im)
+  template <class F>
+  __device__ static void for_each(const Acc& acc, F f) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+    const int g = lane >> 2, tg = lane & 3;
+#pragma unroll
+    for (int a = 0; a < MI; ++a)
+#pragma unroll
+      for (int b = 0; b < NI; ++b)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          int row = wm * WTM + a * 16 + g + ((v >> 1) << 3);
+          int col = wn * WTN + b * 8 + 2 * tg + (v & 1);
+          f(row, col, acc.r[a][b][v], CPLX ? acc.i[CPLX ? a : 0][CPLX ? b : 0][v] : 0.0);
+        }
+  }
+
+  __device__ static void load_stage(double* st, const Seg& sg, int kofs, int m0, int n0, int M, int N,
+                                    int64_t aim, int64_t bim) {
+    double* As = st;
+    double* Bs = st + NPL * A_TILE;
+    const int tid = threadIdx.x;
+    // ---- A tile
+    if constexpr (!A_KM) {
+      constexpr int CH = BK * (BM / 2);
+#pragma unroll
+      for (int c = tid; c < CH; c += NTHR) {
+        int kk = c / (BM / 2), mm = (c % (BM / 2)) * 2;
+        int gm = m0 + mm, gk = kofs + kk;
+        int bytes = (gk < sg.K && gm < M) ? (gm + 1 < M ? 16 : 8) : 0;
+        const double* src = sg.a;
+        if (bytes) src = sg.a + gm + (int64_t)(sg.acol ? sg.acol[gk] : gk) * sg.lda;
+        cp_async16(As + kk * A_LD + mm, src, bytes);
+        if constexpr (CPLX) cp_async16(As + A_TILE + kk * A_LD + mm, bytes ? src + aim : src, bytes);
+      }
+    } else {
+      constexpr int CH = BM * (BK / 2);
+#pragma unroll
+      for (int c = tid; c < CH; c += NTHR) {
+        int mm = c / (BK / 2), kk = (c % (BK / 2)) * 2;
+        int gm = m0 + mm, gk = kofs + kk;
+        int bytes = (gk < sg.K && gm < M) ? (gk + 1 < sg.K ? 16 : 8) : 0;
+        const double* src = bytes ? sg.a + gk + (int64_t)gm * sg.lda : sg.a;
+        cp_async16(As + mm * A_LD + kk, src, bytes);
+        if constexpr (CPLX) cp_async16(As + A_TILE + mm * A_LD + kk, bytes ? src + aim : src, bytes);
+      }
+    }
+    // ---- B tile
+    if constexpr (!B_KN) {
+      constexpr int CH = BK * (BN / 2);
+#pragma unroll
+      for (int c = tid; c < CH; c += NTHR) {
+        int kk = c / (BN / 2), nn = (c % (BN / 2)) * 2;
+        int gn = n0 + nn, gk = kofs + kk;
+        int bytes = (gk < sg.K && gn < N) ? (gn + 1 < N ? 16 : 8) : 0;
+        const double* src = bytes ? sg.b + gn + (int64_t)gk * sg.ldb : sg.b;
+        cp_async16(Bs + kk * B_LD + nn, src, bytes);
+        if constexpr (CPLX) cp_async16(Bs + B_TILE + kk * B_LD + nn, bytes ? src + bim : src, bytes);
+      }
+    } else {
+      constexpr int CH = BN * (BK / 2);
+#pragma unroll
+      for (int c = tid; c < CH; c += NTHR) {
+        int nn = c / (BK / 2), kk = (c % (BK / 2)) * 2;
+        int gn = n0 + nn, gk = kofs + kk;
+        int bytes = (gk < sg.K && gn < N) ? (gk + 1 < sg.K ? 16 : 8) : 0;
+        const double* src = bytes ? sg.b + gk + (int64_t)gn * sg.ldb : sg.b;
+        cp_async16(Bs + nn * B_LD + kk, src, bytes);
+        if constexpr (CPLX) cp_async16(Bs + B_TILE + nn * B_LD + kk, bytes ? src + bim : src, bytes);
+      }
+    }
+  }
+
+  __device__ static void compute_stage(const double* st, Acc& acc) {
+    const double* As = st;
+    const double* Bs = st + NPL * A_TILE;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+    const int g = lane >> 2, tg = lane & 3;
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      const int k = ks * 4 + tg;
+      double ar[MI][2], br[NI];
+      double ai[CPLX ? MI : 1][2], bi[CPLX ? NI : 1];
+#pragma unroll
+      for (int a = 0; a < MI; ++a) {
+        int m = wm * WTM + a * 16 + g;
+        int o0 = A_KM ? (m * A_LD + k) : (k * A_LD + m);
+        int o1 = A_KM ? ((m + 8) * A_LD + k) : (k * A_LD + m + 8);
+        ar[a][0] = As[o0];
+        ar[a][1] = As[o1];
+        if constexpr (CPLX) {
+          ai[a][0] = As[A_TILE + o0];
+          ai[a][1] = As[A_TILE + o1];
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < NI; ++b) {
+        int n = wn * WTN + b * 8 + g;
+        int o = B_KN ? (n * B_LD + k) : (k * B_LD + n);
+        br[b] = Bs[o];
+        if constexpr (CPLX) bi[b] = Bs[B_TILE + o];
+      }
+#pragma unroll
+      for (int a = 0; a < MI; ++a)
+#pragma unroll
+        for (int b = 0; b < NI; ++b) {
+          dmma16x8x4(acc.r[a][b], ar[a][0], ar[a][1], br[b]);
+          if constexpr (CPLX) {
+            dmma16x8x4(acc.r[a][b], dneg(ai[a][0]), dneg(ai[a][1]), bi[b]);
+            dmma16x8x4(acc.i[a][b], ar[a][0], ar[a][1], bi[b]);
+            dmma16x8x4(acc.i[a][b], ai[a][0], ai[a][1], br[b]);
+          }
+        }
+    }
+  }
+
+  // Main loop over a segment list. SegFn: Seg(int idx). All threads of the CTA call this
+  // with identical arguments.  smem: STAGES*STAGE doubles.  Ends with a __syncthreads().
+  template <class SegFn>
+  __device__ static void run(SegFn segfn, int nseg, int m0, int n0, int M, int N, int64_t aim, int64_t bim,
+                             double* smem, Acc& acc) {
+    int pseg = 0, pk = 0;
+    Seg cur;
+    while (pseg < nseg) {  // skip empty segments
+      cur = segfn(pseg);
+      if (cur.K > 0) break;
+      ++pseg;
+    }
+    auto advance = [&]() {
+      pk += BK;
+      if (pk >= cur.K) {
+        pk = 0;
+        ++pseg;
+        while (pseg < nseg) {
+          cur = segfn(pseg);
+          if (cur.K > 0) break;
+          ++pseg;
+        }
+      }
+    };
+    int issued = 0;
+#pragma unroll 1
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (pseg < nseg) {
+        load_stage(smem + (issued % STAGES) * STAGE, cur, pk, m0, n0, M, N, aim, bim);
+        advance();
+        ++issued;
+      }
+      cp_async_commit();
+    }
+    int done = 0;
+#pragma unroll 1
+    while (done < issued) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      if (pseg < nseg) {
+        load_stage(smem + (issued % STAGES) * STAGE, cur, pk, m0, n0, M, N, aim, bim);
+        advance();
+        ++issued;
+      }
+      cp_async_commit();
+      compute_stage(smem + (done % STAGES) * STAGE, acc);
+      ++done;
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+};
+
+}  // namespace ddk

@@ -1,0 +1,646 @@
+// Factor-phase kernels (sm_100a).  PAPER.md:29 (§II): "custom block LDL^T with
+// restricted Bunch-Kaufman pivoting"; SURVEY.md §8(a) rows a1-a6.
+//
+//   k0_*        a1  load caller blocks into the zeroed panel arena (planar, position order)
+//   k1_diag_bk  a2  restricted BK LDL^T of each diagonal block of a level (one CTA per block),
+//                   blocked dlasyf-style: left-looking panel of K1NB columns with warp-shuffle
+//                   (value, index) pivot search, trailing update on DMMA; then the TB x TB
+//                   inverse diagonal tiles of L_kk used by every TRSM
+//   k_rowperm       apply P_t to the rows of block t inside earlier panels (explicit form, L5)
+//   k2_panel    a3  W = (A P^T) L^{-T} by row strips (blocked TRSM as DMMA GEMMs), L = W D^{-1}
+//   k3_update   a4  A_ij -= sum_k W_ik L_jk^T, owner-computes tiles with gathered K (DMMA)
+//   k4_stats    a6  inertia / pivot statistics reduction
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "gemm_core.cuh"
+#include "launch.hpp"
+
+using namespace ddaux;
+
+namespace ddk {
+
+// ============================================================================ K0 load
+// Copy input block (I,J) (caller layout, interleaved complex) into the arena block of the
+// panel of the earlier-eliminated of the two, transposing when I is eliminated first.
+template <bool C>
+__global__ void k0_load(const double* __restrict__ vals, const LoadBlock* __restrict__ lb, int nblocks,
+                        double* __restrict__ arena, int64_t aim) {
+  int b = blockIdx.y;
+  if (b >= nblocks) return;
+  LoadBlock L = lb[b];
+  const int64_t total = (int64_t)L.rows * L.cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e % L.rows, c = e / L.rows;  // source element (r, c) of the stored s_I x s_J block
+    if (L.diag && r < c) continue;            // diagonal blocks: lower triangle only
+    int64_t src = L.voff + e;
+    double re, im = 0.0;
+    if (C) {
+      re = vals[2 * src];
+      im = vals[2 * src + 1];
+    } else {
+      re = vals[src];
+    }
+    int64_t dst = L.trans ? (L.dst + c + r * L.ld) : (L.dst + r + c * L.ld);
+    arena[dst] = re;
+    if (C) arena[dst + aim] = im;
+  }
+}
+
+// ============================================================================ K1 diagonal BK
+constexpr int NT1 = 256;
+using K1GemmR = Gemm<64, 64, 16, 2, 4, 2, false, false, false>;
+using K1GemmC = Gemm<64, 64, 16, 2, 4, 2, true, false, false>;
+
+__device__ __forceinline__ void warp_argmax(double& v, int& i) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    if (v2 > v || (v2 == v && i2 < i)) {
+      v = v2;
+      i = i2;
+    }
+  }
+}
+
+// block-wide (max value, smallest index on ties): IDAMAX semantics (reading L3)
+__device__ __forceinline__ void block_argmax(double& v, int& i, double* shv, int* shi) {
+  warp_argmax(v, i);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    shv[w] = v;
+    shi[w] = i;
+  }
+  __syncthreads();
+  v = shv[0];
+  i = shi[0];
+#pragma unroll
+  for (int q = 1; q < NT1 / 32; ++q) {
+    double v2 = shv[q];
+    int i2 = shi[q];
+    if (v2 > v || (v2 == v && i2 < i)) {
+      v = v2;
+      i = i2;
+    }
+  }
+  __syncthreads();
+}
+
+template <bool C>
+__global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
+  using G = typename std::conditional<C, K1GemmC, K1GemmR>::type;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double shv[NT1 / 32];
+  __shared__ int shi[NT1 / 32];
+  __shared__ double wrow_r[K1NB], wrow_i[K1NB];
+  __shared__ int s_kp, s_kstep, s_zero, s_imax;
+  __shared__ double s_absakk, s_colmax;
+
+  const int t = a.nodes[blockIdx.x];
+  const NodeDev nd = a.nd[t];
+  const int s = nd.s;
+  const int64_t ldA = nd.ld;
+  double* A = a.arena + nd.panel;  // diagonal block = panel rows [0, s)
+  const int64_t aim = a.aim;
+  double* W = a.work + nd.k1w;     // s x K1NB scratch, ld = sp
+  const int64_t ldW = nd.sp;
+  const int64_t wim = a.wim;
+  int* perm = a.perm + nd.ydof;
+  int* ipiv = a.ipiv + nd.ydof;
+  double* dv_ = a.arena + a.d_off + nd.ydof;
+  double* ev_ = a.arena + a.e_off + nd.ydof;
+  const int tid = threadIdx.x;
+  const double alpha = (1.0 + sqrt(17.0)) / 8.0;
+
+  auto Ael = [&](int i, int j) { return (int64_t)i + (int64_t)j * ldA; };
+  auto Wel = [&](int i, int m) { return (int64_t)i + (int64_t)m * ldW; };
+
+  for (int i = tid; i < s; i += NT1) perm[i] = i;
+  int n2x2 = 0, nswap = 0, zero_col = -1;
+  __syncthreads();
+
+  int k = 0;
+  while (k < s) {
+    const int c0 = k;
+    const bool last_panel = (s - c0) <= K1NB;
+    // ------------------------------------------------------------ panel (left-looking)
+    while (k < s) {
+      const int kk = k - c0;
+      if (!last_panel && kk >= K1NB - 1) break;
+      // W(k, 0:kk) -> shared
+      for (int m = tid; m < kk; m += NT1) {
+        cz w = ld<C>(W, Wel(k, m), wim);
+        wrow_r[m] = w.r;
+        wrow_i[m] = w.i;
+      }
+      __syncthreads();
+      // updated column k:  W(k:s, kk) = A(k:s, k) - L(k:s, c0:k) W(k, 0:kk)^T
+      double bv = -1.0;
+      int bi = INT_MAX;
+      for (int i = k + tid; i < s; i += NT1) {
+        cz v = ld<C>(A, Ael(i, k), aim);
+        for (int m = 0; m < kk; ++m) v = fms<C>(v, ld<C>(A, Ael(i, c0 + m), aim), mk(wrow_r[m], wrow_i[m]));
+        st<C>(W, Wel(i, kk), wim, v);
+        double av = cabs1<C>(v);
+        if (i == k) s_absakk = av;
+        else if (av > bv) {
+          bv = av;
+          bi = i;
+        }
+      }
+      block_argmax(bv, bi, shv, shi);
+      // ---- pivot decision (Bunch-Kaufman, LAPACK xSYTF2 order)
+      const double absakk = s_absakk;
+      const double colmax = bv > 0.0 ? bv : 0.0;
+      const int imax = bi;
+      int kp, kstep = 1;
+      bool zero = false;
+      if (fmax(absakk, colmax) == 0.0) {
+        zero = true;
+        kp = k;
+      } else if (absakk >= alpha * colmax) {
+        kp = k;
+      } else {
+        // updated column imax -> W(:, kk+1) (symmetric access of the not-yet-updated trailing A)
+        for (int m = tid; m < kk; m += NT1) {
+          cz w = ld<C>(W, Wel(imax, m), wim);
+          wrow_r[m] = w.r;
+          wrow_i[m] = w.i;
+        }
+        __syncthreads();
+        double rv = -1.0;
+        int ri = INT_MAX;
+        for (int i = k + tid; i < s; i += NT1) {
+          cz v = (i < imax) ? ld<C>(A, Ael(imax, i), aim) : ld<C>(A, Ael(i, imax), aim);
+          for (int m = 0; m < kk; ++m) v = fms<C>(v, ld<C>(A, Ael(i, c0 + m), aim), mk(wrow_r[m], wrow_i[m]));
+          st<C>(W, Wel(i, kk + 1), wim, v);
+          if (i != imax) {
+            double av = cabs1<C>(v);
+            if (av > rv) {
+              rv = av;
+              ri = i;
+            }
+          }
+        }
+        block_argmax(rv, ri, shv, shi);
+        const double rowmax = rv;
+        if (absakk >= alpha * colmax * (colmax / rowmax)) {
+          kp = k;
+        } else {
+          __threadfence();
+          const double aii = cabs1<C>(ld<C>(W, Wel(imax, kk + 1), wim));
+          if (aii >= alpha * rowmax) {
+            kp = imax;
+            for (int i = k + tid; i < s; i += NT1) st<C>(W, Wel(i, kk), wim, ld<C>(W, Wel(i, kk + 1), wim));
+          } else {
+            kp = imax;
+            kstep = 2;
+          }
+        }
+      }
+      __syncthreads();
+      const int kkk = k + kstep - 1;
+      if (kp != kkk) {
+        // move the non-updated column kkk of the trailing block to position kp (dlasyf)
+        if (tid == 0) st<C>(A, Ael(kp, kp), aim, ld<C>(A, Ael(kkk, kkk), aim));
+        for (int j = kkk + 1 + tid; j < kp; j += NT1) st<C>(A, Ael(kp, j), aim, ld<C>(A, Ael(j, kkk), aim));
+        for (int j = kp + 1 + tid; j < s; j += NT1) st<C>(A, Ael(j, kp), aim, ld<C>(A, Ael(j, kkk), aim));
+        // explicit form (L5): interchange rows kkk, kp in every computed L column 0..k-1
+        for (int j = tid; j < k; j += NT1) {
+          cz x = ld<C>(A, Ael(kkk, j), aim), y = ld<C>(A, Ael(kp, j), aim);
+          st<C>(A, Ael(kkk, j), aim, y);
+          st<C>(A, Ael(kp, j), aim, x);
+        }
+        // rows kkk, kp of W columns 0..kk+kstep-1
+        for (int m = tid; m < kk + kstep; m += NT1) {
+          cz x = ld<C>(W, Wel(kkk, m), wim), y = ld<C>(W, Wel(kp, m), wim);
+          st<C>(W, Wel(kkk, m), wim, y);
+          st<C>(W, Wel(kp, m), wim, x);
+        }
+        if (tid == 0) {
+          int x = perm[kkk];
+          perm[kkk] = perm[kp];
+          perm[kp] = x;
+        }
+      }
+      __syncthreads();
+      // ---- store L and D
+      if (kstep == 1) {
+        const cz D = ld<C>(W, Wel(k, kk), wim);
+        for (int i = k + 1 + tid; i < s; i += NT1) {
+          cz w = ld<C>(W, Wel(i, kk), wim);
+          st<C>(A, Ael(i, k), aim, zero ? w : dv<C>(w, D));
+        }
+        if (tid == 0) {
+          st<C>(A, Ael(k, k), aim, D);
+          st<C>(dv_, 0 + k, aim, D);
+          st<C>(ev_, 0 + k, aim, mk(0.0, 0.0));
+          ipiv[k] = kp + 1;
+          if (zero && zero_col < 0) zero_col = k;
+          if (kp != k) ++nswap;
+        }
+      } else {
+        const cz w11 = ld<C>(W, Wel(k, kk), wim), w21 = ld<C>(W, Wel(k + 1, kk), wim),
+                 w22 = ld<C>(W, Wel(k + 1, kk + 1), wim);
+        // LAPACK dlasyf scaled closed form of [W_k W_k+1] D^{-1}
+        const cz d11 = dv<C>(w22, w21), d22 = dv<C>(w11, w21);
+        const cz tt = dv<C>(mk(1.0, 0.0), mul<C>(d11, d22) - mk(1.0, 0.0));
+        const cz d21 = dv<C>(tt, w21);
+        for (int i = k + 2 + tid; i < s; i += NT1) {
+          cz wk = ld<C>(W, Wel(i, kk), wim), wk1 = ld<C>(W, Wel(i, kk + 1), wim);
+          st<C>(A, Ael(i, k), aim, mul<C>(d21, mul<C>(d11, wk) - wk1));
+          st<C>(A, Ael(i, k + 1), aim, mul<C>(d21, mul<C>(d22, wk1) - wk));
+        }
+        if (tid == 0) {
+          st<C>(A, Ael(k, k), aim, w11);
+          st<C>(A, Ael(k + 1, k), aim, mk(0.0, 0.0));  // L is unit lower with an identity 2x2 block
+          st<C>(A, Ael(k + 1, k + 1), aim, w22);
+          st<C>(dv_, k, aim, w11);
+          st<C>(dv_, k + 1, aim, w22);
+          st<C>(ev_, k, aim, w21);
+          st<C>(ev_, k + 1, aim, mk(0.0, 0.0));
+          ipiv[k] = ipiv[k + 1] = -(kp + 1);
+          ++n2x2;
+          if (kp != k + 1) ++nswap;
+        }
+      }
+      __threadfence();
+      __syncthreads();
+      k += kstep;
+    }
+    // ------------------------------------------------------------ trailing update (DMMA)
+    if (k < s) {
+      // A(k:s, k:s) -= L(k:s, c0:k) W(k:s, 0:kb)^T.  The GEMM window starts at the even
+      // row ke <= k (16-byte aligned cp.async chunks); row/column ke < k is masked.
+      const int kb = k - c0, ke = k & ~1, M = s - ke;
+      __threadfence();
+      __syncthreads();
+      Seg sg;
+      sg.a = A + Ael(ke, c0);
+      sg.lda = ldA;
+      sg.b = W + ke;  // B(q, n) = W(ke + n, q)
+      sg.ldb = ldW;
+      sg.acol = nullptr;
+      sg.K = kb;
+      const int nt = (M + 63) / 64;
+      for (int tm = 0; tm < nt; ++tm)
+        for (int tn = 0; tn <= tm; ++tn) {
+          typename G::Acc acc;
+          G::zero(acc);
+          G::run([&](int) { return sg; }, 1, tm * 64, tn * 64, M, M, aim, wim, smem, acc);
+          double* Cb = A + Ael(ke + tm * 64, ke + tn * 64);
+          G::for_each(acc, [&](int r, int c, double vr, double vi) {
+            const int gr = ke + tm * 64 + r, gc = ke + tn * 64 + c;
+            if (gr < s && gc < s && gr >= k && gc >= k) {
+              int64_t e = (int64_t)r + (int64_t)c * ldA;
+              Cb[e] -= vr;
+              if (C) Cb[e + aim] -= vi;
+            }
+          });
+        }
+      __threadfence();
+      __syncthreads();
+    }
+  }
+
+  // ---------------------------------------------------------------- inverse diagonal tiles of L
+  {
+    const int ntiles = (s + TB - 1) / TB;
+    const int warp = tid >> 5, lane = tid & 31;
+    double* Lr = smem + warp * (2 * TB * TB);  // per-warp staging (re, im)
+    double* Li = Lr + TB * TB;
+    double* Vb = a.arena + nd.linv;
+    for (int p = warp; p < ntiles; p += NT1 / 32) {
+      const int r0 = p * TB, w = min(TB, s - r0);
+      for (int e = lane; e < TB * TB; e += 32) {
+        int i = e % TB, j = e / TB;
+        cz v = (i < w && j < w && i > j) ? ld<C>(A, Ael(r0 + i, r0 + j), aim) : mk(0.0, 0.0);
+        Lr[e] = v.r;
+        Li[e] = v.i;
+      }
+      __syncwarp();
+      // lane j computes column j of L_pp^{-1}: x_i = delta_ij - sum_{m<i} L(i,m) x_m
+      cz x[TB];
+#pragma unroll
+      for (int i = 0; i < TB; ++i) {
+        cz v = mk(i == lane ? 1.0 : 0.0, 0.0);
+#pragma unroll
+        for (int m = 0; m < i; ++m) v = fms<C>(v, mk(Lr[i + m * TB], Li[i + m * TB]), x[m]);
+        x[i] = (i < lane) ? mk(0.0, 0.0) : v;
+      }
+#pragma unroll
+      for (int i = 0; i < TB; ++i) st<C>(Vb, (int64_t)p * TB * TB + i + (int64_t)lane * TB, aim, x[i]);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // ---------------------------------------------------------------- global permutation maps + stats
+  for (int m = tid; m < nd.sp; m += NT1) {
+    if (m < s) {
+      int o = (int)(nd.odof + perm[m]);
+      a.gperm[nd.ydof + m] = o;
+      a.ginv[o] = (int)(nd.ydof + m);
+    } else {
+      a.gperm[nd.ydof + m] = -1;
+    }
+  }
+  if (tid == 0) {
+    int64_t np = 0, nn = 0, nz = 0;
+    if (!C) {
+      int q = 0;
+      while (q < s) {
+        if (ipiv[q] < 0) {
+          double x = dv_[q], y = ev_[q], z = dv_[q + 1];
+          double det = x * z - y * y;
+          if (det < 0) {
+            ++np;
+            ++nn;
+          } else if (det > 0) {
+            if (x + z > 0) np += 2;
+            else nn += 2;
+          } else {
+            ++nz;
+            if (x + z > 0) ++np;
+            else if (x + z < 0) ++nn;
+            else ++nz;
+          }
+          q += 2;
+        } else {
+          double x = dv_[q];
+          if (x > 0) ++np;
+          else if (x < 0) ++nn;
+          else ++nz;
+          ++q;
+        }
+      }
+    }
+    int64_t* S = a.stats + (int64_t)t * 8;
+    S[0] = np;
+    S[1] = nn;
+    S[2] = nz;
+    S[3] = n2x2;
+    S[4] = nswap;
+    S[5] = zero_col >= 0 ? nd.odof + perm[zero_col] + 1 : 0;
+    S[6] = 0;
+    S[7] = 0;
+  }
+}
+
+// ============================================================================ row permutation
+// rows [ro, ro + s_t) of panel k are block t's rows of L_tk; reorder them by perm_t.
+template <bool C>
+__global__ void k_rowperm(RowpermArgs a) {
+  const RowPerm R = a.list[blockIdx.y];
+  const NodeDev nt = a.nd[R.t];
+  const NodeDev nk = a.nd[R.k];
+  const int s = nt.s;
+  const int* perm = a.perm + nt.ydof;
+  extern __shared__ __align__(16) double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* br = sm + (size_t)warp * 2 * s;
+  double* bi = br + s;
+  for (int c = blockIdx.x * nw + warp; c < nk.s; c += gridDim.x * nw) {
+    double* col = a.arena + nk.panel + R.ro + (int64_t)c * nk.ld;
+    for (int m = lane; m < s; m += 32) {
+      br[m] = col[perm[m]];
+      if (C) bi[m] = col[perm[m] + a.aim];
+    }
+    __syncwarp();
+    for (int m = lane; m < s; m += 32) {
+      col[m] = br[m];
+      if (C) col[m + a.aim] = bi[m];
+    }
+    __syncwarp();
+  }
+}
+
+// ============================================================================ K2 panel TRSM
+constexpr int NT2 = 128;
+using K2GemmR = Gemm<64, TB, 16, 2, 2, 3, false, false, false>;
+using K2GemmC = Gemm<64, TB, 16, 2, 2, 3, true, false, false>;
+
+template <bool C>
+__global__ void __launch_bounds__(NT2) k2_panel(K2Args a) {
+  using G = typename std::conditional<C, K2GemmC, K2GemmR>::type;
+  extern __shared__ __align__(16) double smem[];
+  const Strip S = a.strips[blockIdx.x];
+  const NodeDev nd = a.nd[S.t];
+  const int s = nd.s;
+  const int64_t ldA = nd.ld, ldW = nd.ldw;
+  double* P = a.arena + nd.panel;                 // panel t
+  double* Ahat = P + nd.sp + S.row0;             // strip rows of A_struct,t (before permutation)
+  double* W = a.work + nd.w + S.row0;            // strip rows of W_t
+  const int* perm = a.perm + nd.ydof;
+  const double* Linv = a.arena + nd.linv;
+  const int64_t aim = a.aim, wim = a.wim;
+  const int M = S.nrows;
+  const int np = (s + TB - 1) / TB;
+  for (int p = 0; p < np; ++p) {
+    const int c0 = p * TB, w = min(TB, s - c0);
+    typename G::Acc acc;
+    G::zero(acc);
+    if (c0 > 0) {  // acc = W(:, 0:c0) L(c0:c0+w, 0:c0)^T
+      Seg sg{W, P + c0, nullptr, ldW, ldA, c0};
+      G::run([&](int) { return sg; }, 1, 0, 0, M, w, wim, aim, smem, acc);
+    }
+    // T = Ahat(:, perm[c0:c0+w]) - acc  -> W(:, c0:c0+w)
+    G::for_each(acc, [&](int r, int c, double vr, double vi) {
+      if (r < M && c < w) {
+        int64_t src = (int64_t)r + (int64_t)perm[c0 + c] * ldA;
+        int64_t dst = (int64_t)r + (int64_t)(c0 + c) * ldW;
+        W[dst] = Ahat[src] - vr;
+        if (C) W[dst + wim] = Ahat[src + aim] - vi;
+      }
+    });
+    __threadfence();
+    __syncthreads();
+    // W(:, c0:c0+w) = T Linv_pp^T
+    G::zero(acc);
+    {
+      Seg sg{W + (int64_t)c0 * ldW, Linv + (int64_t)p * TB * TB, nullptr, ldW, TB, w};
+      G::run([&](int) { return sg; }, 1, 0, 0, M, w, wim, aim, smem, acc);
+    }
+    G::for_each(acc, [&](int r, int c, double vr, double vi) {
+      if (r < M && c < w) {
+        int64_t dst = (int64_t)r + (int64_t)(c0 + c) * ldW;
+        W[dst] = vr;
+        if (C) W[dst + wim] = vi;
+      }
+    });
+    __threadfence();
+    __syncthreads();
+  }
+  // L = W D^{-1} (1x1 / 2x2 closed form) -> panel rows (overwrites A_struct,t)
+  const double* dv_ = a.arena + a.d_off + nd.ydof;
+  const double* ev_ = a.arena + a.e_off + nd.ydof;
+  const int* ipiv = a.ipiv + nd.ydof;
+  for (int c = 0; c < s; ++c) {
+    const bool two = ipiv[c] < 0;
+    // a 2x2 pivot is only taken when colmax > 0, so e != 0 exactly on the first column of a pair
+    const cz e0 = ld<C>(ev_, c, aim);
+    const int c1 = (two && (e0.r != 0.0 || e0.i != 0.0)) ? c : c - 1;  // first column of the pair
+    for (int r = threadIdx.x; r < M; r += NT2) {
+      int64_t e = (int64_t)r + (int64_t)c * ldW;
+      cz wv = ld<C>(W, e, wim);
+      cz out;
+      if (!two) {
+        cz d = ld<C>(dv_, c, aim);
+        out = (d.r == 0.0 && d.i == 0.0) ? wv : dv<C>(wv, d);
+      } else {
+        cz d11 = ld<C>(dv_, c1, aim), d22 = ld<C>(dv_, c1 + 1, aim), d21 = ld<C>(ev_, c1, aim);
+        cz wk = ld<C>(W, (int64_t)r + (int64_t)c1 * ldW, wim), wk1 = ld<C>(W, (int64_t)r + (int64_t)(c1 + 1) * ldW, wim);
+        cz a11 = dv<C>(d22, d21), a22 = dv<C>(d11, d21);
+        cz tt = dv<C>(mk(1.0, 0.0), mul<C>(a11, a22) - mk(1.0, 0.0));
+        cz s21 = dv<C>(tt, d21);
+        out = (c == c1) ? mul<C>(s21, mul<C>(a11, wk) - wk1) : mul<C>(s21, mul<C>(a22, wk1) - wk);
+      }
+      st<C>(Ahat, (int64_t)r + (int64_t)c * ldA, aim, out);
+    }
+  }
+}
+
+// ============================================================================ K3 Schur update
+constexpr int NT3 = 256;
+using K3GemmR = Gemm<128, 128, 16, 2, 4, 4, false, false, false>;
+using K3GemmC = Gemm<64, 128, 16, 2, 4, 3, true, false, false>;
+
+template <bool C>
+__global__ void __launch_bounds__(NT3, 1) k3_update(K3Args a) {
+  using G = typename std::conditional<C, K3GemmC, K3GemmR>::type;
+  constexpr int BM = C ? 64 : 128, BN = 128;
+  extern __shared__ __align__(16) double smem[];
+  const Tile T = a.tiles[blockIdx.x];
+  const UpdTarget tg = a.targets[T.target];
+  const NodeDev nj = a.nd[tg.j];
+  typename G::Acc acc;
+  G::zero(acc);
+  const UpdContrib* cl = a.contribs + tg.c0;
+  auto segfn = [&](int q) {
+    const UpdContrib u = cl[q];
+    const NodeDev nk = a.nd[u.k];
+    Seg sg;
+    sg.a = a.work + nk.w + u.arow;          // W_ik
+    sg.lda = nk.ldw;
+    sg.b = a.arena + nk.panel + u.brow;     // B(q, n) = L_jk(n, q)
+    sg.ldb = nk.ld;
+    sg.acol = nullptr;
+    sg.K = nk.s;
+    return sg;
+  };
+  G::run(segfn, tg.c1 - tg.c0, T.tm * BM, T.tn * BN, tg.M, tg.N, a.wim, a.aim, smem, acc);
+  double* Cb = a.arena + nj.panel + tg.ro + (int64_t)T.tm * BM + (int64_t)T.tn * BN * nj.ld;
+  const int mlim = tg.M - T.tm * BM, nlim = tg.N - T.tn * BN;
+  const int64_t ldc = nj.ld, aim = a.aim;
+  G::for_each(acc, [&](int r, int c, double vr, double vi) {
+    if (r < mlim && c < nlim) {
+      int64_t e = (int64_t)r + (int64_t)c * ldc;
+      Cb[e] -= vr;
+      if (C) Cb[e + aim] -= vi;
+    }
+  });
+}
+
+// ============================================================================ K4 stats
+__global__ void k4_stats(const int64_t* __restrict__ node_stats, int nnodes, int64_t* __restrict__ out) {
+  __shared__ int64_t sh[8][8];
+  int64_t acc[6] = {0, 0, 0, 0, 0, INT64_MAX};
+  for (int t = threadIdx.x; t < nnodes; t += blockDim.x) {
+    const int64_t* S = node_stats + (int64_t)t * 8;
+    for (int q = 0; q < 5; ++q) acc[q] += S[q];
+    if (S[5] > 0 && S[5] < acc[5]) acc[5] = S[5];  // NOTE: smallest original DoF among zero pivots
+  }
+  // simple two-level reduction (256 threads)
+  for (int q = 0; q < 6; ++q) {
+    int64_t v = acc[q];
+    for (int o = 16; o; o >>= 1) {
+      int64_t u = __shfl_xor_sync(0xffffffffu, v, o);
+      v = (q == 5) ? (u < v ? u : v) : v + u;
+    }
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t r[6] = {0, 0, 0, 0, 0, INT64_MAX};
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+      for (int q = 0; q < 6; ++q) r[q] = (q == 5) ? (sh[w][q] < r[q] ? sh[w][q] : r[q]) : r[q] + sh[w][q];
+    for (int q = 0; q < 5; ++q) out[q] = r[q];
+    out[5] = r[5] == INT64_MAX ? 0 : r[5];
+  }
+}
+
+// ============================================================================ launchers
+template <class K>
+static void set_smem(K kern, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+void launch_load(bool cplx, const double* vals, const LoadBlock* lb, int nblocks, int64_t max_elems, double* arena,
+                 int64_t aim, cudaStream_t st) {
+  if (nblocks == 0) return;
+  int gx = (int)std::min<int64_t>((max_elems + 255) / 256, 64);
+  dim3 grid(gx, nblocks);
+  if (cplx) k0_load<true><<<grid, 256, 0, st>>>(vals, lb, nblocks, arena, aim);
+  else k0_load<false><<<grid, 256, 0, st>>>(vals, lb, nblocks, arena, aim);
+}
+
+size_t k1_smem(bool cplx) {
+  size_t g = cplx ? K1GemmC::SMEM_BYTES : K1GemmR::SMEM_BYTES;
+  size_t inv = (size_t)(NT1 / 32) * 2 * TB * TB * sizeof(double);
+  return g > inv ? g : inv;
+}
+
+void launch_k1(bool cplx, const K1Args& a, int nnodes, cudaStream_t st) {
+  size_t sm = k1_smem(cplx);
+  if (cplx) {
+    set_smem(k1_diag_bk<true>, sm);
+    k1_diag_bk<true><<<nnodes, NT1, sm, st>>>(a);
+  } else {
+    set_smem(k1_diag_bk<false>, sm);
+    k1_diag_bk<false><<<nnodes, NT1, sm, st>>>(a);
+  }
+}
+
+void launch_rowperm(bool cplx, const RowpermArgs& a, int nlist, int max_s, cudaStream_t st) {
+  if (nlist == 0) return;
+  size_t sm = (size_t)4 * 2 * max_s * sizeof(double);  // 4 warps
+  dim3 grid(8, nlist);
+  if (cplx) {
+    set_smem(k_rowperm<true>, sm);
+    k_rowperm<true><<<grid, 128, sm, st>>>(a);
+  } else {
+    set_smem(k_rowperm<false>, sm);
+    k_rowperm<false><<<grid, 128, sm, st>>>(a);
+  }
+}
+
+void launch_k2(bool cplx, const K2Args& a, int nstrips, cudaStream_t st) {
+  if (nstrips == 0) return;
+  if (cplx) {
+    set_smem(k2_panel<true>, K2GemmC::SMEM_BYTES);
+    k2_panel<true><<<nstrips, NT2, K2GemmC::SMEM_BYTES, st>>>(a);
+  } else {
+    set_smem(k2_panel<false>, K2GemmR::SMEM_BYTES);
+    k2_panel<false><<<nstrips, NT2, K2GemmR::SMEM_BYTES, st>>>(a);
+  }
+}
+
+int k3_bm(bool cplx) { return cplx ? 64 : 128; }
+int k3_bn(bool) { return 128; }
+
+void launch_k3(bool cplx, const K3Args& a, int ntiles, cudaStream_t st) {
+  if (ntiles == 0) return;
+  if (cplx) {
+    set_smem(k3_update<true>, K3GemmC::SMEM_BYTES);
+    k3_update<true><<<ntiles, NT3, K3GemmC::SMEM_BYTES, st>>>(a);
+  } else {
+    set_smem(k3_update<false>, K3GemmR::SMEM_BYTES);
+    k3_update<false><<<ntiles, NT3, K3GemmR::SMEM_BYTES, st>>>(a);
+  }
+}
+
+void launch_k4(const int64_t* node_stats, int nnodes, int64_t* out, cudaStream_t st) {
+  k4_stats<<<1, 256, 0, st>>>(node_stats, nnodes, out);
+}
+
+}  // namespace ddk

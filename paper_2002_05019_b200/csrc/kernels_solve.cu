@@ -1,0 +1,447 @@
+// Solve-phase kernels (sm_100a).  PAPER.md:29 (§II) "Once the auxiliary problem has been
+// efficiently factorized" it is solved by forward/backward substitution for many
+// excitations (Fig. 2c "200 excitations"); SURVEY.md §8(a) a7, a8.
+//
+//   y = P b              k_perm_in     (block order + in-block pivots, planar complex)
+//   forward, per level:  k_fdiag       z_t = L_tt^{-1} y_t   (TB-tile inverses -> DMMA GEMMs)
+//                        k_fupd        y_i -= sum_k L_ik z_k (owner-computes, gathered K)
+//   y = D^{-1} y         k_dsolve      (1x1 / 2x2 closed form)
+//   backward, per level: k_bupd        y_t -= sum_i L_it^T y_i   (pull, conflict-free)
+//                        k_bdiag       y_t = L_tt^{-T} y_t
+//   x = P^T y            k_perm_out    (store, or accumulate a refinement correction)
+//   r = b - A x          k_spmv        (refinement residual over the ORIGINAL blocks, L7)
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "gemm_core.cuh"
+#include "launch.hpp"
+
+using namespace ddaux;
+
+namespace ddk {
+
+constexpr int SBN = 64;  // rhs tile for every solve GEMM
+using FDiagR = Gemm<TB, SBN, 16, 1, 4, 3, false, false, true>;
+using FDiagC = Gemm<TB, SBN, 16, 1, 4, 3, true, false, true>;
+using BDiagR = Gemm<TB, SBN, 16, 1, 4, 3, false, true, true>;
+using BDiagC = Gemm<TB, SBN, 16, 1, 4, 3, true, true, true>;
+constexpr int SUBM = 64;
+using FUpdR = Gemm<SUBM, SBN, 16, 2, 2, 3, false, false, true>;
+using FUpdC = Gemm<SUBM, SBN, 16, 2, 2, 3, true, false, true>;
+using BUpdR = Gemm<SUBM, SBN, 16, 2, 2, 3, false, true, true>;
+using BUpdC = Gemm<SUBM, SBN, 16, 2, 2, 3, true, true, true>;
+
+// ---------------------------------------------------------------------------- permutations
+template <bool C>
+__global__ void k_perm_in(PermArgs a) {
+  const int c = blockIdx.y;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.nrows; g += (int64_t)gridDim.x * blockDim.x) {
+    const int o = a.gperm[g];
+    double re = 0.0, im = 0.0;
+    if (o >= 0) {
+      int64_t e = (int64_t)o + (int64_t)c * a.lds;
+      if (C) {
+        re = a.src[2 * e];
+        im = a.src[2 * e + 1];
+      } else {
+        re = a.src[e];
+      }
+    }
+    int64_t d = g + (int64_t)c * a.ldy;
+    a.y[d] = re;
+    if (C) a.y[d + a.yim] = im;
+  }
+}
+
+template <bool C>
+__global__ void k_perm_out(PermArgs a) {
+  const int c = blockIdx.y;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.nrows; g += (int64_t)gridDim.x * blockDim.x) {
+    const int o = a.gperm[g];
+    if (o < 0) continue;
+    int64_t s = g + (int64_t)c * a.ldy;
+    int64_t e = (int64_t)o + (int64_t)c * a.ldd;
+    if (C) {
+      double re = a.y[s], im = a.y[s + a.yim];
+      if (a.accumulate) {
+        a.dst[2 * e] += re;
+        a.dst[2 * e + 1] += im;
+      } else {
+        a.dst[2 * e] = re;
+        a.dst[2 * e + 1] = im;
+      }
+    } else {
+      if (a.accumulate) a.dst[e] += a.y[s];
+      else a.dst[e] = a.y[s];
+    }
+  }
+}
+
+__global__ void k_copy(const double* __restrict__ src, int64_t lds, double* __restrict__ dst, int64_t ldd,
+                       int64_t n, int w) {
+  const int c = blockIdx.y;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n * w; r += (int64_t)gridDim.x * blockDim.x)
+    dst[r + (int64_t)c * ldd * w] = src[r + (int64_t)c * lds * w];
+}
+
+// ---------------------------------------------------------------------------- diagonal solves
+template <bool C>
+__global__ void __launch_bounds__(128) k_fdiag(SolveArgs a) {
+  using G = typename std::conditional<C, FDiagC, FDiagR>::type;
+  extern __shared__ __align__(16) double smem[];
+  const int t = a.nodes[blockIdx.x];
+  const NodeDev nd = a.nd[t];
+  const int s = nd.s, n0 = blockIdx.y * SBN;
+  const double* P = a.arena + nd.panel;
+  const double* Linv = a.arena + nd.linv;
+  double* y = a.y + nd.ydof;  // y(k, n) = y[k + n*ldy]
+  const int64_t ldy = a.ldy, yim = a.yim;
+  const int np = (s + TB - 1) / TB;
+  for (int p = 0; p < np; ++p) {
+    const int c0 = p * TB, w = min(TB, s - c0);
+    typename G::Acc acc;
+    G::zero(acc);
+    if (c0 > 0) {  // acc = L(c0:c0+w, 0:c0) z(0:c0)
+      Seg sg{P + c0, y, nullptr, (int64_t)nd.ld, ldy, c0};
+      G::run([&](int) { return sg; }, 1, 0, n0, w, a.nrhs, a.aim, yim, smem, acc);
+    }
+    G::for_each(acc, [&](int r, int c, double vr, double vi) {
+      if (r < w && n0 + c < a.nrhs) {
+        int64_t e = (int64_t)(c0 + r) + (int64_t)(n0 + c) * ldy;
+        y[e] -= vr;
+        if (C) y[e + yim] -= vi;
+      }
+    });
+    __threadfence();
+    __syncthreads();
+    G::zero(acc);
+    {
+      Seg sg{Linv + (int64_t)p * TB * TB, y + c0, nullptr, (int64_t)TB, ldy, w};
+      G::run([&](int) { return sg; }, 1, 0, n0, w, a.nrhs, a.aim, yim, smem, acc);
+    }
+    G::for_each(acc, [&](int r, int c, double vr, double vi) {
+      if (r < w && n0 + c < a.nrhs) {
+        int64_t e = (int64_t)(c0 + r) + (int64_t)(n0 + c) * ldy;
+        y[e] = vr;
+        if (C) y[e + yim] = vi;
+      }
+    });
+    __threadfence();
+    __syncthreads();
+  }
+}
+
+template <bool C>
+__global__ void __launch_bounds__(128) k_bdiag(SolveArgs a) {
+  using G = typename std::conditional<C, BDiagC, BDiagR>::type;
+  extern __shared__ __align__(16) double smem[];
+  const int t = a.nodes[blockIdx.x];
+  const NodeDev nd = a.nd[t];
+  const int s = nd.s, n0 = blockIdx.y * SBN;
+  const double* P = a.arena + nd.panel;
+  const double* Linv = a.arena + nd.linv;
+  double* y = a.y + nd.ydof;
+  const int64_t ldy = a.ldy, yim = a.yim, ldA = nd.ld;
+  const int np = (s + TB - 1) / TB;
+  for (int p = np - 1; p >= 0; --p) {
+    const int c0 = p * TB, w = min(TB, s - c0), c1 = c0 + w;
+    typename G::Acc acc;
+    G::zero(acc);
+    if (c1 < s) {  // acc = L(c1:s, c0:c1)^T z(c1:s)
+      Seg sg{P + c1 + (int64_t)c0 * ldA, y + c1, nullptr, ldA, ldy, s - c1};
+      G::run([&](int) { return sg; }, 1, 0, n0, w, a.nrhs, a.aim, yim, smem, acc);
+    }
+    G::for_each(acc, [&](int r, int c, double vr, double vi) {
+      if (r < w && n0 + c < a.nrhs) {
+        int64_t e = (int64_t)(c0 + r) + (int64_t)(n0 + c) * ldy;
+        y[e] -= vr;
+        if (C) y[e + yim] -= vi;
+      }
+    });
+    __threadfence();
+    __syncthreads();
+    G::zero(acc);
+    {
+      Seg sg{Linv + (int64_t)p * TB * TB, y + c0, nullptr, (int64_t)TB, ldy, w};
+      G::run([&](int) { return sg; }, 1, 0, n0, w, a.nrhs, a.aim, yim, smem, acc);
+    }
+    G::for_each(acc, [&](int r, int c, double vr, double vi) {
+      if (r < w && n0 + c < a.nrhs) {
+        int64_t e = (int64_t)(c0 + r) + (int64_t)(n0 + c) * ldy;
+        y[e] = vr;
+        if (C) y[e + yim] = vi;
+      }
+    });
+    __threadfence();
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------- level updates
+template <bool C>
+__global__ void __launch_bounds__(128) k_fupd(SolveArgs a) {
+  using G = typename std::conditional<C, FUpdC, FUpdR>::type;
+  extern __shared__ __align__(16) double smem[];
+  const SolveTarget T = a.ftargets[blockIdx.x];
+  const NodeDev ni = a.nd[T.i];
+  const int n0 = blockIdx.y * SBN, m0 = T.tm * SUBM;
+  typename G::Acc acc;
+  G::zero(acc);
+  const SolveContrib* cl = a.fcontribs + T.c0;
+  auto segfn = [&](int q) {
+    const SolveContrib u = cl[q];
+    const NodeDev nk = a.nd[u.k];
+    Seg sg{a.arena + nk.panel + u.ro, a.y + nk.ydof, nullptr, (int64_t)nk.ld, a.ldy, nk.s};
+    return sg;
+  };
+  G::run(segfn, T.c1 - T.c0, m0, n0, ni.s, a.nrhs, a.aim, a.yim, smem, acc);
+  double* y = a.y + ni.ydof;
+  G::for_each(acc, [&](int r, int c, double vr, double vi) {
+    if (m0 + r < ni.s && n0 + c < a.nrhs) {
+      int64_t e = (int64_t)(m0 + r) + (int64_t)(n0 + c) * a.ldy;
+      y[e] -= vr;
+      if (C) y[e + a.yim] -= vi;
+    }
+  });
+}
+
+template <bool C>
+__global__ void __launch_bounds__(128) k_bupd(SolveArgs a) {
+  using G = typename std::conditional<C, BUpdC, BUpdR>::type;
+  extern __shared__ __align__(16) double smem[];
+  const int2 T = a.btiles[blockIdx.x];  // (t, tm)
+  const NodeDev nt = a.nd[T.x];
+  const int n0 = blockIdx.y * SBN, m0 = T.y * SUBM;
+  typename G::Acc acc;
+  G::zero(acc);
+  auto segfn = [&](int q) {
+    const int ipos = a.st_pos[nt.st0 + q];
+    const int ro = a.st_row[nt.st0 + q];
+    const NodeDev ni = a.nd[ipos];
+    // A(m, k) = L_it(k, m) = panel_t[(ro + k) + m*ld]  (KM)
+    Seg sg{a.arena + nt.panel + ro, a.y + ni.ydof, nullptr, (int64_t)nt.ld, a.ldy, ni.s};
+    return sg;
+  };
+  G::run(segfn, nt.nst, m0, n0, nt.s, a.nrhs, a.aim, a.yim, smem, acc);
+  double* y = a.y + nt.ydof;
+  G::for_each(acc, [&](int r, int c, double vr, double vi) {
+    if (m0 + r < nt.s && n0 + c < a.nrhs) {
+      int64_t e = (int64_t)(m0 + r) + (int64_t)(n0 + c) * a.ldy;
+      y[e] -= vr;
+      if (C) y[e + a.yim] -= vi;
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------- D solve
+template <bool C>
+__global__ void k_dsolve(SolveArgs a) {
+  const int c = blockIdx.y;
+  const double* dv_ = a.arena + a.d_off;
+  const double* ev_ = a.arena + a.e_off;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.nrows; g += (int64_t)gridDim.x * blockDim.x) {
+    const int pv = a.ipiv[g];
+    if (pv == 0) continue;  // padding row
+    int64_t e = g + (int64_t)c * a.ldy;
+    if (pv > 0) {
+      cz d = ld<C>(dv_, g, a.aim);
+      if (d.r == 0.0 && d.i == 0.0) continue;
+      st<C>(a.y, e, a.yim, dv<C>(ld<C>(a.y, e, a.yim), d));
+    } else {
+      cz ee = ld<C>(ev_, g, a.aim);
+      if (ee.r == 0.0 && ee.i == 0.0) continue;  // second row of a pair: handled by the first
+      cz d1 = ld<C>(dv_, g, a.aim), d2 = ld<C>(dv_, g + 1, a.aim);
+      cz y1 = ld<C>(a.y, e, a.yim), y2 = ld<C>(a.y, e + 1, a.yim);
+      // LAPACK xSYTRS scaled closed form
+      cz akm1 = dv<C>(d1, ee), ak = dv<C>(d2, ee);
+      cz den = mul<C>(akm1, ak) - mk(1.0, 0.0);
+      cz bkm1 = dv<C>(y1, ee), bk = dv<C>(y2, ee);
+      st<C>(a.y, e, a.yim, dv<C>(mul<C>(ak, bkm1) - bk, den));
+      st<C>(a.y, e + 1, a.yim, dv<C>(mul<C>(akm1, bk) - bkm1, den));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------- residual SpMV
+// R = Bsave - A X over the caller's original blocks (both triangles), SIMT FP64, written
+// permuted into y.  CTA tile: 64 rows x 32 rhs; 256 threads, 4 x 2 outputs each.
+constexpr int SPM = 64, SPN = 32, SPK = 16;
+template <bool C>
+__global__ void __launch_bounds__(256) k_spmv(SpmvArgs a) {
+  __shared__ double Ar[SPK][SPM + 1], Ai[C ? SPK : 1][C ? SPM + 1 : 1];
+  __shared__ double Xr[SPK][SPN + 1], Xi[C ? SPK : 1][C ? SPN + 1 : 1];
+  const SpRow R = a.rows[blockIdx.x];
+  const int I = R.I;
+  const int sI = (int)a.blk_size[I];
+  const int m0 = R.tm * SPM, n0 = blockIdx.y * SPN;
+  const int tid = threadIdx.x;
+  const int tr = tid % 16, tc = tid / 16;  // rows tr*4.., cols tc*2..
+  double accr[4][2] = {}, acci[4][2] = {};
+  for (int q = R.c0; q < R.c1; ++q) {
+    const SpSeg sg = a.segs[q];
+    const int sJ = (int)a.blk_size[sg.J];
+    const int64_t oJ = a.odof[sg.J];
+    for (int k0 = 0; k0 < sJ; k0 += SPK) {
+      __syncthreads();
+      for (int e = tid; e < SPM * SPK; e += 256) {
+        int m = e % SPM, k = e / SPM;
+        int gm = m0 + m, gk = k0 + k;
+        double vr = 0.0, vi = 0.0;
+        if (gm < sI && gk < sJ) {
+          int64_t idx;
+          if (sg.mode == 0) idx = gm + (int64_t)gk * sI;           // stored (I,J): s_I x s_J
+          else if (sg.mode == 1) idx = gk + (int64_t)gm * sJ;      // stored (J,I): s_J x s_I, transposed
+          else idx = gm >= gk ? gm + (int64_t)gk * sI : gk + (int64_t)gm * sI;  // diagonal, lower triangle
+          idx += sg.voff;
+          if (C) {
+            vr = a.vals[2 * idx];
+            vi = a.vals[2 * idx + 1];
+          } else {
+            vr = a.vals[idx];
+          }
+        }
+        Ar[k][m] = vr;
+        if (C) Ai[k][m] = vi;
+      }
+      for (int e = tid; e < SPK * SPN; e += 256) {
+        int k = e % SPK, n = e / SPK;
+        int gk = k0 + k, gn = n0 + n;
+        double vr = 0.0, vi = 0.0;
+        if (gk < sJ && gn < a.nrhs) {
+          int64_t idx = oJ + gk + (int64_t)gn * a.ldx;
+          if (C) {
+            vr = a.X[2 * idx];
+            vi = a.X[2 * idx + 1];
+          } else {
+            vr = a.X[idx];
+          }
+        }
+        Xr[k][n] = vr;
+        if (C) Xi[k][n] = vi;
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int k = 0; k < SPK; ++k) {
+        double ar[4], ai[4], xr[2], xi[2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ar[u] = Ar[k][tr * 4 + u];
+          if (C) ai[u] = Ai[k][tr * 4 + u];
+        }
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          xr[v] = Xr[k][tc * 2 + v];
+          if (C) xi[v] = Xi[k][tc * 2 + v];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            accr[u][v] = fma(ar[u], xr[v], accr[u][v]);
+            if (C) {
+              accr[u][v] = fma(-ai[u], xi[v], accr[u][v]);
+              acci[u][v] = fma(ar[u], xi[v], acci[u][v]);
+              acci[u][v] = fma(ai[u], xr[v], acci[u][v]);
+            }
+          }
+      }
+    }
+  }
+  const int64_t oI = a.odof[I];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      int gm = m0 + tr * 4 + u, gn = n0 + tc * 2 + v;
+      if (gm < sI && gn < a.nrhs) {
+        int64_t orow = oI + gm;
+        int64_t bidx = orow + (int64_t)gn * a.ldb;
+        int64_t yidx = (int64_t)a.ginv[orow] + (int64_t)gn * a.ldy;
+        if (C) {
+          a.y[yidx] = a.Bsave[2 * bidx] - accr[u][v];
+          a.y[yidx + a.yim] = a.Bsave[2 * bidx + 1] - acci[u][v];
+        } else {
+          a.y[yidx] = a.Bsave[bidx] - accr[u][v];
+        }
+      }
+    }
+}
+
+// ---------------------------------------------------------------------------- launchers
+template <class K>
+static void set_smem(K kern, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+int solve_bm(bool) { return SUBM; }
+int solve_bn(bool) { return SBN; }
+int spmv_bm() { return SPM; }
+
+static dim3 rows_grid(int64_t nrows, int nrhs) {
+  int gx = (int)std::min<int64_t>((nrows + 255) / 256, 1024);
+  return dim3(gx > 0 ? gx : 1, nrhs);
+}
+
+void launch_perm_in(bool cplx, const PermArgs& a, cudaStream_t st) {
+  if (a.nrhs == 0) return;
+  if (cplx) k_perm_in<true><<<rows_grid(a.nrows, a.nrhs), 256, 0, st>>>(a);
+  else k_perm_in<false><<<rows_grid(a.nrows, a.nrhs), 256, 0, st>>>(a);
+}
+void launch_perm_out(bool cplx, const PermArgs& a, cudaStream_t st) {
+  if (a.nrhs == 0) return;
+  if (cplx) k_perm_out<true><<<rows_grid(a.nrows, a.nrhs), 256, 0, st>>>(a);
+  else k_perm_out<false><<<rows_grid(a.nrows, a.nrhs), 256, 0, st>>>(a);
+}
+void launch_copy(bool cplx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t n, int nrhs,
+                 cudaStream_t st) {
+  if (nrhs == 0) return;
+  int w = cplx ? 2 : 1;
+  k_copy<<<rows_grid(n * w, nrhs), 256, 0, st>>>(src, lds, dst, ldd, n, w);
+}
+
+#define DD_LAUNCH_GEMM_KERNEL(KER, GR, GC, GRID, THREADS)                   \
+  do {                                                                      \
+    if (cplx) {                                                             \
+      set_smem(KER<true>, GC::SMEM_BYTES);                                  \
+      KER<true><<<GRID, THREADS, GC::SMEM_BYTES, st>>>(a);                  \
+    } else {                                                                \
+      set_smem(KER<false>, GR::SMEM_BYTES);                                 \
+      KER<false><<<GRID, THREADS, GR::SMEM_BYTES, st>>>(a);                 \
+    }                                                                       \
+  } while (0)
+
+static int ntn(int nrhs) { return (nrhs + SBN - 1) / SBN; }
+
+void launch_fdiag(bool cplx, const SolveArgs& a, int nnodes, cudaStream_t st) {
+  if (nnodes == 0 || a.nrhs == 0) return;
+  dim3 grid(nnodes, ntn(a.nrhs));
+  DD_LAUNCH_GEMM_KERNEL(k_fdiag, FDiagR, FDiagC, grid, 128);
+}
+void launch_bdiag(bool cplx, const SolveArgs& a, int nnodes, cudaStream_t st) {
+  if (nnodes == 0 || a.nrhs == 0) return;
+  dim3 grid(nnodes, ntn(a.nrhs));
+  DD_LAUNCH_GEMM_KERNEL(k_bdiag, BDiagR, BDiagC, grid, 128);
+}
+void launch_fupd(bool cplx, const SolveArgs& a, int ntiles, cudaStream_t st) {
+  if (ntiles == 0 || a.nrhs == 0) return;
+  dim3 grid(ntiles, ntn(a.nrhs));
+  DD_LAUNCH_GEMM_KERNEL(k_fupd, FUpdR, FUpdC, grid, 128);
+}
+void launch_bupd(bool cplx, const SolveArgs& a, int ntiles, cudaStream_t st) {
+  if (ntiles == 0 || a.nrhs == 0) return;
+  dim3 grid(ntiles, ntn(a.nrhs));
+  DD_LAUNCH_GEMM_KERNEL(k_bupd, BUpdR, BUpdC, grid, 128);
+}
+void launch_dsolve(bool cplx, const SolveArgs& a, cudaStream_t st) {
+  if (a.nrhs == 0) return;
+  if (cplx) k_dsolve<true><<<rows_grid(a.nrows, a.nrhs), 256, 0, st>>>(a);
+  else k_dsolve<false><<<rows_grid(a.nrows, a.nrhs), 256, 0, st>>>(a);
+}
+void launch_spmv(bool cplx, const SpmvArgs& a, int nrow_tiles, cudaStream_t st) {
+  if (nrow_tiles == 0 || a.nrhs == 0) return;
+  dim3 grid(nrow_tiles, (a.nrhs + SPN - 1) / SPN);
+  if (cplx) k_spmv<true><<<grid, 256, 0, st>>>(a);
+  else k_spmv<false><<<grid, 256, 0, st>>>(a);
+}
+
+}  // namespace ddk

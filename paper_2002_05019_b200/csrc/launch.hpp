@@ -1,0 +1,138 @@
+// Kernel argument blocks and launchers (host <-> device boundary inside the library).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "layout.hpp"
+
+namespace ddk {
+using namespace ddaux;
+
+struct LoadBlock {     // K0: one caller block -> arena
+  int64_t voff;        // element offset in d_vals
+  int64_t dst;         // element offset of the destination (row 0, col 0) in the arena
+  int64_t ld;          // destination leading dimension
+  int32_t rows, cols;  // stored block shape s_I x s_J
+  int32_t trans, diag; // write transposed; diagonal block (lower only)
+};
+
+struct K1Args {
+  const int* nodes;
+  const NodeDev* nd;
+  double* arena;
+  int64_t aim;
+  double* work;
+  int64_t wim;
+  int* perm;
+  int* ipiv;
+  int* gperm;
+  int* ginv;
+  int64_t d_off, e_off;
+  int64_t* stats;
+};
+
+struct RowpermArgs {
+  const RowPerm* list;
+  const NodeDev* nd;
+  double* arena;
+  int64_t aim;
+  const int* perm;
+};
+
+struct K2Args {
+  const Strip* strips;
+  const NodeDev* nd;
+  double* arena;
+  int64_t aim;
+  double* work;
+  int64_t wim;
+  const int* perm;
+  const int* ipiv;
+  int64_t d_off, e_off;
+};
+
+struct K3Args {
+  const Tile* tiles;
+  const UpdTarget* targets;
+  const UpdContrib* contribs;
+  const NodeDev* nd;
+  double* arena;
+  int64_t aim;
+  const double* work;
+  int64_t wim;
+};
+
+struct SolveArgs {
+  const NodeDev* nd;
+  const double* arena;  // factor values
+  int64_t aim;
+  double* y;            // position-ordered padded RHS block, planar
+  int64_t yim, ldy;
+  int nrhs;
+  const int* nodes;             // level nodes (diag kernels)
+  const SolveTarget* ftargets;  // forward update tiles
+  const SolveContrib* fcontribs;
+  const int2* btiles;           // backward update tiles (t, tm)
+  const int* st_pos;            // struct arrays
+  const int* st_row;
+  const int* ipiv;
+  int64_t d_off, e_off;
+  int64_t nrows;                // padded n
+};
+
+struct PermArgs {
+  const int* gperm;   // padded position row -> original DoF (-1 pad)
+  int64_t nrows;      // padded n
+  int nrhs;
+  const double* src;  // interleaved (complex) or real, column-major, leading dim lds
+  int64_t lds;
+  double* dst;
+  int64_t ldd;
+  double* y;
+  int64_t yim, ldy;
+  int accumulate;
+};
+
+struct SpmvArgs {
+  const SpRow* rows;
+  const SpSeg* segs;
+  const int64_t* blk_size;   // original sizes
+  const int64_t* odof;       // original DoF offsets per block
+  const double* vals;        // caller's original blocks (interleaved complex)
+  const double* X;           // current solution (caller's B buffer), ld ldx
+  int64_t ldx;
+  const double* Bsave;       // original right-hand sides, ld n
+  int64_t ldb;
+  const int* ginv;           // original DoF -> padded position row
+  double* y;                 // residual out (position order, planar)
+  int64_t yim, ldy;
+  int nrhs;
+};
+
+void launch_load(bool cplx, const double* vals, const LoadBlock* lb, int nblocks, int64_t max_elems, double* arena,
+                 int64_t aim, cudaStream_t st);
+size_t k1_smem(bool cplx);
+void launch_k1(bool cplx, const K1Args& a, int nnodes, cudaStream_t st);
+void launch_rowperm(bool cplx, const RowpermArgs& a, int nlist, int max_s, cudaStream_t st);
+void launch_k2(bool cplx, const K2Args& a, int nstrips, cudaStream_t st);
+int k3_bm(bool cplx);
+int k3_bn(bool cplx);
+void launch_k3(bool cplx, const K3Args& a, int ntiles, cudaStream_t st);
+void launch_k4(const int64_t* node_stats, int nnodes, int64_t* out, cudaStream_t st);
+
+int solve_bm(bool cplx);   // row tile of the forward/backward update kernels
+int solve_bn(bool cplx);   // rhs tile
+void launch_perm_in(bool cplx, const PermArgs& a, cudaStream_t st);
+void launch_perm_out(bool cplx, const PermArgs& a, cudaStream_t st);
+void launch_copy(bool cplx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t n, int nrhs,
+                 cudaStream_t st);
+void launch_fdiag(bool cplx, const SolveArgs& a, int nnodes, cudaStream_t st);
+void launch_fupd(bool cplx, const SolveArgs& a, int ntiles, cudaStream_t st);
+void launch_dsolve(bool cplx, const SolveArgs& a, cudaStream_t st);
+void launch_bupd(bool cplx, const SolveArgs& a, int ntiles, cudaStream_t st);
+void launch_bdiag(bool cplx, const SolveArgs& a, int nnodes, cudaStream_t st);
+int spmv_bm();
+void launch_spmv(bool cplx, const SpmvArgs& a, int nrows_tiles, cudaStream_t st);
+
+}  // namespace ddk

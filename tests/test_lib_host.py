@@ -1,0 +1,125 @@
+"""Host-only checks of the C-ABI library (no GPU needed): the .so loads, exports every
+symbol include/dd_aux.h declares, and dd_aux_analyze's integer results (fill, levels,
+flops, etree) equal the oracle's independent elimination game for the same order.
+"""
+import ctypes
+import re
+import os
+
+import numpy as np
+import pytest
+
+import dd_inputs
+import oracle
+from oracle.block_ldlt import symbolic, flops_factor, flops_solve_per_rhs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _lib():
+    import paper_2002_05019_b200 as dd
+    return dd
+
+
+def test_header_symbols_exported():
+    dd = _lib()
+    hdr = open(os.path.join(ROOT, "include", "dd_aux.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|void|const char\*)\s+(dd_aux_\w+)\s*\(", hdr, re.M))
+    assert declared == set(dd.EXPORTED_SYMBOLS)
+    so = ctypes.CDLL(dd.LIB_PATH)
+    for name in declared:
+        assert hasattr(so, name), name
+    assert "sm_100a" in dd.dd_aux_version()
+
+
+@pytest.mark.parametrize("name,kw,order", [
+    ("cfg0", {}, "auto"),
+    ("cfg1", {}, "nd"),
+    ("cfg1", {"grid": (3, 3, 2), "sizes": 17}, "mindeg"),
+    ("cfg3", {"grid": (4, 4, 2), "sizes": 8}, "auto"),
+    ("cfg2", {"grid": (4, 4, 3), "sizes": lambda n, r: r.integers(3, 40, n)}, "auto"),
+])
+def test_analyze_matches_oracle_symbolic(name, kw, order):
+    dd = _lib()
+    p = dd_inputs.config(name, **kw)
+    o = {"auto": dd.DD_ORDER_AUTO, "nd": dd.DD_ORDER_ND, "mindeg": dd.DD_ORDER_MINDEG}[order]
+    h = dd.dd_aux_analyze(p.blk_size, p.colptr, p.rowidx, dd.DD_COMPLEX128 if p.is_complex else dd.DD_REAL64,
+                          dd.dd_aux_default_options(o))
+    try:
+        info = dd.dd_aux_get_info(h)
+        perm = dd.dd_aux_get_order(h)
+        assert sorted(perm.tolist()) == list(range(p.nblk))
+        sym = symbolic(p.nblk, p.colptr, p.rowidx, perm)
+        mu = 4 if p.is_complex else 1
+        assert info["n"] == p.n and info["nblk"] == p.nblk and info["nnzb_in"] == p.nnzb
+        assert info["nnzb_filled"] == p.nblk + len(sym["orig"]) + len(sym["fill"])
+        assert info["flops_factor"] == pytest.approx(flops_factor(p.blk_size, sym, mu), rel=1e-12)
+        assert info["flops_solve_per_rhs"] == pytest.approx(flops_solve_per_rhs(p.blk_size, sym, mu), rel=1e-12)
+        parent, level, nnz = dd.dd_aux_get_etree(h)
+        assert nnz == sum(len(s) for s in sym["struct"])
+        np.testing.assert_array_equal(parent, sym["parent"])
+        np.testing.assert_array_equal(level, sym["level"])
+        assert info["n_levels"] == int(sym["level"].max()) + 1
+        assert info["factor_bytes"] > 0 and info["work_bytes"] > 0
+    finally:
+        dd.dd_aux_destroy(h)
+
+
+def test_cfg1_nd_quality():
+    """Graph ND without METIS reaches the geometric-ND flop count of SURVEY.md App. A (4.24e11)."""
+    dd = _lib()
+    p = dd_inputs.config("cfg1", sizes=1)  # topology only; flops scale as s^3
+    h = dd.dd_aux_analyze(p.blk_size * 256, p.colptr, p.rowidx, dd.DD_REAL64, dd.dd_aux_default_options(dd.DD_ORDER_ND))
+    info = dd.dd_aux_get_info(h)
+    dd.dd_aux_destroy(h)
+    assert info["flops_factor"] <= 4.3e11
+    assert info["n_levels"] <= 40
+
+
+def test_auto_picks_lower_flops():
+    dd = _lib()
+    p = dd_inputs.config("cfg3", grid=(4, 4, 4), sizes=16)
+    res = {}
+    for o in (dd.DD_ORDER_AUTO, dd.DD_ORDER_ND, dd.DD_ORDER_MINDEG):
+        h = dd.dd_aux_analyze(p.blk_size, p.colptr, p.rowidx, dd.DD_COMPLEX128, dd.dd_aux_default_options(o))
+        res[o] = dd.dd_aux_get_info(h)["flops_factor"]
+        dd.dd_aux_destroy(h)
+    assert res[dd.DD_ORDER_AUTO] == min(res[dd.DD_ORDER_ND], res[dd.DD_ORDER_MINDEG])
+
+
+def test_user_and_natural_order():
+    dd = _lib()
+    p = dd_inputs.config("cfg0")
+    h = dd.dd_aux_analyze(p.blk_size, p.colptr, p.rowidx, dd.DD_REAL64, dd.dd_aux_default_options(user_order=[2, 0, 3, 1]))
+    assert dd.dd_aux_get_order(h).tolist() == [2, 0, 3, 1]
+    dd.dd_aux_destroy(h)
+    h = dd.dd_aux_analyze(p.blk_size, p.colptr, p.rowidx, dd.DD_REAL64, dd.dd_aux_default_options(dd.DD_ORDER_NATURAL))
+    assert dd.dd_aux_get_order(h).tolist() == [0, 1, 2, 3]
+    dd.dd_aux_destroy(h)
+
+
+@pytest.mark.parametrize("bad,rule", [
+    (dict(colptr=[0, 1, 2], rowidx=[0, 0]), "diagonal"),
+    (dict(colptr=[0, 2, 3], rowidx=[0, 0, 1]), "unsorted"),
+    (dict(colptr=[0, 1, 3], rowidx=[0, 1, 0]), "upper"),
+    (dict(colptr=[0, 2, 3], rowidx=[0, 5, 1]), "range"),
+])
+def test_pattern_errors(bad, rule):
+    dd = _lib()
+    with pytest.raises(dd.DDAuxError) as ei:
+        dd.dd_aux_analyze([3, 4], bad["colptr"], bad["rowidx"])
+    assert ei.value.code == dd.DD_ERR_PATTERN
+    assert rule in str(ei.value)
+
+
+def test_argument_errors():
+    dd = _lib()
+    with pytest.raises(dd.DDAuxError) as ei:
+        dd.dd_aux_analyze([3, 0], [0, 1, 2], [0, 1])
+    assert ei.value.code == dd.DD_ERR_PATTERN
+    with pytest.raises(dd.DDAuxError) as ei:
+        dd.dd_aux_analyze([3], [0, 1], [0], dtype=7)
+    assert ei.value.code == -5
+    with pytest.raises(dd.DDAuxError):
+        dd.dd_aux_default_options(user_order=[0, 0])  # not a permutation -> rejected at analyze
+        dd.dd_aux_analyze([3, 3], [0, 1, 2], [0, 1], opt=dd.dd_aux_default_options(user_order=[0, 0]))
