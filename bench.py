@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""Benchmark of the auxiliary-matrix block LDL^T + multi-RHS solve on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl reference]
+
+Metric (BASELINE.json): "aux-matrix LDL^T factor FP64 GFLOP/s (% of FP64 peak); solve ms
+per 1000 RHS".  One step = one pass of the whole hot path over one batch: dd_aux_factor
+(a1 load + a2..a6 level-scheduled factorization) followed by dd_aux_solve of the config's
+nrhs right-hand sides (a7 sweeps + a8 refinement).  `value` = factor GFLOP/s (algorithmic
+flops of the order used / device time of dd_aux_factor), whole job = sum over ranks.
+Inputs are device-resident and far larger than L2 (126 MB), so no flush is needed.
+
+Multi-GPU: the path does not shard (north_star: one GPU, no collectives) -> N independent
+replicas (weak scaling), torch.distributed only for the barrier and max-over-ranks timing.
+`--impl reference` times the CPU oracle (oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import dd_inputs  # noqa: E402
+
+# bounded oracle samples: corner sub-grid of the same workload
+SAMPLE_GRID = {"cfg0": (2, 2, 1), "cfg1": (4, 4, 2), "cfg2": (3, 3, 2), "cfg3": (3, 3, 2), "cfg3alt": (3, 3, 2),
+               "cfg4": (3, 3, 2)}
+WORKLOAD_TXT = {
+    "cfg0": "configs[0]: 2x2x1 grid, 4 x 32 real fp64, n=128",
+    "cfg1": "configs[1]: 4x4x4 grid, 144 x 256 real fp64, n=36864, ND order",
+    "cfg2": "configs[2]: 6x6x6 unstructured-like (L9), sizes U[128,1024], real fp64",
+    "cfg3": "configs[3]: 8x8x4 grid (L10), 640 x 512 complex128 symmetric, n=327680",
+    "cfg3alt": "configs[3] alt (L10): 3x6x10 grid, 432 x 512 complex128, n=221184",
+    "cfg4": "configs[4]: configs[3] matrix, 10 x 1000 complex128 RHS",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("DD_BENCH_CONFIG", "cfg3"))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--refine", type=int, default=1)
+    ap.add_argument("--nrhs", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--trace-out", default=None, help="write the per-kernel trace JSON here")
+    return ap.parse_args()
+
+
+def fp64_peak(cplx):
+    """Measured FP64 tensor peak (TFLOP/s): cuBLAS DGEMM / ZGEMM 8192^3 (tools/fp64_peak.py)."""
+    path = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
+    d = json.load(open(path))
+    return (d["zgemm_tflops_burst"] if cplx else d["dgemm_tflops_burst"]), os.path.relpath(path, ROOT)
+
+
+class Clocks:
+    """nvidia-smi sampler (B200_PROFILING.md clocks line) running during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(gpu_index)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.count(",") >= 8]
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        mhz = sorted(float(r[1]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip().lower() == "active"})
+        return {"sm_mhz": mhz[len(mhz) // 2], "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def oracle_sample(prob, cfg):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload."""
+    import oracle
+    from oracle.block_ldlt import flops_factor
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    keep = dd_inputs.corner_interfaces(prob, SAMPLE_GRID[cfg])
+    sub = dd_inputs.subproblem(prob, keep)
+    order = list(range(sub.nblk))
+    t0 = time.perf_counter()
+    F = oracle.block_factor(sub, order)
+    dt = time.perf_counter() - t0
+    mu = 4 if sub.is_complex else 1
+    fl = flops_factor(sub.blk_size, F.sym, mu)
+    g = SAMPLE_GRID[cfg]
+    sample = (f"oracle.block_factor on the principal sub-matrix of the {len(keep)} interfaces inside the "
+              f"{g[0]}x{g[1]}x{g[2]} corner sub-grid of this workload (n={sub.n}, same bytes), natural order, "
+              f"{fl:.3g} algorithmic flops, {dt:.2f} s")
+    return {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": int(cores), "kind": "oracle", "sample": sample,
+            "seconds": dt}
+
+
+def dist_setup(args):
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo" if args.impl == "reference" else "nccl")
+        pg = dist
+    return rank, world, local, pg
+
+
+def reference_arm(args, rank, world):
+    """The oracle on the box's host cores; rank 0 only (others exit 0 without work)."""
+    if rank != 0:
+        return
+    cfg = args.config
+    try:
+        import torch
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+    except Exception:
+        dev = "cpu"
+    c = dd_inputs.CONFIGS[cfg]
+    if dev == "cuda":  # same bytes as our arm's workload, carved on the device
+        prob = dd_inputs.config(cfg, seed=args.seed, backend="torch", device="cuda")
+    else:
+        prob = dd_inputs.config(cfg, seed=args.seed, grid=SAMPLE_GRID[cfg])
+    for _ in range(args.warmup):
+        oracle_sample(prob, cfg)
+    vals, secs = [], 0.0
+    cb = None
+    for _ in range(args.steps):
+        cb = oracle_sample(prob, cfg)
+        vals.append(cb["value"])
+        secs += cb["seconds"]
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": "aux-matrix LDL^T factor FP64 GFLOP/s (% of FP64 peak); solve ms per 1000 RHS",
+            "value": v, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": secs * 1e3 / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128" if c["complex_"] else "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD_TXT[cfg], "nrhs": c["nrhs"], "sample": SAMPLE_GRID[cfg]},
+            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cb["cores"], "kind": "oracle", "sample": cb["sample"]},
+            "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def gpu_arm(args, rank, world, local, dist):
+    import torch
+    import paper_2002_05019_b200 as dd
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = args.config
+    c = dd_inputs.CONFIGS[cfg]
+    nrhs = args.nrhs or c["nrhs"]
+    t0 = time.time()
+    prob = dd_inputs.config(cfg, seed=args.seed + rank, backend="torch", device=str(dev))
+    torch.cuda.synchronize()
+    gen_s = time.time() - t0
+    cplx = prob.is_complex
+    order = dd.DD_ORDER_ND if c["order"] == "nd" else dd.DD_ORDER_AUTO
+    t0 = time.time()
+    solver = dd.AuxSolver(prob.blk_size, prob.colptr, prob.rowidx, complex_=cplx, order=order,
+                          refine_steps=args.refine, device=str(dev))
+    analyze_s = time.time() - t0
+    info = solver.info
+    vals = prob.values
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + args.seed + rank)
+    tdt = torch.complex128 if cplx else torch.float64
+    Bsrc = torch.randn((nrhs, prob.n), dtype=tdt, device=dev, generator=gen).t()  # column-major n x nrhs
+    Bw = torch.empty((nrhs, prob.n), dtype=tdt, device=dev).t()
+    solver.factor(vals, prob.val_offset)  # allocates factor/work buffers
+    solver._work(max(info["work_bytes"], dd.dd_aux_solve_work_bytes(solver.h, nrhs)))
+    stream = torch.cuda.current_stream()
+
+    def step(ev):
+        ev[0].record(stream)
+        rc, fi = solver.factor(vals, prob.val_offset)
+        if rc != dd.DD_OK:
+            raise RuntimeError(f"factor rc={rc}")
+        ev[1].record(stream)
+        Bw.copy_(Bsrc)
+        ev[2].record(stream)
+        solver.solve_(Bw)
+        ev[3].record(stream)
+        return fi
+
+    mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(4)]  # noqa: E731
+    for _ in range(args.warmup):
+        step(mk())
+    torch.cuda.synchronize()
+    dd.dd_aux_set_trace(solver.h, True)
+    dd.dd_aux_get_trace(solver.h, reset=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [mk() for _ in range(args.steps)]
+    start.record(stream)
+    finfo = None
+    for k in range(args.steps):
+        finfo = step(evs[k])
+    end.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = start.elapsed_time(end)
+    fac_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
+    sol_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
+    trace = dd.dd_aux_get_trace(solver.h, reset=True)
+    dd.dd_aux_set_trace(solver.h, False)
+
+    # ---- max over ranks (device-timed), NCCL all-reduce of three scalars (plumbing only)
+    tm = torch.tensor([total_ms, fac_ms, sol_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    total_ms, fac_ms, sol_ms = [float(x) for x in tm.tolist()]
+
+    K = args.steps
+    flops = info["flops_factor"]
+    value = world * flops * K / (fac_ms * 1e-3) / 1e9
+    peak_tf, peak_src = fp64_peak(cplx)
+    # ---- roofline of the dominant kernel (largest device time in the step)
+    dom = max(trace, key=lambda p: trace[p]["ms"])
+    dk = trace[dom]
+    achieved = dk["flops"] / (dk["ms"] * 1e-3) / 1e12 if dk["ms"] > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{cfg}.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    step_ms = total_ms / K
+
+    # ---- e2e: host buffers through the public API (H2D inputs, D2H result inside the region)
+    e2e = None
+    if not args.no_e2e:
+        vh = vals.cpu().pin_memory()
+        bh = Bsrc.t().contiguous().cpu().pin_memory()  # (nrhs, n) row-major == column-major n x nrhs
+        xh = torch.empty_like(bh).pin_memory()
+        evs2 = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        torch.cuda.synchronize()
+        evs2[0].record(stream)
+        vals.copy_(vh, non_blocking=True)
+        rc, _ = solver.factor(vals, prob.val_offset)
+        evs2[1].record(stream)
+        Bw.t().copy_(bh, non_blocking=True)
+        solver.solve_(Bw)
+        xh.copy_(Bw.t(), non_blocking=True)
+        evs2[2].record(stream)
+        torch.cuda.synchronize()
+        f_ms = evs2[0].elapsed_time(evs2[1])
+        s_ms = evs2[1].elapsed_time(evs2[2])
+        e2e = {"value": world * flops / (f_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(vh.numel() * vh.element_size() + bh.numel() * bh.element_size()),
+               "d2h_bytes_per_step": int(xh.numel() * xh.element_size()),
+               "solve_ms_per_1000_rhs": s_ms * 1000.0 / nrhs, "factor_ms": f_ms}
+        del vh, bh, xh
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_sample(prob, cfg)
+        cpu.pop("seconds", None)
+    launches = sum(v["launches"] for v in trace.values())
+    line = {
+        "metric": "aux-matrix LDL^T factor FP64 GFLOP/s (% of FP64 peak); solve ms per 1000 RHS",
+        "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128" if cplx else "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD_TXT[cfg], "n": prob.n, "nblk": prob.nblk, "nrhs": nrhs,
+                   "order": ["auto", "nd", "mindeg", "natural", "user"][info["order_used"]],
+                   "levels": info["n_levels"], "refine_steps": args.refine,
+                   "l2": "inputs larger than L2 (no flush needed)",
+                   "parallelism": "replicas" if world > 1 else "single GPU"},
+        "factor_ms": fac_ms / K, "factor_frac_of_fp64_peak": value / world / 1e3 / peak_tf,
+        "solve_ms_per_1000_rhs": sol_ms / K * 1000.0 / nrhs, "solve_ms_per_batch": sol_ms / K,
+        "flops_factor": flops, "flops_solve_per_rhs": info["flops_solve_per_rhs"],
+        "roofline": {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": achieved / peak_tf, "traffic": traffic,
+                     "peak_src": f"measured cuBLAS {'ZGEMM' if cplx else 'DGEMM'} 8192^3 ({peak_src})"},
+        "phases": {p: {"ms_per_step": v["ms"] / K, "launches_per_step": v["launches"] / K,
+                       "tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["ms"] > 0 and v["flops"] > 0 else None}
+                   for p, v in trace.items() if v["launches"]},
+        "gpu_launches": launches,
+        "clocks": clk, "cpu_baseline": cpu, "e2e": e2e,
+        "setup_s": {"generate": gen_s, "analyze": analyze_s},
+    }
+    if args.trace_out:
+        json.dump({"trace": trace, "line": line}, open(args.trace_out, "w"), indent=1)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local, dist = dist_setup(args)
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+    else:
+        gpu_arm(args, rank, world, local, dist)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,6 +1,9 @@
 """Build libdd_aux.so in-tree with nvcc for sm_100a (no torch types in the library).
 
-    python -m paper_2002_05019_b200._build [--force] [--verbose]
+    python dd_build.py [--force] [--verbose]
+
+Kept outside the package on purpose: importing paper_2002_05019_b200 loads the
+library eagerly and fails loudly when it is missing or stale.
 """
 from __future__ import annotations
 
@@ -9,9 +12,9 @@ import os
 import subprocess
 import sys
 
-HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.abspath(__file__))
+HERE = os.path.join(ROOT, "paper_2002_05019_b200")
 CSRC = os.path.join(HERE, "csrc")
-ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libdd_aux.so")
 SOURCES = ["api.cu", "kernels_factor.cu", "kernels_solve.cu", "analyze.cpp"]
 HEADERS = ["analyze.hpp", "layout.hpp", "launch.hpp", "common.cuh", "gemm_core.cuh"]

@@ -77,7 +77,9 @@ class Problem:
 
     @property
     def is_complex(self) -> bool:
-        return np.iscomplexobj(self.values)
+        if isinstance(self.values, np.ndarray):
+            return np.iscomplexobj(self.values)
+        return bool(self.values.is_complex())  # torch tensor (device-resident values)
 
     @property
     def dof_offset(self) -> np.ndarray:
@@ -226,7 +228,11 @@ def build_problem(nx, ny, nz, sizes_fn, *, complex_=False, seed=0, topology="fac
     colptr, rowidx = block_pattern_from_cliques(nblk, [c for _, c in cliques])
     val_offset, total = _layout(blk_size, colptr, rowidx)
     dtype = np.complex128 if complex_ else np.float64
-    values = np.zeros(total, dtype=dtype)
+    if backend == "torch":
+        import torch
+        values = torch.zeros(total, dtype=torch.complex128 if complex_ else torch.float64, device=device)
+    else:
+        values = np.zeros(total, dtype=dtype)
     pos = {}
     for j in range(nblk):
         for p in range(int(colptr[j]), int(colptr[j + 1])):
@@ -265,7 +271,6 @@ def build_problem(nx, ny, nz, sizes_fn, *, complex_=False, seed=0, topology="fac
             S = G.transpose(0, 1) @ (d[:, None] * G)
             S = S + sigma * torch.eye(m, dtype=tdt, device=device)
             S = 0.5 * (S + S.transpose(0, 1))
-            S = S.cpu().numpy()
         offs = np.concatenate([[0], np.cumsum([blk_size[I] for I in members])])
         for a, I in enumerate(members):
             for b, J in enumerate(members):
@@ -274,9 +279,62 @@ def build_problem(nx, ny, nz, sizes_fn, *, complex_=False, seed=0, topology="fac
                 blk = S[offs[a]:offs[a + 1], offs[b]:offs[b + 1]]
                 pp = pos[(I, J)]
                 si, sj = int(blk_size[I]), int(blk_size[J])
-                dst = values[val_offset[pp]:val_offset[pp] + si * sj].reshape(sj, si).T
-                dst += blk
-    return Problem(blk_size, colptr, rowidx, values, val_offset, cliques, name)
+                if backend == "torch":
+                    values[val_offset[pp]:val_offset[pp] + si * sj].view(sj, si).add_(blk.transpose(0, 1))
+                else:
+                    dst = values[val_offset[pp]:val_offset[pp] + si * sj].reshape(sj, si).T
+                    dst += blk
+    prob = Problem(blk_size, colptr, rowidx, values, val_offset, cliques, name)
+    prob.pairs = pairs
+    prob.grid = (nx, ny, nz)
+    return prob
+
+
+def corner_interfaces(prob: Problem, sub_grid) -> List[int]:
+    """Interfaces whose two subdomains both lie in the corner sub-grid [0,gx)x[0,gy)x[0,gz)."""
+    nx, ny, _ = prob.grid
+    gx, gy, gz = sub_grid
+
+    def inside(p):
+        x, y, z = p % nx, (p // nx) % ny, p // (nx * ny)
+        return x < gx and y < gy and z < gz
+
+    return [I for I, (p, q) in enumerate(prob.pairs) if inside(p) and inside(q)]
+
+
+def subproblem(prob: Problem, keep) -> Problem:
+    """Principal sub-matrix on the interface subset `keep` (renumbered ascending), host numpy values.
+
+    Used only to carve a BOUNDED sample of a large workload for the CPU oracle timing
+    (bench.py cpu_baseline); pure data movement.
+    """
+    keep = sorted(int(k) for k in keep)
+    new = {old: i for i, old in enumerate(keep)}
+    blocks = []
+    for j in keep:
+        for p in range(int(prob.colptr[j]), int(prob.colptr[j + 1])):
+            i = int(prob.rowidx[p])
+            if i in new:
+                blocks.append((new[j], new[i], p))
+    blocks.sort()
+    nb = len(keep)
+    sizes = np.asarray([prob.blk_size[k] for k in keep], dtype=np.int64)
+    colptr = np.zeros(nb + 1, dtype=np.int64)
+    rowidx = np.zeros(len(blocks), dtype=np.int32)
+    offs = np.zeros(len(blocks), dtype=np.int64)
+    chunks = []
+    tot = 0
+    for q, (jn, in_, p) in enumerate(blocks):
+        colptr[jn + 1] += 1
+        rowidx[q] = in_
+        offs[q] = tot
+        ln = int(prob.blk_size[prob.rowidx[p]]) * int(prob.blk_size[keep[jn]])
+        seg = prob.values[int(prob.val_offset[p]):int(prob.val_offset[p]) + ln]
+        chunks.append(seg if isinstance(seg, np.ndarray) else seg.cpu().numpy())
+        tot += ln
+    colptr = np.cumsum(colptr)
+    vals = np.concatenate(chunks) if chunks else np.zeros(0)
+    return Problem(sizes, colptr, rowidx, vals, offs, [], prob.name + "-sample")
 
 
 def random_rhs(n: int, nrhs: int, complex_: bool, seed: int) -> np.ndarray:

@@ -149,6 +149,24 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
  * Entries are grouped by elimination position (block order[0] first).  Any pointer may be NULL. */
 int dd_aux_get_pivots(dd_aux_handle_t h, const void* d_factor, int32_t* ipiv, int32_t* perm, void* d, void* e);
 
+/* Tracing (SURVEY.md §5 "CUDA events per phase").  Launch counts and algorithmic flops per
+ * kernel class are always accumulated; with tracing enabled every kernel launch is also
+ * bracketed by a CUDA-event pair recorded on the launching stream, so ms[] is device time.
+ * dd_aux_get_trace synchronizes the recorded events, returns the sums since the last reset
+ * and resets them when reset != 0. */
+enum {
+  DD_PH_LOAD = 0, DD_PH_K1, DD_PH_ROWPERM, DD_PH_K2, DD_PH_K3, DD_PH_STATS,
+  DD_PH_PERM, DD_PH_FDIAG, DD_PH_FUPD, DD_PH_DSOLVE, DD_PH_BUPD, DD_PH_BDIAG, DD_PH_SPMV,
+  DD_NPHASE
+};
+typedef struct {
+  double ms[16];        /* device milliseconds per kernel class (tracing enabled only) */
+  int64_t launches[16]; /* kernel launches per class                                     */
+  double flops[16];     /* algorithmic flops per class (SURVEY.md §8(d) formulas)          */
+} dd_aux_trace;
+int dd_aux_set_trace(dd_aux_handle_t h, int32_t enable);
+int dd_aux_get_trace(dd_aux_handle_t h, dd_aux_trace* out, int32_t reset);
+
 int dd_aux_destroy(dd_aux_handle_t h);
 
 const char* dd_aux_last_error(void);

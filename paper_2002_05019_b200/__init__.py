@@ -20,7 +20,7 @@ __all__ = ["DD_REAL64", "DD_COMPLEX128", "DD_ORDER_AUTO", "DD_ORDER_ND", "DD_ORD
            "DD_ORDER_USER", "DD_OK", "DD_ZERO_PIVOT", "DDAuxError", "dd_aux_default_options", "dd_aux_analyze",
            "dd_aux_get_info", "dd_aux_get_order", "dd_aux_get_etree", "dd_aux_solve_work_bytes", "dd_aux_factor",
            "dd_aux_solve", "dd_aux_get_pivots", "dd_aux_destroy", "dd_aux_last_error", "dd_aux_version",
-           "AuxSolver", "LIB_PATH", "EXPORTED_SYMBOLS"]
+           "dd_aux_set_trace", "dd_aux_get_trace", "AuxSolver", "LIB_PATH", "EXPORTED_SYMBOLS", "PHASES"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdd_aux.so")
 
@@ -31,7 +31,10 @@ DD_ERR_CUDA, DD_ERR_WORKSPACE, DD_ERR_NOT_FACTORED, DD_ERR_SINGULAR, DD_ERR_PATT
 
 EXPORTED_SYMBOLS = ["dd_aux_default_options", "dd_aux_analyze", "dd_aux_get_info", "dd_aux_get_order",
                     "dd_aux_get_etree", "dd_aux_solve_work_bytes", "dd_aux_factor", "dd_aux_solve",
-                    "dd_aux_get_pivots", "dd_aux_destroy", "dd_aux_last_error", "dd_aux_version"]
+                    "dd_aux_get_pivots", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_destroy",
+                    "dd_aux_last_error", "dd_aux_version"]
+PHASES = ["load", "k1_diag_bk", "rowperm", "k2_panel", "k3_update", "stats", "perm", "fdiag", "fupd", "dsolve",
+          "bupd", "bdiag", "spmv"]
 
 
 class DDAuxError(RuntimeError):
@@ -60,9 +63,13 @@ class dd_aux_factor_info(ctypes.Structure):
                 ("ms_load", ctypes.c_float), ("ms_factor", ctypes.c_float)]
 
 
+class dd_aux_trace(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * 16), ("launches", ctypes.c_int64 * 16), ("flops", ctypes.c_double * 16)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        raise ImportError(f"{LIB_PATH} is not built; run `python dd_build.py`")
     lib = ctypes.CDLL(LIB_PATH)
     P = ctypes.c_void_p
     i64, i32 = ctypes.c_int64, ctypes.c_int32
@@ -78,6 +85,8 @@ def _load():
         "dd_aux_factor": (ctypes.c_int, [P, P, pi64, P, P, P, ctypes.POINTER(dd_aux_factor_info)]),
         "dd_aux_solve": (ctypes.c_int, [P, P, P, i64, P, i64, P, P]),
         "dd_aux_get_pivots": (ctypes.c_int, [P, P, pi32, pi32, P, P]),
+        "dd_aux_set_trace": (ctypes.c_int, [P, i32]),
+        "dd_aux_get_trace": (ctypes.c_int, [P, ctypes.POINTER(dd_aux_trace), i32]),
         "dd_aux_destroy": (ctypes.c_int, [P]),
         "dd_aux_last_error": (ctypes.c_char_p, []),
         "dd_aux_version": (ctypes.c_char_p, []),
@@ -212,6 +221,17 @@ def dd_aux_get_pivots(h, d_factor, cplx=False) -> dict:
     _check(_lib.dd_aux_get_pivots(h, _dev_ptr(d_factor), _np_ptr(ipiv, ctypes.c_int32), _np_ptr(perm, ctypes.c_int32),
                                   ctypes.c_void_p(d.ctypes.data), ctypes.c_void_p(e.ctypes.data)))
     return dict(ipiv=ipiv, perm=perm, d=d, e=e)
+
+
+def dd_aux_set_trace(h, enable=True):
+    _check(_lib.dd_aux_set_trace(h, int(bool(enable))))
+
+
+def dd_aux_get_trace(h, reset=True) -> dict:
+    """{phase: {"ms", "launches", "flops"}} since the last reset (synchronizes recorded events)."""
+    t = dd_aux_trace()
+    _check(_lib.dd_aux_get_trace(h, ctypes.byref(t), int(bool(reset))))
+    return {name: {"ms": t.ms[i], "launches": int(t.launches[i]), "flops": t.flops[i]} for i, name in enumerate(PHASES)}
 
 
 def dd_aux_destroy(h):

@@ -63,6 +63,8 @@ struct LevelRanges {
   int t0, t1;     // K3 tiles
   int f0, f1;     // forward-solve tiles
   int b0, b1;     // backward-solve tiles
+  double fl_k1, fl_k2, fl_k3;      // algorithmic flops of the level's factor kernels
+  double fl_diag, fl_upd;          // solve flops per rhs: one diagonal sweep / one update sweep
 };
 
 }  // namespace
@@ -102,7 +104,51 @@ struct dd_aux_handle_s {
   int64_t max_front = 0, max_width = 0;
   bool factored = false, singular = false;
   const void* factored_ptr = nullptr;
+  double nnz_full = 0;  // entries of the full symmetric A (K6 flops)
+  // tracing
+  bool trace = false;
+  std::vector<cudaEvent_t> pool;
+  struct Rec { int ph, e0, e1; };
+  std::vector<Rec> recs;
+  int64_t launches[16] = {0};
+  double flops[16] = {0};
+  double ms_acc[16] = {0};
+  int ev() {
+    int id = (int)recs.size() * 2;
+    while ((int)pool.size() < id + 2) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return id;
+  }
+  ~dd_aux_handle_s() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
 };
+
+namespace {
+// bracket one kernel launch: counts + flops always, CUDA events when tracing
+struct TraceScope {
+  dd_aux_handle_s* h;
+  int ph, id = -1;
+  cudaStream_t st;
+  TraceScope(dd_aux_handle_s* h_, int ph_, double fl, cudaStream_t st_) : h(h_), ph(ph_), st(st_) {
+    h->launches[ph] += 1;
+    h->flops[ph] += fl;
+    if (h->trace) {
+      id = h->ev();
+      cudaEventRecord(h->pool[id], st);
+    }
+  }
+  ~TraceScope() {
+    if (id >= 0) {
+      cudaEventRecord(h->pool[id + 1], st);
+      h->recs.push_back({ph, id, id + 1});
+    }
+  }
+};
+}  // namespace
 
 extern "C" {
 
@@ -368,6 +414,19 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
       if (h->nodes[t].nst > 0)
         for (int tm = 0; tm * SBM < h->nodes[t].s; ++tm) btiles.push_back(make_int2(t, tm));
     R.b1 = (int)btiles.size();
+    {
+      const double mu = h->cplx ? 4.0 : 1.0;
+      R.fl_k1 = R.fl_k2 = R.fl_k3 = R.fl_diag = R.fl_upd = 0;
+      for (int t : L) {
+        double sv = h->nodes[t].s, rv = 0;
+        for (int q = 0; q < h->nodes[t].nst; ++q) rv += h->nodes[st_pos[h->nodes[t].st0 + q]].s;
+        R.fl_k1 += mu * sv * sv * sv / 3.0;
+        R.fl_k2 += mu * rv * sv * sv;
+        R.fl_k3 += mu * rv * rv * sv;
+        R.fl_diag += mu * sv * sv;
+        R.fl_upd += mu * 2.0 * rv * sv;
+      }
+    }
     h->lv.push_back(R);
   }
   // K6 residual rows: block row I of the full symmetric A
@@ -381,6 +440,9 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
         rowsegs[j].push_back(SpSeg{p, i, 1});  // (j, i) = stored^T
       }
     }
+  for (int j = 0; j < N; ++j)
+    for (int64_t p = colptr[j]; p < colptr[j + 1]; ++p)
+      h->nnz_full += (double)blk_size[rowidx[p]] * blk_size[j] * (rowidx[p] == j ? 1.0 : 2.0);
   std::vector<SpRow> sprows;
   const int SPM = spmv_bm();
   for (int I = 0; I < N; ++I) {
@@ -567,8 +629,11 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   cudaEventRecord(e0, st);
   // ---- a1: zero the arena, load the caller's blocks
   CUDA_TRY(cudaMemsetAsync(arena, 0, (size_t)h->nA * (C ? 2 : 1) * sizeof(double), st));
-  launch_load(C, (const double*)d_vals, (const LoadBlock*)(Wb + h->w_off_load), (int)lbs.size(), max_elems, arena,
-              aim, st);
+  {
+    TraceScope ts(h, DD_PH_LOAD, 0.0, st);
+    launch_load(C, (const double*)d_vals, (const LoadBlock*)(Wb + h->w_off_load), (int)lbs.size(), max_elems, arena,
+                aim, st);
+  }
   LAUNCH_CHECK("k0_load");
   cudaEventRecord(e1, st);
 
@@ -594,24 +659,39 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   // ---- a2-a5: level-scheduled factorization
   for (const LevelRanges& R : h->lv) {
     k1.nodes = lvlnodes + R.n0;
-    launch_k1(C, k1, R.n1 - R.n0, st);
+    {
+      TraceScope ts(h, DD_PH_K1, R.fl_k1, st);
+      launch_k1(C, k1, R.n1 - R.n0, st);
+    }
     LAUNCH_CHECK("k1_diag_bk");
     RowpermArgs r = rp;
     r.list = rp.list + R.r0;
-    launch_rowperm(C, r, R.r1 - R.r0, h->max_s, st);
+    if (R.r1 > R.r0) {
+      TraceScope ts(h, DD_PH_ROWPERM, 0.0, st);
+      launch_rowperm(C, r, R.r1 - R.r0, h->max_s, st);
+    }
     LAUNCH_CHECK("k_rowperm");
     K2Args a2 = k2;
     a2.strips = k2.strips + R.s0;
-    launch_k2(C, a2, R.s1 - R.s0, st);
+    if (R.s1 > R.s0) {
+      TraceScope ts(h, DD_PH_K2, R.fl_k2, st);
+      launch_k2(C, a2, R.s1 - R.s0, st);
+    }
     LAUNCH_CHECK("k2_panel");
     K3Args a3 = k3;
     a3.tiles = k3.tiles + R.t0;
-    launch_k3(C, a3, R.t1 - R.t0, st);
+    if (R.t1 > R.t0) {
+      TraceScope ts(h, DD_PH_K3, R.fl_k3, st);
+      launch_k3(C, a3, R.t1 - R.t0, st);
+    }
     LAUNCH_CHECK("k3_update");
   }
   // ---- a6: statistics
   int64_t* totals_d = (int64_t*)(F + h->off_totals);
-  launch_k4((const int64_t*)(F + h->off_stats), N, totals_d, st);
+  {
+    TraceScope ts(h, DD_PH_STATS, 0.0, st);
+    launch_k4((const int64_t*)(F + h->off_stats), N, totals_d, st);
+  }
   LAUNCH_CHECK("k4_stats");
   cudaEventRecord(e2, st);
   int64_t totals[16] = {0};
@@ -663,22 +743,37 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
   for (const LevelRanges& R : h->lv) {
     SolveArgs b = a;
     b.nodes = lvlnodes + R.n0;
-    launch_fdiag(C, b, R.n1 - R.n0, st);
+    {
+      TraceScope ts(h, DD_PH_FDIAG, R.fl_diag * nrhs, st);
+      launch_fdiag(C, b, R.n1 - R.n0, st);
+    }
     LAUNCH_CHECK("k_fdiag");
     b.ftargets = a.ftargets + R.f0;
-    launch_fupd(C, b, R.f1 - R.f0, st);
+    if (R.f1 > R.f0) {
+      TraceScope ts(h, DD_PH_FUPD, R.fl_upd * nrhs, st);
+      launch_fupd(C, b, R.f1 - R.f0, st);
+    }
     LAUNCH_CHECK("k_fupd");
   }
-  launch_dsolve(C, a, st);
+  {
+    TraceScope ts(h, DD_PH_DSOLVE, 0.0, st);
+    launch_dsolve(C, a, st);
+  }
   LAUNCH_CHECK("k_dsolve");
   for (int l = (int)h->lv.size() - 1; l >= 0; --l) {
     const LevelRanges& R = h->lv[l];
     SolveArgs b = a;
     b.btiles = a.btiles + R.b0;
-    launch_bupd(C, b, R.b1 - R.b0, st);
+    if (R.b1 > R.b0) {
+      TraceScope ts(h, DD_PH_BUPD, R.fl_upd * nrhs, st);
+      launch_bupd(C, b, R.b1 - R.b0, st);
+    }
     LAUNCH_CHECK("k_bupd");
     b.nodes = lvlnodes + R.n0;
-    launch_bdiag(C, b, R.n1 - R.n0, st);
+    {
+      TraceScope ts(h, DD_PH_BDIAG, R.fl_diag * nrhs, st);
+      launch_bdiag(C, b, R.n1 - R.n0, st);
+    }
     LAUNCH_CHECK("k_bdiag");
   }
   return DD_OK;
@@ -716,19 +811,26 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
   pa.yim = yim;
   pa.ldy = ldy;
   if (refine > 0) {
+    TraceScope ts(h, DD_PH_PERM, 0.0, st);
     launch_copy(C, (const double*)d_B, ldb, Bsave, h->n, h->n, (int)nrhs, st);
     LAUNCH_CHECK("k_copy");
   }
   pa.src = (const double*)d_B;
   pa.lds = ldb;
-  launch_perm_in(C, pa, st);
+  {
+    TraceScope ts(h, DD_PH_PERM, 0.0, st);
+    launch_perm_in(C, pa, st);
+  }
   LAUNCH_CHECK("k_perm_in");
   int rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st);
   if (rc) return rc;
   pa.dst = (double*)d_B;
   pa.ldd = ldb;
   pa.accumulate = 0;
-  launch_perm_out(C, pa, st);
+  {
+    TraceScope ts(h, DD_PH_PERM, 0.0, st);
+    launch_perm_out(C, pa, st);
+  }
   LAUNCH_CHECK("k_perm_out");
   for (int r = 0; r < refine; ++r) {
     SpmvArgs sa{};
@@ -746,12 +848,18 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
     sa.yim = yim;
     sa.ldy = ldy;
     sa.nrhs = (int)nrhs;
-    launch_spmv(C, sa, h->n_sprows, st);
+    {
+      TraceScope ts(h, DD_PH_SPMV, (C ? 8.0 : 2.0) * h->nnz_full * (double)nrhs, st);
+      launch_spmv(C, sa, h->n_sprows, st);
+    }
     LAUNCH_CHECK("k_spmv");
     rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st);
     if (rc) return rc;
     pa.accumulate = 1;
-    launch_perm_out(C, pa, st);
+    {
+      TraceScope ts(h, DD_PH_PERM, 0.0, st);
+      launch_perm_out(C, pa, st);
+    }
     LAUNCH_CHECK("k_perm_out");
   }
   return DD_OK;
@@ -798,6 +906,37 @@ int dd_aux_get_pivots(dd_aux_handle_t h, const void* d_factor, int32_t* ipiv, in
           ((double*)e)[q] = ev[g];
         }
       }
+    }
+  }
+  return DD_OK;
+}
+
+int dd_aux_set_trace(dd_aux_handle_t h, int32_t enable) {
+  if (!h) return fail(-1, "handle is NULL");
+  h->trace = enable != 0;
+  return DD_OK;
+}
+
+int dd_aux_get_trace(dd_aux_handle_t h, dd_aux_trace* out, int32_t reset) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (!out) return fail(-2, "out is NULL");
+  for (auto& r : h->recs) {
+    CUDA_TRY(cudaEventSynchronize(h->pool[r.e1]));
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, h->pool[r.e0], h->pool[r.e1]));
+    h->ms_acc[r.ph] += ms;
+  }
+  h->recs.clear();
+  for (int q = 0; q < 16; ++q) {
+    out->ms[q] = h->ms_acc[q];
+    out->launches[q] = h->launches[q];
+    out->flops[q] = h->flops[q];
+  }
+  if (reset) {
+    for (int q = 0; q < 16; ++q) {
+      h->ms_acc[q] = 0;
+      h->launches[q] = 0;
+      h->flops[q] = 0;
     }
   }
   return DD_OK;
