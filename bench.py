@@ -135,6 +135,15 @@ def dist_setup(args):
     return rank, world, local, pg
 
 
+def reduce_max(values, dist, device="cpu"):
+    """Max over ranks of a few per-rank timings (barrier-bracketed device times)."""
+    import torch
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
 def reference_arm(args, rank, world):
     """The oracle on the box's host cores; rank 0 only (others exit 0 without work)."""
     if rank != 0:
@@ -239,10 +248,7 @@ def gpu_arm(args, rank, world, local, dist):
     dd.dd_aux_set_trace(solver.h, False)
 
     # ---- max over ranks (device-timed), NCCL all-reduce of three scalars (plumbing only)
-    tm = torch.tensor([total_ms, fac_ms, sol_ms], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-    total_ms, fac_ms, sol_ms = [float(x) for x in tm.tolist()]
+    total_ms, fac_ms, sol_ms = reduce_max([total_ms, fac_ms, sol_ms], dist, dev)
 
     K = args.steps
     flops = info["flops_factor"]

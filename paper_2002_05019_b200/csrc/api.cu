@@ -60,7 +60,8 @@ struct LevelRanges {
   int n0, n1;     // level nodes
   int s0, s1;     // K2 strips
   int r0, r1;     // rowperm entries
-  int t0, t1;     // K3 tiles
+  int t0, t1;     // K3 tiles: [t0, ta) update the next level's panels, [ta, t1) the rest
+  int ta;
   int f0, f1;     // forward-solve tiles
   int b0, b1;     // backward-solve tiles
   double fl_k1, fl_k2, fl_k3;      // algorithmic flops of the level's factor kernels
@@ -105,6 +106,10 @@ struct dd_aux_handle_s {
   bool factored = false, singular = false;
   const void* factored_ptr = nullptr;
   double nnz_full = 0;  // entries of the full symmetric A (K6 flops)
+  // lookahead: high-priority side stream + per-level events
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> evA, evB;
+  cudaEvent_t evLoad = nullptr;
   // tracing
   bool trace = false;
   std::vector<cudaEvent_t> pool;
@@ -124,6 +129,10 @@ struct dd_aux_handle_s {
   }
   ~dd_aux_handle_s() {
     for (auto e : pool) cudaEventDestroy(e);
+    for (auto e : evA) cudaEventDestroy(e);
+    for (auto e : evB) cudaEventDestroy(e);
+    if (evLoad) cudaEventDestroy(evLoad);
+    if (side) cudaStreamDestroy(side);
   }
 };
 
@@ -388,7 +397,15 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
         }
     }
     std::stable_sort(ltiles.begin(), ltiles.end(), [](auto& x, auto& y) { return x.first > y.first; });
-    for (auto& x : ltiles) tiles.push_back(x.second);
+    // lookahead split: (a) tiles of targets in panels of the NEXT level's nodes first, (b) the rest
+    std::vector<char> next(N, 0);
+    if (l + 1 < S.nlevels)
+      for (int t : S.level_nodes[l + 1]) next[t] = 1;
+    for (auto& x : ltiles)
+      if (next[targets[x.second.target].j]) tiles.push_back(x.second);
+    R.ta = (int)tiles.size();
+    for (auto& x : ltiles)
+      if (!next[targets[x.second.target].j]) tiles.push_back(x.second);
     R.t1 = (int)tiles.size();
     // forward-solve targets: y_i -= L_ik z_k over the level's contributors
     std::unordered_map<int, std::vector<SolveContrib>> fmap;
@@ -493,8 +510,8 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   o = align256(o + 16 * 8);
   h->factor_bytes = o;
   size_t w = 0;
-  h->w_off_W = w;
-  w = align256(w + (size_t)h->nW * planes * sizeof(double));
+  h->w_off_W = w;  // two W buffers (level parity) for the lookahead
+  w = align256(w + (size_t)h->nW * planes * sizeof(double) * 2);
   h->w_off_K1 = w;
   w = align256(w + (size_t)h->nK1 * planes * sizeof(double));
   h->w_off_load = w;
@@ -656,33 +673,80 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   K3Args k3{(const Tile*)(F + h->off_tiles), (const UpdTarget*)(F + h->off_targets),
             (const UpdContrib*)(F + h->off_contribs), dnodes, arena, aim, work, wim};
   const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
-  // ---- a2-a5: level-scheduled factorization
-  for (const LevelRanges& R : h->lv) {
+  // ---- a2-a5: level-scheduled factorization with a one-level lookahead.
+  // Main stream st: K3a(l) [targets in panels of level l+1] -> K3b(l) [the rest].
+  // Side stream (high priority): K1 / rowperm / K2 of level l+1 as soon as K3a(l) is done, so
+  // the sequential diagonal factorizations overlap the bulk Schur update of level l.
+  // W is double-buffered by level parity (K2(l+1) writes while K3b(l) still reads W(l)).
+  const int nL = (int)h->lv.size();
+  if (!h->side) {
+    int lo, hi;
+    CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->evLoad, cudaEventDisableTiming));
+  }
+  while ((int)h->evA.size() < nL) {
+    cudaEvent_t a, b;
+    CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    h->evA.push_back(a);
+    h->evB.push_back(b);
+  }
+  cudaStream_t sd = h->side;
+  const size_t wpar = (size_t)h->nW * (C ? 2 : 1);  // elements per parity buffer
+  auto diag_phase = [&](int l) -> int {              // K1 + rowperm + K2 of level l on the side stream
+    const LevelRanges& R = h->lv[l];
     k1.nodes = lvlnodes + R.n0;
     {
-      TraceScope ts(h, DD_PH_K1, R.fl_k1, st);
-      launch_k1(C, k1, R.n1 - R.n0, st);
+      TraceScope ts(h, DD_PH_K1, R.fl_k1, sd);
+      launch_k1(C, k1, R.n1 - R.n0, sd);
     }
     LAUNCH_CHECK("k1_diag_bk");
     RowpermArgs r = rp;
     r.list = rp.list + R.r0;
     if (R.r1 > R.r0) {
-      TraceScope ts(h, DD_PH_ROWPERM, 0.0, st);
-      launch_rowperm(C, r, R.r1 - R.r0, h->max_s, st);
+      TraceScope ts(h, DD_PH_ROWPERM, 0.0, sd);
+      launch_rowperm(C, r, R.r1 - R.r0, h->max_s, sd);
     }
     LAUNCH_CHECK("k_rowperm");
     K2Args a2 = k2;
     a2.strips = k2.strips + R.s0;
+    a2.work = work + (l & 1) * wpar;
     if (R.s1 > R.s0) {
-      TraceScope ts(h, DD_PH_K2, R.fl_k2, st);
-      launch_k2(C, a2, R.s1 - R.s0, st);
+      TraceScope ts(h, DD_PH_K2, R.fl_k2, sd);
+      launch_k2(C, a2, R.s1 - R.s0, sd);
     }
     LAUNCH_CHECK("k2_panel");
+    CUDA_TRY(cudaEventRecord(h->evB[l], sd));
+    return DD_OK;
+  };
+  CUDA_TRY(cudaEventRecord(h->evLoad, st));
+  CUDA_TRY(cudaStreamWaitEvent(sd, h->evLoad, 0));
+  if (nL > 0) {
+    int rc = diag_phase(0);
+    if (rc) return rc;
+  }
+  for (int l = 0; l < nL; ++l) {
+    const LevelRanges& R = h->lv[l];
+    CUDA_TRY(cudaStreamWaitEvent(st, h->evB[l], 0));
     K3Args a3 = k3;
+    a3.work = work + (l & 1) * wpar;
     a3.tiles = k3.tiles + R.t0;
-    if (R.t1 > R.t0) {
+    if (R.ta > R.t0) {
+      TraceScope ts(h, DD_PH_K3, R.t1 > R.ta ? 0.0 : R.fl_k3, st);
+      launch_k3(C, a3, R.ta - R.t0, st);
+    }
+    LAUNCH_CHECK("k3_update");
+    CUDA_TRY(cudaEventRecord(h->evA[l], st));
+    if (l + 1 < nL) {
+      CUDA_TRY(cudaStreamWaitEvent(sd, h->evA[l], 0));
+      int rc = diag_phase(l + 1);
+      if (rc) return rc;
+    }
+    a3.tiles = k3.tiles + R.ta;
+    if (R.t1 > R.ta) {
       TraceScope ts(h, DD_PH_K3, R.fl_k3, st);
-      launch_k3(C, a3, R.t1 - R.t0, st);
+      launch_k3(C, a3, R.t1 - R.ta, st);
     }
     LAUNCH_CHECK("k3_update");
   }

@@ -190,17 +190,32 @@ struct Gemm {
         br[b] = Bs[o];
         if constexpr (CPLX) bi[b] = Bs[B_TILE + o];
       }
+      // Issue order: every product class over all (a, b) before the next class, so two
+      // DMMAs into the same accumulator are MI*NI instructions apart (no dependency stall).
 #pragma unroll
       for (int a = 0; a < MI; ++a)
 #pragma unroll
-        for (int b = 0; b < NI; ++b) {
-          dmma16x8x4(acc.r[a][b], ar[a][0], ar[a][1], br[b]);
-          if constexpr (CPLX) {
-            dmma16x8x4(acc.r[a][b], dneg(ai[a][0]), dneg(ai[a][1]), bi[b]);
-            dmma16x8x4(acc.i[a][b], ar[a][0], ar[a][1], bi[b]);
-            dmma16x8x4(acc.i[a][b], ai[a][0], ai[a][1], br[b]);
-          }
+        for (int b = 0; b < NI; ++b) dmma16x8x4(acc.r[a][b], ar[a][0], ar[a][1], br[b]);
+      if constexpr (CPLX) {
+#pragma unroll
+        for (int a = 0; a < MI; ++a)
+#pragma unroll
+          for (int b = 0; b < NI; ++b) dmma16x8x4(acc.i[a][b], ar[a][0], ar[a][1], bi[b]);
+        double nai[MI][2];
+#pragma unroll
+        for (int a = 0; a < MI; ++a) {
+          nai[a][0] = dneg(ai[a][0]);
+          nai[a][1] = dneg(ai[a][1]);
         }
+#pragma unroll
+        for (int a = 0; a < MI; ++a)
+#pragma unroll
+          for (int b = 0; b < NI; ++b) dmma16x8x4(acc.r[a][b], nai[a][0], nai[a][1], bi[b]);
+#pragma unroll
+        for (int a = 0; a < MI; ++a)
+#pragma unroll
+          for (int b = 0; b < NI; ++b) dmma16x8x4(acc.i[a][b], ai[a][0], ai[a][1], br[b]);
+      }
     }
   }
 
