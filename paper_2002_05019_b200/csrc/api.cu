@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -108,6 +109,8 @@ struct dd_aux_handle_s {
   double nnz_full = 0;  // entries of the full symmetric A (K6 flops)
   // lookahead: high-priority side stream + per-level events
   cudaStream_t side = nullptr;
+  int k3cfg = 1;           // K3 tile configuration (env DD_AUX_K3CFG, read at analyze)
+  bool lookahead = true;   // env DD_AUX_LOOKAHEAD=0 disables the side-stream overlap
   std::vector<cudaEvent_t> evA, evB;
   cudaEvent_t evLoad = nullptr;
   // tracing
@@ -330,7 +333,13 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   std::vector<SolveTarget> ftargets;
   std::vector<SolveContrib> fcontribs;
   std::vector<int2> btiles;
-  const int BM3 = k3_bm(h->cplx), BN3 = k3_bn(h->cplx), SBM = solve_bm(h->cplx);
+  {
+    const char* ev = getenv("DD_AUX_K3CFG");
+    h->k3cfg = ev ? atoi(ev) : 1;
+    const char* la = getenv("DD_AUX_LOOKAHEAD");
+    h->lookahead = la ? atoi(la) != 0 : true;
+  }
+  const int BM3 = k3_bm(h->cplx, h->k3cfg), BN3 = k3_bn(h->cplx, h->k3cfg), SBM = solve_bm(h->cplx);
   const int K2BM = 64;
   for (int l = 0; l < S.nlevels; ++l) {
     LevelRanges R{};
@@ -692,7 +701,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     h->evA.push_back(a);
     h->evB.push_back(b);
   }
-  cudaStream_t sd = h->side;
+  cudaStream_t sd = h->lookahead ? h->side : st;
   const size_t wpar = (size_t)h->nW * (C ? 2 : 1);  // elements per parity buffer
   auto diag_phase = [&](int l) -> int {              // K1 + rowperm + K2 of level l on the side stream
     const LevelRanges& R = h->lv[l];
@@ -734,7 +743,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     a3.tiles = k3.tiles + R.t0;
     if (R.ta > R.t0) {
       TraceScope ts(h, DD_PH_K3, R.t1 > R.ta ? 0.0 : R.fl_k3, st);
-      launch_k3(C, a3, R.ta - R.t0, st);
+      launch_k3(C, h->k3cfg, a3, R.ta - R.t0, st);
     }
     LAUNCH_CHECK("k3_update");
     CUDA_TRY(cudaEventRecord(h->evA[l], st));
@@ -746,7 +755,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     a3.tiles = k3.tiles + R.ta;
     if (R.t1 > R.ta) {
       TraceScope ts(h, DD_PH_K3, R.fl_k3, st);
-      launch_k3(C, a3, R.t1 - R.ta, st);
+      launch_k3(C, h->k3cfg, a3, R.t1 - R.ta, st);
     }
     LAUNCH_CHECK("k3_update");
   }

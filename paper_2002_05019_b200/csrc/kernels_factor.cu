@@ -501,14 +501,38 @@ __global__ void __launch_bounds__(NT2) k2_panel(K2Args a) {
 }
 
 // ============================================================================ K3 Schur update
-constexpr int NT3 = 256;
-using K3GemmR = Gemm<128, 128, 16, 2, 4, 4, false, false, false>;
-using K3GemmC = Gemm<64, 128, 16, 2, 4, 3, true, false, false>;
+// Tile configurations (selected at analyze time; env DD_AUX_K3CFG):
+//   0: real 128x128 / complex 64x128, 8 warps, 1 CTA per SM
+//   1: real 128x64  / complex 64x64,  4 warps, 2 CTAs per SM (prologue/epilogue of one CTA
+//      overlap the MMA of the other)
+template <bool C, int CFG>
+struct K3Cfg;
+template <>
+struct K3Cfg<false, 0> {
+  using G = Gemm<128, 128, 16, 2, 4, 4, false, false, false>;
+  static constexpr int NT = 256, BM = 128, BN = 128, MINB = 1;
+};
+template <>
+struct K3Cfg<true, 0> {
+  using G = Gemm<64, 128, 16, 2, 4, 3, true, false, false>;
+  static constexpr int NT = 256, BM = 64, BN = 128, MINB = 1;
+};
+template <>
+struct K3Cfg<false, 1> {
+  using G = Gemm<128, 64, 16, 2, 2, 3, false, false, false>;
+  static constexpr int NT = 128, BM = 128, BN = 64, MINB = 2;
+};
+template <>
+struct K3Cfg<true, 1> {
+  using G = Gemm<64, 64, 16, 2, 2, 3, true, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 2;
+};
 
-template <bool C>
-__global__ void __launch_bounds__(NT3, 1) k3_update(K3Args a) {
-  using G = typename std::conditional<C, K3GemmC, K3GemmR>::type;
-  constexpr int BM = C ? 64 : 128, BN = 128;
+template <bool C, int CFG>
+__global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_update(K3Args a) {
+  using Cf = K3Cfg<C, CFG>;
+  using G = typename Cf::G;
+  constexpr int BM = Cf::BM, BN = Cf::BN;
   extern __shared__ __align__(16) double smem[];
   const Tile T = a.tiles[blockIdx.x];
   const UpdTarget tg = a.targets[T.target];
@@ -625,17 +649,28 @@ void launch_k2(bool cplx, const K2Args& a, int nstrips, cudaStream_t st) {
   }
 }
 
-int k3_bm(bool cplx) { return cplx ? 64 : 128; }
-int k3_bn(bool) { return 128; }
+int k3_bm(bool cplx, int cfg) {
+  return cfg == 1 ? (cplx ? K3Cfg<true, 1>::BM : K3Cfg<false, 1>::BM) : (cplx ? K3Cfg<true, 0>::BM : K3Cfg<false, 0>::BM);
+}
+int k3_bn(bool cplx, int cfg) {
+  return cfg == 1 ? (cplx ? K3Cfg<true, 1>::BN : K3Cfg<false, 1>::BN) : (cplx ? K3Cfg<true, 0>::BN : K3Cfg<false, 0>::BN);
+}
 
-void launch_k3(bool cplx, const K3Args& a, int ntiles, cudaStream_t st) {
+template <bool C, int CFG>
+static void launch_k3_t(const K3Args& a, int ntiles, cudaStream_t st) {
+  using Cf = K3Cfg<C, CFG>;
+  set_smem(k3_update<C, CFG>, Cf::G::SMEM_BYTES);
+  k3_update<C, CFG><<<ntiles, Cf::NT, Cf::G::SMEM_BYTES, st>>>(a);
+}
+
+void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st) {
   if (ntiles == 0) return;
-  if (cplx) {
-    set_smem(k3_update<true>, K3GemmC::SMEM_BYTES);
-    k3_update<true><<<ntiles, NT3, K3GemmC::SMEM_BYTES, st>>>(a);
+  if (cfg == 1) {
+    if (cplx) launch_k3_t<true, 1>(a, ntiles, st);
+    else launch_k3_t<false, 1>(a, ntiles, st);
   } else {
-    set_smem(k3_update<false>, K3GemmR::SMEM_BYTES);
-    k3_update<false><<<ntiles, NT3, K3GemmR::SMEM_BYTES, st>>>(a);
+    if (cplx) launch_k3_t<true, 0>(a, ntiles, st);
+    else launch_k3_t<false, 0>(a, ntiles, st);
   }
 }
 

@@ -116,9 +116,9 @@ size_t k1_smem(bool cplx);
 void launch_k1(bool cplx, const K1Args& a, int nnodes, cudaStream_t st);
 void launch_rowperm(bool cplx, const RowpermArgs& a, int nlist, int max_s, cudaStream_t st);
 void launch_k2(bool cplx, const K2Args& a, int nstrips, cudaStream_t st);
-int k3_bm(bool cplx);
-int k3_bn(bool cplx);
-void launch_k3(bool cplx, const K3Args& a, int ntiles, cudaStream_t st);
+int k3_bm(bool cplx, int cfg);
+int k3_bn(bool cplx, int cfg);
+void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st);
 void launch_k4(const int64_t* node_stats, int nnodes, int64_t* out, cudaStream_t st);
 
 int solve_bm(bool cplx);   // row tile of the forward/backward update kernels
