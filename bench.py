@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--refine", type=int, default=1)
+    ap.add_argument("--refine-tol", type=float, default=0.0,
+                    help="skip a refinement step on the device when every column has berr <= tol (0 = always)")
     ap.add_argument("--nrhs", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -96,6 +98,38 @@ class Clocks:
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip().lower() == "active"})
         return {"sm_mhz": mhz[len(mhz) // 2], "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
                 "samples": len(rows)}
+
+
+def berr_check(prob, Bsrc, X, ncols=8):
+    """Harness check (not the measured library): per-column backward error
+    ||A x - b||_inf / (||A||_inf ||x||_inf) on a few columns, fp64 torch matmuls over the
+    caller's original blocks (both triangles), moduli for complex (L6)."""
+    import torch
+    nrhs = X.shape[1]
+    cols = sorted(set(np.linspace(0, nrhs - 1, min(ncols, nrhs)).astype(int).tolist()))
+    x = X[:, cols].clone()
+    r = Bsrc[:, cols].clone()
+    rs = torch.zeros(prob.n, dtype=torch.float64, device=X.device)
+    off = prob.dof_offset
+    vals = prob.values
+    for j in range(prob.nblk):
+        for p in range(int(prob.colptr[j]), int(prob.colptr[j + 1])):
+            i = int(prob.rowidx[p])
+            si, sj = int(prob.blk_size[i]), int(prob.blk_size[j])
+            vo = int(prob.val_offset[p])
+            blk = vals[vo:vo + si * sj].view(sj, si).t()
+            oi, oj = int(off[i]), int(off[j])
+            if i == j:
+                S = torch.tril(blk) + torch.tril(blk, -1).t()
+                r[oi:oi + si] -= S @ x[oi:oi + si]
+                rs[oi:oi + si] += S.abs().sum(1)
+            else:
+                r[oi:oi + si] -= blk @ x[oj:oj + sj]
+                r[oj:oj + sj] -= blk.t() @ x[oi:oi + si]
+                rs[oi:oi + si] += blk.abs().sum(1)
+                rs[oj:oj + sj] += blk.abs().sum(0)
+    berr = r.abs().amax(0) / (rs.max() * x.abs().amax(0))
+    return float(berr.max()), cols
 
 
 def oracle_sample(prob, cfg):
@@ -195,7 +229,7 @@ def gpu_arm(args, rank, world, local, dist):
     order = dd.DD_ORDER_ND if c["order"] == "nd" else dd.DD_ORDER_AUTO
     t0 = time.time()
     solver = dd.AuxSolver(prob.blk_size, prob.colptr, prob.rowidx, complex_=cplx, order=order,
-                          refine_steps=args.refine, device=str(dev))
+                          refine_steps=args.refine, device=str(dev), refine_tol=args.refine_tol)
     analyze_s = time.time() - t0
     info = solver.info
     vals = prob.values
@@ -246,6 +280,17 @@ def gpu_arm(args, rank, world, local, dist):
     sol_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
     trace = dd.dd_aux_get_trace(solver.h, reset=True)
     dd.dd_aux_set_trace(solver.h, False)
+
+    # ---- accuracy evidence (harness, outside the timed region): berr of the timed result and of
+    # an unrefined solve of the same right-hand sides
+    berr, cols = berr_check(prob, Bsrc, Bw)
+    Bu = torch.empty((len(cols), prob.n), dtype=tdt, device=dev).t()
+    Bu.copy_(Bsrc[:, cols])
+    dd.dd_aux_set_refine(solver.h, 0, 0.0)
+    solver.solve_(Bu)
+    dd.dd_aux_set_refine(solver.h, args.refine, args.refine_tol)
+    berr0, _ = berr_check(prob, Bsrc[:, cols], Bu, ncols=len(cols))
+    del Bu
 
     # ---- max over ranks (device-timed), NCCL all-reduce of three scalars (plumbing only)
     total_ms, fac_ms, sol_ms = reduce_max([total_ms, fac_ms, sol_ms], dist, dev)
@@ -303,12 +348,16 @@ def gpu_arm(args, rank, world, local, dist):
         "dtype": "c128" if cplx else "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD_TXT[cfg], "n": prob.n, "nblk": prob.nblk, "nrhs": nrhs,
                    "order": ["auto", "nd", "mindeg", "natural", "user"][info["order_used"]],
-                   "levels": info["n_levels"], "refine_steps": args.refine,
+                   "levels": info["n_levels"], "refine_steps": args.refine, "refine_tol": args.refine_tol,
                    "l2": "inputs larger than L2 (no flush needed)",
                    "parallelism": "replicas" if world > 1 else "single GPU"},
         "factor_ms": fac_ms / K, "factor_frac_of_fp64_peak": value / world / 1e3 / peak_tf,
         "solve_ms_per_1000_rhs": sol_ms / K * 1000.0 / nrhs, "solve_ms_per_batch": sol_ms / K,
         "flops_factor": flops, "flops_solve_per_rhs": info["flops_solve_per_rhs"],
+        "accuracy": {"berr_max": berr, "berr_unrefined_max": berr0, "columns_checked": len(cols),
+                     "tolerance": 1e-12, "refine_steps": args.refine, "refine_tol": args.refine_tol,
+                     "pivots": {"n2x2": finfo["n2x2"], "nswaps": finfo["nswaps"]},
+                     "inertia": None if cplx else [finfo["npos"], finfo["nneg"], finfo["nzero"]]},
         "roofline": {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved / peak_tf, "traffic": traffic,
                      "peak_src": f"measured cuBLAS {'ZGEMM' if cplx else 'DGEMM'} 8192^3 ({peak_src})"},

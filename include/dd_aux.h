@@ -64,7 +64,9 @@ typedef struct {
   const int32_t* user_order;  /* [nblk] block elimination order for DD_ORDER_USER (copied) */
   int32_t refine_steps;       /* iterative-refinement steps in dd_aux_solve (default 1, L7) */
   int32_t use_graphs;         /* reserved (CUDA-graph capture of the level loop), default 0 */
-  int32_t reserved[4];
+  double refine_tol;          /* a refinement step is skipped (on the device, no host sync) when
+                                 every column already has berr <= refine_tol; 0 = always refine */
+  int32_t reserved[2];
 } dd_aux_options;
 
 typedef struct {
@@ -148,6 +150,9 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
  *  d, e  [n] diagonal and 2x2 sub-diagonal of D (scalar type of the handle; e = 0 off 2x2 firsts)
  * Entries are grouped by elimination position (block order[0] first).  Any pointer may be NULL. */
 int dd_aux_get_pivots(dd_aux_handle_t h, const void* d_factor, int32_t* ipiv, int32_t* perm, void* d, void* e);
+
+/* Change the refinement policy of an analyzed handle (same meaning as the options fields). */
+int dd_aux_set_refine(dd_aux_handle_t h, int32_t refine_steps, double refine_tol);
 
 /* Tracing (SURVEY.md §5 "CUDA events per phase").  Launch counts and algorithmic flops per
  * kernel class are always accumulated; with tracing enabled every kernel launch is also

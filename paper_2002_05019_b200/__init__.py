@@ -20,7 +20,7 @@ __all__ = ["DD_REAL64", "DD_COMPLEX128", "DD_ORDER_AUTO", "DD_ORDER_ND", "DD_ORD
            "DD_ORDER_USER", "DD_OK", "DD_ZERO_PIVOT", "DDAuxError", "dd_aux_default_options", "dd_aux_analyze",
            "dd_aux_get_info", "dd_aux_get_order", "dd_aux_get_etree", "dd_aux_solve_work_bytes", "dd_aux_factor",
            "dd_aux_solve", "dd_aux_get_pivots", "dd_aux_destroy", "dd_aux_last_error", "dd_aux_version",
-           "dd_aux_set_trace", "dd_aux_get_trace", "AuxSolver", "LIB_PATH", "EXPORTED_SYMBOLS", "PHASES"]
+           "dd_aux_set_refine", "dd_aux_set_trace", "dd_aux_get_trace", "AuxSolver", "LIB_PATH", "EXPORTED_SYMBOLS", "PHASES"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdd_aux.so")
 
@@ -31,7 +31,7 @@ DD_ERR_CUDA, DD_ERR_WORKSPACE, DD_ERR_NOT_FACTORED, DD_ERR_SINGULAR, DD_ERR_PATT
 
 EXPORTED_SYMBOLS = ["dd_aux_default_options", "dd_aux_analyze", "dd_aux_get_info", "dd_aux_get_order",
                     "dd_aux_get_etree", "dd_aux_solve_work_bytes", "dd_aux_factor", "dd_aux_solve",
-                    "dd_aux_get_pivots", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_destroy",
+                    "dd_aux_get_pivots", "dd_aux_set_refine", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_destroy",
                     "dd_aux_last_error", "dd_aux_version"]
 PHASES = ["load", "k1_diag_bk", "rowperm", "k2_panel", "k3_update", "stats", "perm", "fdiag", "fupd", "dsolve",
           "bupd", "bdiag", "spmv"]
@@ -45,7 +45,8 @@ class DDAuxError(RuntimeError):
 
 class dd_aux_options(ctypes.Structure):
     _fields_ = [("order", ctypes.c_int32), ("user_order", ctypes.POINTER(ctypes.c_int32)),
-                ("refine_steps", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+                ("refine_steps", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("refine_tol", ctypes.c_double),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class dd_aux_info(ctypes.Structure):
@@ -85,6 +86,7 @@ def _load():
         "dd_aux_factor": (ctypes.c_int, [P, P, pi64, P, P, P, ctypes.POINTER(dd_aux_factor_info)]),
         "dd_aux_solve": (ctypes.c_int, [P, P, P, i64, P, i64, P, P]),
         "dd_aux_get_pivots": (ctypes.c_int, [P, P, pi32, pi32, P, P]),
+        "dd_aux_set_refine": (ctypes.c_int, [P, i32, ctypes.c_double]),
         "dd_aux_set_trace": (ctypes.c_int, [P, i32]),
         "dd_aux_get_trace": (ctypes.c_int, [P, ctypes.POINTER(dd_aux_trace), i32]),
         "dd_aux_destroy": (ctypes.c_int, [P]),
@@ -134,11 +136,13 @@ def dd_aux_version() -> str:
     return _lib.dd_aux_version().decode()
 
 
-def dd_aux_default_options(order=DD_ORDER_AUTO, refine_steps=1, user_order=None) -> dd_aux_options:
+def dd_aux_default_options(order=DD_ORDER_AUTO, refine_steps=1, user_order=None, refine_tol=None) -> dd_aux_options:
     o = dd_aux_options()
     _lib.dd_aux_default_options(ctypes.byref(o))
     o.order = int(order)
     o.refine_steps = int(refine_steps)
+    if refine_tol is not None:
+        o.refine_tol = float(refine_tol)
     if user_order is not None:
         uo = np.ascontiguousarray(user_order, dtype=np.int32)
         o._user_order_keepalive = uo
@@ -223,6 +227,10 @@ def dd_aux_get_pivots(h, d_factor, cplx=False) -> dict:
     return dict(ipiv=ipiv, perm=perm, d=d, e=e)
 
 
+def dd_aux_set_refine(h, refine_steps, refine_tol=0.0):
+    _check(_lib.dd_aux_set_refine(h, int(refine_steps), float(refine_tol)))
+
+
 def dd_aux_set_trace(h, enable=True):
     _check(_lib.dd_aux_set_trace(h, int(bool(enable))))
 
@@ -247,11 +255,11 @@ class AuxSolver:
     """
 
     def __init__(self, blk_size, colptr, rowidx, complex_=False, order=DD_ORDER_AUTO, refine_steps=1,
-                 user_order=None, device="cuda"):
+                 user_order=None, device="cuda", refine_tol=None):
         import torch
         self.torch = torch
         self.cplx = bool(complex_)
-        self.opt = dd_aux_default_options(order, refine_steps, user_order)
+        self.opt = dd_aux_default_options(order, refine_steps, user_order, refine_tol)
         self.h = dd_aux_analyze(blk_size, colptr, rowidx, DD_COMPLEX128 if self.cplx else DD_REAL64, self.opt)
         self.info = dd_aux_get_info(self.h)
         self.device = device

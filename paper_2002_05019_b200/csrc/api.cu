@@ -98,7 +98,7 @@ struct dd_aux_handle_s {
   std::vector<LevelRanges> lv;
   // factor buffer offsets (bytes)
   size_t tables_bytes = 0, off_arena = 0, off_ipiv = 0, off_perm = 0, off_gperm = 0, off_ginv = 0, off_stats = 0,
-         off_totals = 0, factor_bytes = 0;
+         off_totals = 0, off_norm = 0, factor_bytes = 0;
   // work buffer offsets (bytes)
   size_t w_off_W = 0, w_off_K1 = 0, w_off_load = 0, work_bytes = 0;
   // info
@@ -109,6 +109,7 @@ struct dd_aux_handle_s {
   double nnz_full = 0;  // entries of the full symmetric A (K6 flops)
   // lookahead: high-priority side stream + per-level events
   cudaStream_t side = nullptr;
+  bool norm_valid = false;  // ||A||_inf of the current factorization's d_vals computed on device
   int k3cfg = 1;           // K3 tile configuration (env DD_AUX_K3CFG, read at analyze)
   bool lookahead = true;   // env DD_AUX_LOOKAHEAD=0 disables the side-stream overlap
   std::vector<cudaEvent_t> evA, evB;
@@ -189,6 +190,7 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   if (opt_in) opt = *opt_in;
   if (opt.order < DD_ORDER_AUTO || opt.order > DD_ORDER_USER) return fail(-6, "invalid order option");
   if (opt.refine_steps < 0) return fail(-6, "refine_steps must be >= 0");
+  if (!(opt.refine_tol >= 0)) return fail(-6, "refine_tol must be >= 0");
 
   dd_aux_handle_s* h = new (std::nothrow) dd_aux_handle_s();
   if (!h) return fail(DD_ERR_INTERNAL, "out of host memory");
@@ -517,6 +519,8 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   o = align256(o + (size_t)N * 8 * 8);
   h->off_totals = o;
   o = align256(o + 16 * 8);
+  h->off_norm = o;
+  o = align256(o + 8);
   h->factor_bytes = o;
   size_t w = 0;
   h->w_off_W = w;  // two W buffers (level parity) for the lookahead
@@ -577,6 +581,8 @@ int dd_aux_solve_work_bytes(dd_aux_handle_t h, int64_t nrhs, size_t* bytes) {
   const size_t ldy = (size_t)pad8(h->n_pad);
   size_t w = align256(ldy * (size_t)nrhs * planes * sizeof(double));   // y
   w += align256((size_t)h->n * (size_t)nrhs * planes * sizeof(double));  // saved B (refinement)
+  w += align256((size_t)nrhs * sizeof(double)) + 256;                    // per-column berr + flag
+  w += align256(bupd_part_bytes(h->cplx, (int)nrhs));                    // backward split-K partials
   *bytes = w;
   return DD_OK;
 }
@@ -594,6 +600,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   uint8_t* F = (uint8_t*)d_factor;
   uint8_t* Wb = (uint8_t*)d_work;
   h->factored = false;
+  h->norm_valid = false;
 
   // ---- tables: fill the value offsets of the K6 segments, upload everything
   {
@@ -793,7 +800,9 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
 }
 
 static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t yim, int64_t ldy, int nrhs,
-                       cudaStream_t st) {
+                       cudaStream_t st, double* part, const int* flag = nullptr) {
+  // with a device flag the sweep may be skipped: its flops are not counted (conservative trace)
+  const double fs = flag ? 0.0 : 1.0;
   const bool C = h->cplx;
   SolveArgs a{};
   a.nd = (const NodeDev*)(F + h->off_nodes);
@@ -812,18 +821,19 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
   a.d_off = h->d_off;
   a.e_off = h->e_off;
   a.nrows = h->n_pad;
+  a.flag = flag;
   const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
   for (const LevelRanges& R : h->lv) {
     SolveArgs b = a;
     b.nodes = lvlnodes + R.n0;
     {
-      TraceScope ts(h, DD_PH_FDIAG, R.fl_diag * nrhs, st);
+      TraceScope ts(h, DD_PH_FDIAG, R.fl_diag * nrhs * fs, st);
       launch_fdiag(C, b, R.n1 - R.n0, st);
     }
     LAUNCH_CHECK("k_fdiag");
     b.ftargets = a.ftargets + R.f0;
     if (R.f1 > R.f0) {
-      TraceScope ts(h, DD_PH_FUPD, R.fl_upd * nrhs, st);
+      TraceScope ts(h, DD_PH_FUPD, R.fl_upd * nrhs * fs, st);
       launch_fupd(C, b, R.f1 - R.f0, st);
     }
     LAUNCH_CHECK("k_fupd");
@@ -838,13 +848,13 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
     SolveArgs b = a;
     b.btiles = a.btiles + R.b0;
     if (R.b1 > R.b0) {
-      TraceScope ts(h, DD_PH_BUPD, R.fl_upd * nrhs, st);
-      launch_bupd(C, b, R.b1 - R.b0, st);
+      TraceScope ts(h, DD_PH_BUPD, R.fl_upd * nrhs * fs, st);
+      launch_bupd(C, b, R.b1 - R.b0, part, st);
     }
     LAUNCH_CHECK("k_bupd");
     b.nodes = lvlnodes + R.n0;
     {
-      TraceScope ts(h, DD_PH_BDIAG, R.fl_diag * nrhs, st);
+      TraceScope ts(h, DD_PH_BDIAG, R.fl_diag * nrhs * fs, st);
       launch_bdiag(C, b, R.n1 - R.n0, st);
     }
     LAUNCH_CHECK("k_bdiag");
@@ -895,7 +905,10 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
     launch_perm_in(C, pa, st);
   }
   LAUNCH_CHECK("k_perm_in");
-  int rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st);
+  double* berr_d = (double*)((uint8_t*)Bsave + align256((size_t)h->n * nrhs * planes * sizeof(double)));
+  int* flag_d = (int*)((uint8_t*)berr_d + align256((size_t)nrhs * sizeof(double)));
+  double* part = (double*)((uint8_t*)flag_d + 256);
+  int rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part);
   if (rc) return rc;
   pa.dst = (double*)d_B;
   pa.ldd = ldb;
@@ -905,6 +918,8 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
     launch_perm_out(C, pa, st);
   }
   LAUNCH_CHECK("k_perm_out");
+  const double tol = h->opt.refine_tol;
+  unsigned long long* norm_d = (unsigned long long*)(F + h->off_norm);
   for (int r = 0; r < refine; ++r) {
     SpmvArgs sa{};
     sa.rows = (const SpRow*)(F + h->off_sprows);
@@ -926,15 +941,38 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
       launch_spmv(C, sa, h->n_sprows, st);
     }
     LAUNCH_CHECK("k_spmv");
-    rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st);
+    const int* flag = nullptr;
+    if (tol > 0) {  // adaptive: skip the correction on the device when every column is converged
+      if (!h->norm_valid) {
+        CUDA_TRY(cudaMemsetAsync(norm_d, 0, sizeof(unsigned long long), st));
+        launch_norm_a(C, sa, h->n_sprows, norm_d, st);
+        LAUNCH_CHECK("k_norm_a");
+        h->norm_valid = true;
+      }
+      CUDA_TRY(cudaMemsetAsync(flag_d, 0, sizeof(int), st));
+      launch_berr(C, y, yim, ldy, h->n_pad, (const double*)d_B, ldb, h->n, (int)nrhs, norm_d, tol, berr_d, flag_d, st);
+      LAUNCH_CHECK("k_berr");
+      flag = flag_d;
+    }
+    rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, flag);
     if (rc) return rc;
     pa.accumulate = 1;
+    pa.flag = flag;
     {
       TraceScope ts(h, DD_PH_PERM, 0.0, st);
       launch_perm_out(C, pa, st);
     }
     LAUNCH_CHECK("k_perm_out");
   }
+  return DD_OK;
+}
+
+int dd_aux_set_refine(dd_aux_handle_t h, int32_t refine_steps, double refine_tol) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (refine_steps < 0) return fail(-2, "refine_steps must be >= 0");
+  if (!(refine_tol >= 0)) return fail(-3, "refine_tol must be >= 0");
+  h->opt.refine_steps = refine_steps;
+  h->opt.refine_tol = refine_tol;
   return DD_OK;
 }
 

@@ -160,7 +160,28 @@ struct Gemm {
     }
   }
 
-  __device__ static void compute_stage(const double* st, Acc& acc) {
+  // Bit (a*NI + b) set = this warp's 16x8 sub-tile (a, b) intersects the valid region: rows
+  // < mlim, cols < nlim and, when diag_off != NO_DIAG, not strictly above the diagonal
+  // col - row == diag_off (diagonal target blocks store only their lower triangle).  Masked
+  // sub-tiles issue no DMMA, which the co-resident CTA's warps pick up.
+  static constexpr int NO_DIAG = -(1 << 30);
+  __device__ static unsigned tile_mask(int mlim, int nlim, int diag_off) {
+    const int warp = threadIdx.x >> 5;
+    const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+    unsigned m = 0;
+#pragma unroll
+    for (int a = 0; a < MI; ++a)
+#pragma unroll
+      for (int b = 0; b < NI; ++b) {
+        const int r0 = wm * WTM + a * 16, c0 = wn * WTN + b * 8;
+        bool on = r0 < mlim && c0 < nlim;
+        if (diag_off != NO_DIAG && r0 + 15 < c0 + diag_off) on = false;
+        if (on) m |= 1u << (a * NI + b);
+      }
+    return m;
+  }
+
+  __device__ static void compute_stage(const double* st, Acc& acc, unsigned mask = ~0u) {
     const double* As = st;
     const double* Bs = st + NPL * A_TILE;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -195,12 +216,14 @@ struct Gemm {
 #pragma unroll
       for (int a = 0; a < MI; ++a)
 #pragma unroll
-        for (int b = 0; b < NI; ++b) dmma16x8x4(acc.r[a][b], ar[a][0], ar[a][1], br[b]);
+        for (int b = 0; b < NI; ++b)
+          if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.r[a][b], ar[a][0], ar[a][1], br[b]);
       if constexpr (CPLX) {
 #pragma unroll
         for (int a = 0; a < MI; ++a)
 #pragma unroll
-          for (int b = 0; b < NI; ++b) dmma16x8x4(acc.i[a][b], ar[a][0], ar[a][1], bi[b]);
+          for (int b = 0; b < NI; ++b)
+            if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.i[a][b], ar[a][0], ar[a][1], bi[b]);
         double nai[MI][2];
 #pragma unroll
         for (int a = 0; a < MI; ++a) {
@@ -210,11 +233,13 @@ struct Gemm {
 #pragma unroll
         for (int a = 0; a < MI; ++a)
 #pragma unroll
-          for (int b = 0; b < NI; ++b) dmma16x8x4(acc.r[a][b], nai[a][0], nai[a][1], bi[b]);
+          for (int b = 0; b < NI; ++b)
+            if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.r[a][b], nai[a][0], nai[a][1], bi[b]);
 #pragma unroll
         for (int a = 0; a < MI; ++a)
 #pragma unroll
-          for (int b = 0; b < NI; ++b) dmma16x8x4(acc.i[a][b], ai[a][0], ai[a][1], br[b]);
+          for (int b = 0; b < NI; ++b)
+            if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.i[a][b], ai[a][0], ai[a][1], br[b]);
       }
     }
   }
@@ -223,7 +248,7 @@ struct Gemm {
   // with identical arguments.  smem: STAGES*STAGE doubles.  Ends with a __syncthreads().
   template <class SegFn>
   __device__ static void run(SegFn segfn, int nseg, int m0, int n0, int M, int N, int64_t aim, int64_t bim,
-                             double* smem, Acc& acc) {
+                             double* smem, Acc& acc, unsigned mask = ~0u) {
     int pseg = 0, pk = 0;
     Seg cur;
     while (pseg < nseg) {  // skip empty segments
@@ -264,7 +289,7 @@ struct Gemm {
         ++issued;
       }
       cp_async_commit();
-      compute_stage(smem + (done % STAGES) * STAGE, acc);
+      compute_stage(smem + (done % STAGES) * STAGE, acc, mask);
       ++done;
     }
     cp_async_wait<0>();

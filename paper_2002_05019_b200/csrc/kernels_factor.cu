@@ -288,7 +288,8 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
         for (int tn = 0; tn <= tm; ++tn) {
           typename G::Acc acc;
           G::zero(acc);
-          G::run([&](int) { return sg; }, 1, tm * 64, tn * 64, M, M, aim, wim, smem, acc);
+          G::run([&](int) { return sg; }, 1, tm * 64, tn * 64, M, M, aim, wim, smem, acc,
+                 G::tile_mask(M - tm * 64, M - tn * 64, tn * 64 - tm * 64));
           double* Cb = A + Ael(ke + tm * 64, ke + tn * 64);
           G::for_each(acc, [&](int r, int c, double vr, double vi) {
             const int gr = ke + tm * 64 + r, gc = ke + tn * 64 + c;
@@ -552,9 +553,10 @@ __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_upd
     sg.K = nk.s;
     return sg;
   };
-  G::run(segfn, tg.c1 - tg.c0, T.tm * BM, T.tn * BN, tg.M, tg.N, a.wim, a.aim, smem, acc);
-  double* Cb = a.arena + nj.panel + tg.ro + (int64_t)T.tm * BM + (int64_t)T.tn * BN * nj.ld;
   const int mlim = tg.M - T.tm * BM, nlim = tg.N - T.tn * BN;
+  const unsigned mask = G::tile_mask(mlim, nlim, tg.diag ? T.tn * BN - T.tm * BM : G::NO_DIAG);
+  G::run(segfn, tg.c1 - tg.c0, T.tm * BM, T.tn * BN, tg.M, tg.N, a.wim, a.aim, smem, acc, mask);
+  double* Cb = a.arena + nj.panel + tg.ro + (int64_t)T.tm * BM + (int64_t)T.tn * BN * nj.ld;
   const int64_t ldc = nj.ld, aim = a.aim;
   G::for_each(acc, [&](int r, int c, double vr, double vi) {
     if (r < mlim && c < nlim) {

@@ -12,6 +12,9 @@
 //   r = b - A x          k_spmv        (refinement residual over the ORIGINAL blocks, L7)
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "gemm_core.cuh"
 #include "launch.hpp"
@@ -26,6 +29,7 @@ using FDiagC = Gemm<TB, SBN, 16, 1, 4, 3, true, false, true>;
 using BDiagR = Gemm<TB, SBN, 16, 1, 4, 3, false, true, true>;
 using BDiagC = Gemm<TB, SBN, 16, 1, 4, 3, true, true, true>;
 constexpr int SUBM = 64;
+constexpr int BUPD_MAX_PARTS = 320;  // split-K partial tiles of the backward update (workspace bound)
 using FUpdR = Gemm<SUBM, SBN, 16, 2, 2, 3, false, false, true>;
 using FUpdC = Gemm<SUBM, SBN, 16, 2, 2, 3, true, false, true>;
 using BUpdR = Gemm<SUBM, SBN, 16, 2, 2, 3, false, true, true>;
@@ -55,6 +59,7 @@ __global__ void k_perm_in(PermArgs a) {
 
 template <bool C>
 __global__ void k_perm_out(PermArgs a) {
+  if (a.flag && *a.flag == 0) return;
   const int c = blockIdx.y;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.nrows; g += (int64_t)gridDim.x * blockDim.x) {
     const int o = a.gperm[g];
@@ -87,6 +92,7 @@ __global__ void k_copy(const double* __restrict__ src, int64_t lds, double* __re
 // ---------------------------------------------------------------------------- diagonal solves
 template <bool C>
 __global__ void __launch_bounds__(128) k_fdiag(SolveArgs a) {
+  if (a.flag && *a.flag == 0) return;
   using G = typename std::conditional<C, FDiagC, FDiagR>::type;
   extern __shared__ __align__(16) double smem[];
   const int t = a.nodes[blockIdx.x];
@@ -133,6 +139,7 @@ __global__ void __launch_bounds__(128) k_fdiag(SolveArgs a) {
 
 template <bool C>
 __global__ void __launch_bounds__(128) k_bdiag(SolveArgs a) {
+  if (a.flag && *a.flag == 0) return;
   using G = typename std::conditional<C, BDiagC, BDiagR>::type;
   extern __shared__ __align__(16) double smem[];
   const int t = a.nodes[blockIdx.x];
@@ -180,6 +187,7 @@ __global__ void __launch_bounds__(128) k_bdiag(SolveArgs a) {
 // ---------------------------------------------------------------------------- level updates
 template <bool C>
 __global__ void __launch_bounds__(128) k_fupd(SolveArgs a) {
+  if (a.flag && *a.flag == 0) return;
   using G = typename std::conditional<C, FUpdC, FUpdR>::type;
   extern __shared__ __align__(16) double smem[];
   const SolveTarget T = a.ftargets[blockIdx.x];
@@ -194,7 +202,8 @@ __global__ void __launch_bounds__(128) k_fupd(SolveArgs a) {
     Seg sg{a.arena + nk.panel + u.ro, a.y + nk.ydof, nullptr, (int64_t)nk.ld, a.ldy, nk.s};
     return sg;
   };
-  G::run(segfn, T.c1 - T.c0, m0, n0, ni.s, a.nrhs, a.aim, a.yim, smem, acc);
+  G::run(segfn, T.c1 - T.c0, m0, n0, ni.s, a.nrhs, a.aim, a.yim, smem, acc,
+         G::tile_mask(ni.s - m0, a.nrhs - n0, G::NO_DIAG));
   double* y = a.y + ni.ydof;
   G::for_each(acc, [&](int r, int c, double vr, double vi) {
     if (m0 + r < ni.s && n0 + c < a.nrhs) {
@@ -205,37 +214,78 @@ __global__ void __launch_bounds__(128) k_fupd(SolveArgs a) {
   });
 }
 
+// Backward pull update y_t -= sum_{i in struct(t)} L_it^T y_i.  With split-K (G > 1) CTA
+// (tile, g) sums the g-th contiguous chunk of struct(t) into a partial buffer and
+// k_bupd_reduce subtracts the G partials in fixed order g = 0..G-1 (deterministic).
 template <bool C>
-__global__ void __launch_bounds__(128) k_bupd(SolveArgs a) {
-  using G = typename std::conditional<C, BUpdC, BUpdR>::type;
+__global__ void __launch_bounds__(128) k_bupd(SolveArgs a, int G, double* part, int64_t pim) {
+  if (a.flag && *a.flag == 0) return;
+  using G_ = typename std::conditional<C, BUpdC, BUpdR>::type;
   extern __shared__ __align__(16) double smem[];
-  const int2 T = a.btiles[blockIdx.x];  // (t, tm)
+  const int tile = blockIdx.x / G, g = blockIdx.x % G;
+  const int2 T = a.btiles[tile];  // (t, tm)
   const NodeDev nt = a.nd[T.x];
   const int n0 = blockIdx.y * SBN, m0 = T.y * SUBM;
-  typename G::Acc acc;
-  G::zero(acc);
+  const int q0 = (int)((int64_t)nt.nst * g / G), q1 = (int)((int64_t)nt.nst * (g + 1) / G);
+  typename G_::Acc acc;
+  G_::zero(acc);
   auto segfn = [&](int q) {
-    const int ipos = a.st_pos[nt.st0 + q];
-    const int ro = a.st_row[nt.st0 + q];
+    const int ipos = a.st_pos[nt.st0 + q0 + q];
+    const int ro = a.st_row[nt.st0 + q0 + q];
     const NodeDev ni = a.nd[ipos];
     // A(m, k) = L_it(k, m) = panel_t[(ro + k) + m*ld]  (KM)
     Seg sg{a.arena + nt.panel + ro, a.y + ni.ydof, nullptr, (int64_t)nt.ld, a.ldy, ni.s};
     return sg;
   };
-  G::run(segfn, nt.nst, m0, n0, nt.s, a.nrhs, a.aim, a.yim, smem, acc);
-  double* y = a.y + nt.ydof;
-  G::for_each(acc, [&](int r, int c, double vr, double vi) {
-    if (m0 + r < nt.s && n0 + c < a.nrhs) {
-      int64_t e = (int64_t)(m0 + r) + (int64_t)(n0 + c) * a.ldy;
-      y[e] -= vr;
-      if (C) y[e + a.yim] -= vi;
+  G_::run(segfn, q1 - q0, m0, n0, nt.s, a.nrhs, a.aim, a.yim, smem, acc,
+          G_::tile_mask(nt.s - m0, a.nrhs - n0, G_::NO_DIAG));
+  if (G == 1) {
+    double* y = a.y + nt.ydof;
+    G_::for_each(acc, [&](int r, int c, double vr, double vi) {
+      if (m0 + r < nt.s && n0 + c < a.nrhs) {
+        int64_t e = (int64_t)(m0 + r) + (int64_t)(n0 + c) * a.ldy;
+        y[e] -= vr;
+        if (C) y[e + a.yim] -= vi;
+      }
+    });
+  } else {
+    double* P = part + (int64_t)blockIdx.x * SUBM * a.nrhs;  // SUBM x nrhs, ld SUBM
+    G_::for_each(acc, [&](int r, int c, double vr, double vi) {
+      if (n0 + c < a.nrhs) {
+        int64_t e = (int64_t)r + (int64_t)(n0 + c) * SUBM;
+        P[e] = vr;
+        if (C) P[e + pim] = vi;
+      }
+    });
+  }
+}
+
+template <bool C>
+__global__ void k_bupd_reduce(SolveArgs a, int G, const double* __restrict__ part, int64_t pim) {
+  if (a.flag && *a.flag == 0) return;
+  const int tile = blockIdx.x;
+  const int2 T = a.btiles[tile];
+  const NodeDev nt = a.nd[T.x];
+  const int m0 = T.y * SUBM;
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < SUBM * a.nrhs; e += gridDim.y * blockDim.x) {
+    const int r = e % SUBM, c = e / SUBM;
+    if (m0 + r >= nt.s) continue;
+    double sr = 0.0, si = 0.0;
+    for (int g = 0; g < G; ++g) {
+      const double* P = part + (int64_t)(tile * G + g) * SUBM * a.nrhs;
+      sr += P[e];
+      if (C) si += P[e + pim];
     }
-  });
+    int64_t o = nt.ydof + (int64_t)(m0 + r) + (int64_t)c * a.ldy;
+    a.y[o] -= sr;
+    if (C) a.y[o + a.yim] -= si;
+  }
 }
 
 // ---------------------------------------------------------------------------- D solve
 template <bool C>
 __global__ void k_dsolve(SolveArgs a) {
+  if (a.flag && *a.flag == 0) return;
   const int c = blockIdx.y;
   const double* dv_ = a.arena + a.d_off;
   const double* ev_ = a.arena + a.e_off;
@@ -367,6 +417,205 @@ __global__ void __launch_bounds__(256) k_spmv(SpmvArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------- residual SpMV on DMMA
+// Same product as k_spmv, on the FP64 tensor pipe: CTA tile 64 rows x 64 rhs, K = the columns of
+// every stored block of block-row I (ascending J, fixed order).  The caller's blocks are read
+// element-wise (interleaved complex at arbitrary offsets, so no 16-byte cp.async chunks): each
+// thread gathers its 8 A and 8 B elements of the next K-chunk into registers while the DMMAs
+// of the current chunk run, then stores them into the engine's MK / KN shared-memory tiles.
+using SpG_R = Gemm<64, 64, 16, 2, 2, 2, false, false, true>;
+using SpG_C = Gemm<64, 64, 16, 2, 2, 2, true, false, true>;
+constexpr int SPT_M = 64, SPT_N = 64, SPT_K = 16;
+
+template <bool C>
+__global__ void __launch_bounds__(128) k_spmv_dmma(SpmvArgs a) {
+  using G = typename std::conditional<C, SpG_C, SpG_R>::type;
+  extern __shared__ __align__(16) double smem[];
+  const SpRow R = a.rows[blockIdx.x];
+  const int I = R.I, sI = (int)a.blk_size[I];
+  const int m0 = R.tm * SPT_M, n0 = blockIdx.y * SPT_N;
+  const int tid = threadIdx.x;
+  constexpr int PER = SPT_M * SPT_K / 128;  // 8 elements of A and of B per thread per chunk
+  double ra[PER], ia[PER], rb[PER], ib[PER];
+  // chunk iterator over (segment, k0)
+  int q = R.c0, k0 = 0;
+  auto fetch = [&](int qq, int kk0) {
+    const SpSeg sg = a.segs[qq];
+    const int sJ = (int)a.blk_size[sg.J];
+    const int64_t oJ = a.odof[sg.J];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + u * 128;
+      // A(m, k): m fastest for stored / diagonal blocks, k fastest for transposed ones (coalescing)
+      int m, k;
+      if (sg.mode == 1) {
+        k = e % SPT_K;
+        m = e / SPT_K;
+      } else {
+        m = e % SPT_M;
+        k = e / SPT_M;
+      }
+      const int gm = m0 + m, gk = kk0 + k;
+      double vr = 0.0, vi = 0.0;
+      if (gm < sI && gk < sJ) {
+        int64_t idx;
+        if (sg.mode == 0) idx = gm + (int64_t)gk * sI;
+        else if (sg.mode == 1) idx = gk + (int64_t)gm * sJ;
+        else idx = gm >= gk ? gm + (int64_t)gk * sI : gk + (int64_t)gm * sI;
+        idx += sg.voff;
+        if (C) {
+          vr = a.vals[2 * idx];
+          vi = a.vals[2 * idx + 1];
+        } else {
+          vr = a.vals[idx];
+        }
+      }
+      ra[u] = vr;
+      ia[u] = vi;
+      // B(k, n) = X(oJ + k, n): k fastest
+      const int kb = e % SPT_K, nb = e / SPT_K;
+      const int gkb = kk0 + kb, gn = n0 + nb;
+      double wr = 0.0, wi = 0.0;
+      if (gkb < sJ && gn < a.nrhs) {
+        int64_t idx = oJ + gkb + (int64_t)gn * a.ldx;
+        if (C) {
+          wr = a.X[2 * idx];
+          wi = a.X[2 * idx + 1];
+        } else {
+          wr = a.X[idx];
+        }
+      }
+      rb[u] = wr;
+      ib[u] = wi;
+    }
+  };
+  auto store = [&](double* st, int mode) {
+    double* As = st;
+    double* Bs = st + G::NPL * G::A_TILE;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + u * 128;
+      int m, k;
+      if (mode == 1) {
+        k = e % SPT_K;
+        m = e / SPT_K;
+      } else {
+        m = e % SPT_M;
+        k = e / SPT_M;
+      }
+      As[k * G::A_LD + m] = ra[u];
+      if (C) As[G::A_TILE + k * G::A_LD + m] = ia[u];
+      const int kb = e % SPT_K, nb = e / SPT_K;
+      Bs[nb * G::B_LD + kb] = rb[u];
+      if (C) Bs[G::B_TILE + nb * G::B_LD + kb] = ib[u];
+    }
+  };
+  typename G::Acc acc;
+  G::zero(acc);
+  if (q < R.c1) {
+    fetch(q, k0);
+    int buf = 0;
+    for (;;) {
+      const int mode = a.segs[q].mode;
+      store(smem + buf * G::STAGE, mode);
+      __syncthreads();
+      // advance and prefetch the next chunk into registers
+      const int sJ = (int)a.blk_size[a.segs[q].J];
+      k0 += SPT_K;
+      if (k0 >= sJ) {
+        k0 = 0;
+        ++q;
+      }
+      const bool more = q < R.c1;
+      if (more) fetch(q, k0);
+      G::compute_stage(smem + buf * G::STAGE, acc);
+      buf ^= 1;
+      if (!more) break;
+    }
+  }
+  const int64_t oI = a.odof[I];
+  G::for_each(acc, [&](int r, int c, double vr, double vi) {
+    const int gm = m0 + r, gn = n0 + c;
+    if (gm < sI && gn < a.nrhs) {
+      const int64_t orow = oI + gm;
+      const int64_t bidx = orow + (int64_t)gn * a.ldb;
+      const int64_t yidx = (int64_t)a.ginv[orow] + (int64_t)gn * a.ldy;
+      if (C) {
+        a.y[yidx] = a.Bsave[2 * bidx] - vr;
+        a.y[yidx + a.yim] = a.Bsave[2 * bidx + 1] - vi;
+      } else {
+        a.y[yidx] = a.Bsave[bidx] - vr;
+      }
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------- ||A||_inf, berr
+template <bool C>
+__global__ void k_norm_a(SpmvArgs a, unsigned long long* out) {
+  __shared__ double red[256];
+  const SpRow R = a.rows[blockIdx.x];
+  const int I = R.I, sI = (int)a.blk_size[I];
+  double best = 0.0;
+  for (int m = R.tm * SPM + threadIdx.x; m < min(sI, (R.tm + 1) * SPM); m += blockDim.x) {
+    double acc = 0.0;  // row sum of moduli over every block of block-row I (fixed order)
+    for (int q = R.c0; q < R.c1; ++q) {
+      const SpSeg sg = a.segs[q];
+      const int sJ = (int)a.blk_size[sg.J];
+      for (int k = 0; k < sJ; ++k) {
+        int64_t idx;
+        if (sg.mode == 0) idx = m + (int64_t)k * sI;
+        else if (sg.mode == 1) idx = k + (int64_t)m * sJ;
+        else idx = m >= k ? m + (int64_t)k * sI : k + (int64_t)m * sI;
+        idx += sg.voff;
+        acc += C ? hypot(a.vals[2 * idx], a.vals[2 * idx + 1]) : fabs(a.vals[idx]);
+      }
+    }
+    best = fmax(best, acc);
+  }
+  red[threadIdx.x] = best;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(red[0]));  // >= 0: bit order == value order
+}
+
+template <bool C>
+__global__ void k_berr(const double* __restrict__ y, int64_t yim, int64_t ldy, int64_t nrows,
+                       const double* __restrict__ X, int64_t ldx, int64_t n, const unsigned long long* normA,
+                       double tol, double* berr, int* flag) {
+  __shared__ double rr[256], rx[256];
+  const int c = blockIdx.x;
+  double mr = 0.0, mx = 0.0;
+  for (int64_t g = threadIdx.x; g < nrows; g += blockDim.x) {
+    int64_t e = g + (int64_t)c * ldy;
+    mr = fmax(mr, C ? hypot(y[e], y[e + yim]) : fabs(y[e]));
+  }
+  for (int64_t g = threadIdx.x; g < n; g += blockDim.x) {
+    int64_t e = g + (int64_t)c * ldx;
+    mx = fmax(mx, C ? hypot(X[2 * e], X[2 * e + 1]) : fabs(X[e]));
+  }
+  rr[threadIdx.x] = mr;
+  rx[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o; o >>= 1) {
+    if (threadIdx.x < o) {
+      rr[threadIdx.x] = fmax(rr[threadIdx.x], rr[threadIdx.x + o]);
+      rx[threadIdx.x] = fmax(rx[threadIdx.x], rx[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double na = __longlong_as_double((long long)*normA);
+    const double den = na * rx[0];
+    const double b = den > 0 ? rr[0] / den : (rr[0] > 0 ? INFINITY : 0.0);
+    berr[c] = b;
+    if (!(b <= tol)) atomicOr(flag, 1);
+  }
+}
+
 // ---------------------------------------------------------------------------- launchers
 template <class K>
 static void set_smem(K kern, size_t bytes) {
@@ -374,6 +623,7 @@ static void set_smem(K kern, size_t bytes) {
 }
 
 int solve_bm(bool) { return SUBM; }
+size_t bupd_part_bytes(bool cplx, int nrhs) { return (size_t)BUPD_MAX_PARTS * SUBM * nrhs * (cplx ? 2 : 1) * 8; }
 int solve_bn(bool) { return SBN; }
 int spmv_bm() { return SPM; }
 
@@ -427,21 +677,69 @@ void launch_fupd(bool cplx, const SolveArgs& a, int ntiles, cudaStream_t st) {
   dim3 grid(ntiles, ntn(a.nrhs));
   DD_LAUNCH_GEMM_KERNEL(k_fupd, FUpdR, FUpdC, grid, 128);
 }
-void launch_bupd(bool cplx, const SolveArgs& a, int ntiles, cudaStream_t st) {
+int bupd_split(int ntiles, int nrhs) {
+  // enough CTAs for two per SM; partial buffer bounded by BUPD_MAX_PARTS tiles
+  const int ctas = ntiles * ntn(nrhs);
+  if (ctas >= 2 * 148) return 1;
+  int G = (2 * 148 + ctas - 1) / ctas;
+  G = std::min(G, std::max(1, BUPD_MAX_PARTS / std::max(ntiles, 1)));
+  return std::max(1, std::min(G, 16));
+}
+
+void launch_bupd(bool cplx, const SolveArgs& a, int ntiles, double* part, cudaStream_t st) {
   if (ntiles == 0 || a.nrhs == 0) return;
-  dim3 grid(ntiles, ntn(a.nrhs));
-  DD_LAUNCH_GEMM_KERNEL(k_bupd, BUpdR, BUpdC, grid, 128);
+  const int G = part ? bupd_split(ntiles, a.nrhs) : 1;
+  const int64_t pim = (int64_t)BUPD_MAX_PARTS * SUBM * a.nrhs;
+  dim3 grid(ntiles * G, ntn(a.nrhs));
+  if (cplx) {
+    set_smem(k_bupd<true>, BUpdC::SMEM_BYTES);
+    k_bupd<true><<<grid, 128, BUpdC::SMEM_BYTES, st>>>(a, G, part, pim);
+  } else {
+    set_smem(k_bupd<false>, BUpdR::SMEM_BYTES);
+    k_bupd<false><<<grid, 128, BUpdR::SMEM_BYTES, st>>>(a, G, part, pim);
+  }
+  if (G > 1) {
+    dim3 g2(ntiles, std::min(64, (SUBM * a.nrhs + 255) / 256));
+    if (cplx) k_bupd_reduce<true><<<g2, 256, 0, st>>>(a, G, part, pim);
+    else k_bupd_reduce<false><<<g2, 256, 0, st>>>(a, G, part, pim);
+  }
 }
 void launch_dsolve(bool cplx, const SolveArgs& a, cudaStream_t st) {
   if (a.nrhs == 0) return;
   if (cplx) k_dsolve<true><<<rows_grid(a.nrows, a.nrhs), 256, 0, st>>>(a);
   else k_dsolve<false><<<rows_grid(a.nrows, a.nrhs), 256, 0, st>>>(a);
 }
+void launch_norm_a(bool cplx, const SpmvArgs& a, int nrow_tiles, unsigned long long* out, cudaStream_t st) {
+  if (nrow_tiles == 0) return;
+  if (cplx) k_norm_a<true><<<nrow_tiles, 64, 0, st>>>(a, out);
+  else k_norm_a<false><<<nrow_tiles, 64, 0, st>>>(a, out);
+}
+
+void launch_berr(bool cplx, const double* y, int64_t yim, int64_t ldy, int64_t nrows, const double* X, int64_t ldx,
+                 int64_t n, int nrhs, const unsigned long long* normA, double tol, double* berr, int* flag,
+                 cudaStream_t st) {
+  if (nrhs == 0) return;
+  if (cplx) k_berr<true><<<nrhs, 256, 0, st>>>(y, yim, ldy, nrows, X, ldx, n, normA, tol, berr, flag);
+  else k_berr<false><<<nrhs, 256, 0, st>>>(y, yim, ldy, nrows, X, ldx, n, normA, tol, berr, flag);
+}
+
 void launch_spmv(bool cplx, const SpmvArgs& a, int nrow_tiles, cudaStream_t st) {
   if (nrow_tiles == 0 || a.nrhs == 0) return;
-  dim3 grid(nrow_tiles, (a.nrhs + SPN - 1) / SPN);
-  if (cplx) k_spmv<true><<<grid, 256, 0, st>>>(a);
-  else k_spmv<false><<<grid, 256, 0, st>>>(a);
+  static const bool simt = getenv("DD_AUX_SPMV_SIMT") && atoi(getenv("DD_AUX_SPMV_SIMT"));
+  if (simt) {
+    dim3 grid(nrow_tiles, (a.nrhs + SPN - 1) / SPN);
+    if (cplx) k_spmv<true><<<grid, 256, 0, st>>>(a);
+    else k_spmv<false><<<grid, 256, 0, st>>>(a);
+    return;
+  }
+  dim3 grid(nrow_tiles, (a.nrhs + SPT_N - 1) / SPT_N);
+  if (cplx) {
+    set_smem(k_spmv_dmma<true>, SpG_C::SMEM_BYTES);
+    k_spmv_dmma<true><<<grid, 128, SpG_C::SMEM_BYTES, st>>>(a);
+  } else {
+    set_smem(k_spmv_dmma<false>, SpG_R::SMEM_BYTES);
+    k_spmv_dmma<false><<<grid, 128, SpG_R::SMEM_BYTES, st>>>(a);
+  }
 }
 
 }  // namespace ddk

@@ -79,6 +79,7 @@ struct SolveArgs {
   const int* ipiv;
   int64_t d_off, e_off;
   int64_t nrows;                // padded n
+  const int* flag;              // refinement sweep: run only if *flag != 0 (nullptr = always)
 };
 
 struct PermArgs {
@@ -92,6 +93,7 @@ struct PermArgs {
   double* y;
   int64_t yim, ldy;
   int accumulate;
+  const int* flag;    // accumulate only if *flag != 0 (nullptr = always)
 };
 
 struct SpmvArgs {
@@ -130,9 +132,16 @@ void launch_copy(bool cplx, const double* src, int64_t lds, double* dst, int64_t
 void launch_fdiag(bool cplx, const SolveArgs& a, int nnodes, cudaStream_t st);
 void launch_fupd(bool cplx, const SolveArgs& a, int ntiles, cudaStream_t st);
 void launch_dsolve(bool cplx, const SolveArgs& a, cudaStream_t st);
-void launch_bupd(bool cplx, const SolveArgs& a, int ntiles, cudaStream_t st);
+void launch_bupd(bool cplx, const SolveArgs& a, int ntiles, double* part, cudaStream_t st);
+size_t bupd_part_bytes(bool cplx, int nrhs);
 void launch_bdiag(bool cplx, const SolveArgs& a, int nnodes, cudaStream_t st);
 int spmv_bm();
+// ||A||_inf of the caller's original blocks (max row sum of moduli) -> *out (bits of a double)
+void launch_norm_a(bool cplx, const SpmvArgs& a, int nrow_tiles, unsigned long long* out, cudaStream_t st);
+// per-column backward error of the residual held in y against X; sets *flag if any > tol
+void launch_berr(bool cplx, const double* y, int64_t yim, int64_t ldy, int64_t nrows, const double* X, int64_t ldx,
+                 int64_t n, int nrhs, const unsigned long long* normA, double tol, double* berr, int* flag,
+                 cudaStream_t st);
 void launch_spmv(bool cplx, const SpmvArgs& a, int nrows_tiles, cudaStream_t st);
 
 }  // namespace ddk

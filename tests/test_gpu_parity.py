@@ -187,3 +187,26 @@ def test_cfg1_full_size():
     """BASELINE configs[1] at full size (n = 36,864, ND order), nrhs 64, vs the oracle."""
     p = dd_inputs.config("cfg1")
     _parity(p, nrhs=64)
+
+
+def test_adaptive_refinement_policy():
+    """refine_tol: the correction is skipped on the device iff every column's berr <= tol."""
+    import torch
+    import paper_2002_05019_b200 as dd
+    from tests._gpu import to_dev_colmajor
+    p = dd_inputs.config("cfg3", grid=(2, 2, 2), sizes=60)
+    B = random_rhs(p.n, 6, True, 5)
+    s = dd.AuxSolver(p.blk_size, p.colptr, p.rowidx, complex_=True)
+    vals = torch.from_numpy(p.values).cuda()
+    s.factor(vals, p.val_offset)
+    out = {}
+    for name, steps, tol in [("plain", 0, 0.0), ("always", 1, 0.0), ("skip", 1, 1.0), ("tight", 1, 1e-300)]:
+        dd.dd_aux_set_refine(s.h, steps, tol)
+        b = to_dev_colmajor(B, torch)
+        s.solve_(b)
+        torch.cuda.synchronize()
+        out[name] = b.cpu().numpy()
+    s.close()
+    np.testing.assert_array_equal(out["skip"], out["plain"])     # converged -> no correction applied
+    np.testing.assert_array_equal(out["tight"], out["always"])   # not converged -> same as always
+    assert residual_berr(p, out["always"], B).max() <= TOL_BERR
