@@ -1,7 +1,10 @@
 #!/usr/bin/env python
 """Benchmark of the auxiliary-matrix block LDL^T + multi-RHS solve on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl reference]
+
+Default workload: configs[2] (the largest config by factor flops; the north_star target is
+">= 50% of measured FP64 tensor peak in the factor phase of the largest config").
 
 Metric (BASELINE.json): "aux-matrix LDL^T factor FP64 GFLOP/s (% of FP64 peak); solve ms
 per 1000 RHS".  One step = one pass of the whole hot path over one batch: dd_aux_factor
@@ -49,7 +52,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=os.environ.get("DD_BENCH_CONFIG", "cfg3"))
+    ap.add_argument("--config", default=os.environ.get("DD_BENCH_CONFIG", "cfg2"))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--refine", type=int, default=1)
@@ -278,7 +281,9 @@ def gpu_arm(args, rank, world, local, dist):
     total_ms = start.elapsed_time(end)
     fac_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
     sol_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
-    trace = dd.dd_aux_get_trace(solver.h, reset=True)
+    trace = dd.dd_aux_get_trace(solver.h, reset=False)
+    lvl = dd.dd_aux_get_level_trace(solver.h)
+    dd.dd_aux_get_trace(solver.h, reset=True)
     dd.dd_aux_set_trace(solver.h, False)
 
     # ---- accuracy evidence (harness, outside the timed region): berr of the timed result and of
@@ -369,7 +374,9 @@ def gpu_arm(args, rank, world, local, dist):
         "setup_s": {"generate": gen_s, "analyze": analyze_s},
     }
     if args.trace_out:
-        json.dump({"trace": trace, "line": line}, open(args.trace_out, "w"), indent=1)
+        json.dump({"trace": trace, "line": line, "phases": dd.PHASES,
+                   "level_ms": (lvl["ms"] / K).tolist(), "level_flops": (lvl["flops"] / K).tolist()},
+                  open(args.trace_out, "w"), indent=1)
     print(json.dumps(line), flush=True)
 
 

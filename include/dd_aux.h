@@ -171,6 +171,9 @@ typedef struct {
 } dd_aux_trace;
 int dd_aux_set_trace(dd_aux_handle_t h, int32_t enable);
 int dd_aux_get_trace(dd_aux_handle_t h, dd_aux_trace* out, int32_t reset);
+/* Per-level factor trace since the last reset, row-major [n_levels][16] (DD_PH_* columns):
+ * device ms (tracing enabled) and algorithmic flops.  Call after dd_aux_get_trace(reset=0). */
+int dd_aux_get_level_trace(dd_aux_handle_t h, double* ms, double* flops);
 
 int dd_aux_destroy(dd_aux_handle_t h);
 

@@ -20,7 +20,7 @@ __all__ = ["DD_REAL64", "DD_COMPLEX128", "DD_ORDER_AUTO", "DD_ORDER_ND", "DD_ORD
            "DD_ORDER_USER", "DD_OK", "DD_ZERO_PIVOT", "DDAuxError", "dd_aux_default_options", "dd_aux_analyze",
            "dd_aux_get_info", "dd_aux_get_order", "dd_aux_get_etree", "dd_aux_solve_work_bytes", "dd_aux_factor",
            "dd_aux_solve", "dd_aux_get_pivots", "dd_aux_destroy", "dd_aux_last_error", "dd_aux_version",
-           "dd_aux_set_refine", "dd_aux_set_trace", "dd_aux_get_trace", "AuxSolver", "LIB_PATH", "EXPORTED_SYMBOLS", "PHASES"]
+           "dd_aux_set_refine", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_get_level_trace", "AuxSolver", "LIB_PATH", "EXPORTED_SYMBOLS", "PHASES"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdd_aux.so")
 
@@ -31,7 +31,7 @@ DD_ERR_CUDA, DD_ERR_WORKSPACE, DD_ERR_NOT_FACTORED, DD_ERR_SINGULAR, DD_ERR_PATT
 
 EXPORTED_SYMBOLS = ["dd_aux_default_options", "dd_aux_analyze", "dd_aux_get_info", "dd_aux_get_order",
                     "dd_aux_get_etree", "dd_aux_solve_work_bytes", "dd_aux_factor", "dd_aux_solve",
-                    "dd_aux_get_pivots", "dd_aux_set_refine", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_destroy",
+                    "dd_aux_get_pivots", "dd_aux_set_refine", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_get_level_trace", "dd_aux_destroy",
                     "dd_aux_last_error", "dd_aux_version"]
 PHASES = ["load", "k1_diag_bk", "rowperm", "k2_panel", "k3_update", "stats", "perm", "fdiag", "fupd", "dsolve",
           "bupd", "bdiag", "spmv"]
@@ -89,6 +89,7 @@ def _load():
         "dd_aux_set_refine": (ctypes.c_int, [P, i32, ctypes.c_double]),
         "dd_aux_set_trace": (ctypes.c_int, [P, i32]),
         "dd_aux_get_trace": (ctypes.c_int, [P, ctypes.POINTER(dd_aux_trace), i32]),
+        "dd_aux_get_level_trace": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
         "dd_aux_destroy": (ctypes.c_int, [P]),
         "dd_aux_last_error": (ctypes.c_char_p, []),
         "dd_aux_version": (ctypes.c_char_p, []),
@@ -240,6 +241,15 @@ def dd_aux_get_trace(h, reset=True) -> dict:
     t = dd_aux_trace()
     _check(_lib.dd_aux_get_trace(h, ctypes.byref(t), int(bool(reset))))
     return {name: {"ms": t.ms[i], "launches": int(t.launches[i]), "flops": t.flops[i]} for i, name in enumerate(PHASES)}
+
+
+def dd_aux_get_level_trace(h) -> dict:
+    """Per-level factor trace: {"ms": [n_levels x 16], "flops": [...]} (columns = PHASES)."""
+    nl = dd_aux_get_info(h)["n_levels"]
+    ms = np.zeros(nl * 16)
+    fl = np.zeros(nl * 16)
+    _check(_lib.dd_aux_get_level_trace(h, _np_ptr(ms, ctypes.c_double), _np_ptr(fl, ctypes.c_double)))
+    return {"ms": ms.reshape(nl, 16)[:, :len(PHASES)], "flops": fl.reshape(nl, 16)[:, :len(PHASES)]}
 
 
 def dd_aux_destroy(h):

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <numeric>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -117,7 +118,9 @@ struct dd_aux_handle_s {
   // tracing
   bool trace = false;
   std::vector<cudaEvent_t> pool;
-  struct Rec { int ph, e0, e1; };
+  struct Rec { int ph, e0, e1, level; };
+  int cur_level = -1;                          // level being enqueued (per-level trace)
+  std::vector<double> lvl_ms, lvl_fl;          // [nlevels * 16]
   std::vector<Rec> recs;
   int64_t launches[16] = {0};
   double flops[16] = {0};
@@ -146,7 +149,8 @@ struct TraceScope {
   dd_aux_handle_s* h;
   int ph, id = -1;
   cudaStream_t st;
-  TraceScope(dd_aux_handle_s* h_, int ph_, double fl, cudaStream_t st_) : h(h_), ph(ph_), st(st_) {
+  double fl;
+  TraceScope(dd_aux_handle_s* h_, int ph_, double fl_, cudaStream_t st_) : h(h_), ph(ph_), st(st_), fl(fl_) {
     h->launches[ph] += 1;
     h->flops[ph] += fl;
     if (h->trace) {
@@ -157,7 +161,14 @@ struct TraceScope {
   ~TraceScope() {
     if (id >= 0) {
       cudaEventRecord(h->pool[id + 1], st);
-      h->recs.push_back({ph, id, id + 1});
+      h->recs.push_back({ph, id, id + 1, h->cur_level});
+      if (h->cur_level >= 0) {
+        if (h->lvl_fl.size() < (size_t)(h->cur_level + 1) * 16) {
+          h->lvl_fl.resize((size_t)(h->cur_level + 1) * 16, 0.0);
+          h->lvl_ms.resize((size_t)(h->cur_level + 1) * 16, 0.0);
+        }
+        h->lvl_fl[(size_t)h->cur_level * 16 + ph] += fl;
+      }
     }
   }
 };
@@ -337,7 +348,9 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   std::vector<int2> btiles;
   {
     const char* ev = getenv("DD_AUX_K3CFG");
-    h->k3cfg = ev ? atoi(ev) : 1;
+    // default tile config per scalar type (measured on B200): real 64x64 at
+    // 4 CTAs/SM (least ragged-tile padding), complex 64x64 4M at 2 CTAs/SM
+    h->k3cfg = ev ? atoi(ev) : (h->cplx ? 1 : 4);
     const char* la = getenv("DD_AUX_LOOKAHEAD");
     h->lookahead = la ? atoi(la) != 0 : true;
   }
@@ -712,6 +725,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   const size_t wpar = (size_t)h->nW * (C ? 2 : 1);  // elements per parity buffer
   auto diag_phase = [&](int l) -> int {              // K1 + rowperm + K2 of level l on the side stream
     const LevelRanges& R = h->lv[l];
+    h->cur_level = l;
     k1.nodes = lvlnodes + R.n0;
     {
       TraceScope ts(h, DD_PH_K1, R.fl_k1, sd);
@@ -744,6 +758,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   }
   for (int l = 0; l < nL; ++l) {
     const LevelRanges& R = h->lv[l];
+    h->cur_level = l;
     CUDA_TRY(cudaStreamWaitEvent(st, h->evB[l], 0));
     K3Args a3 = k3;
     a3.work = work + (l & 1) * wpar;
@@ -760,12 +775,14 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
       if (rc) return rc;
     }
     a3.tiles = k3.tiles + R.ta;
+    h->cur_level = l;
     if (R.t1 > R.ta) {
       TraceScope ts(h, DD_PH_K3, R.fl_k3, st);
       launch_k3(C, h->k3cfg, a3, R.t1 - R.ta, st);
     }
     LAUNCH_CHECK("k3_update");
   }
+  h->cur_level = -1;
   // ---- a6: statistics
   int64_t* totals_d = (int64_t*)(F + h->off_totals);
   {
@@ -1036,6 +1053,7 @@ int dd_aux_get_trace(dd_aux_handle_t h, dd_aux_trace* out, int32_t reset) {
     float ms = 0;
     CUDA_TRY(cudaEventElapsedTime(&ms, h->pool[r.e0], h->pool[r.e1]));
     h->ms_acc[r.ph] += ms;
+    if (r.level >= 0 && (size_t)r.level * 16 + r.ph < h->lvl_ms.size()) h->lvl_ms[(size_t)r.level * 16 + r.ph] += ms;
   }
   h->recs.clear();
   for (int q = 0; q < 16; ++q) {
@@ -1044,11 +1062,23 @@ int dd_aux_get_trace(dd_aux_handle_t h, dd_aux_trace* out, int32_t reset) {
     out->flops[q] = h->flops[q];
   }
   if (reset) {
+    std::fill(h->lvl_ms.begin(), h->lvl_ms.end(), 0.0);
+    std::fill(h->lvl_fl.begin(), h->lvl_fl.end(), 0.0);
     for (int q = 0; q < 16; ++q) {
       h->ms_acc[q] = 0;
       h->launches[q] = 0;
       h->flops[q] = 0;
     }
+  }
+  return DD_OK;
+}
+
+int dd_aux_get_level_trace(dd_aux_handle_t h, double* ms, double* flops) {
+  if (!h) return fail(-1, "handle is NULL");
+  const size_t nl = h->S.nlevels;
+  for (size_t q = 0; q < nl * 16; ++q) {
+    if (ms) ms[q] = q < h->lvl_ms.size() ? h->lvl_ms[q] : 0.0;
+    if (flops) flops[q] = q < h->lvl_fl.size() ? h->lvl_fl[q] : 0.0;
   }
   return DD_OK;
 }

@@ -529,6 +529,38 @@ struct K3Cfg<true, 1> {
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 2;
 };
 
+template <>
+struct K3Cfg<false, 2> {  // real 128x64, 4 stages (deeper prefetch for DRAM-resident W panels)
+  using G = Gemm<128, 64, 16, 2, 2, 4, false, false, false>;
+  static constexpr int NT = 128, BM = 128, BN = 64, MINB = 2;
+};
+template <>
+struct K3Cfg<true, 2> {
+  using G = Gemm<64, 64, 16, 2, 2, 4, true, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 1;
+};
+
+template <>
+struct K3Cfg<false, 3> {  // real 128x64, register-capped for 3 CTAs per SM (12 warps)
+  using G = Gemm<128, 64, 16, 2, 2, 3, false, false, false>;
+  static constexpr int NT = 128, BM = 128, BN = 64, MINB = 3;
+};
+template <>
+struct K3Cfg<true, 3> {
+  using G = Gemm<64, 64, 16, 2, 2, 3, true, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 2;
+};
+template <>
+struct K3Cfg<false, 4> {  // real 64x64, 4 CTAs per SM (16 warps), least ragged-tile padding
+  using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
+};
+template <>
+struct K3Cfg<true, 4> {
+  using G = Gemm<64, 64, 16, 2, 2, 3, true, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 2;
+};
+
 template <bool C, int CFG>
 __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_update(K3Args a) {
   using Cf = K3Cfg<C, CFG>;
@@ -651,11 +683,28 @@ void launch_k2(bool cplx, const K2Args& a, int nstrips, cudaStream_t st) {
   }
 }
 
+template <int CFG>
+static int bm_of(bool cplx) { return cplx ? K3Cfg<true, CFG>::BM : K3Cfg<false, CFG>::BM; }
+template <int CFG>
+static int bn_of(bool cplx) { return cplx ? K3Cfg<true, CFG>::BN : K3Cfg<false, CFG>::BN; }
+
 int k3_bm(bool cplx, int cfg) {
-  return cfg == 1 ? (cplx ? K3Cfg<true, 1>::BM : K3Cfg<false, 1>::BM) : (cplx ? K3Cfg<true, 0>::BM : K3Cfg<false, 0>::BM);
+  switch (cfg) {
+    case 0: return bm_of<0>(cplx);
+    case 2: return bm_of<2>(cplx);
+    case 3: return bm_of<3>(cplx);
+    case 4: return bm_of<4>(cplx);
+    default: return bm_of<1>(cplx);
+  }
 }
 int k3_bn(bool cplx, int cfg) {
-  return cfg == 1 ? (cplx ? K3Cfg<true, 1>::BN : K3Cfg<false, 1>::BN) : (cplx ? K3Cfg<true, 0>::BN : K3Cfg<false, 0>::BN);
+  switch (cfg) {
+    case 0: return bn_of<0>(cplx);
+    case 2: return bn_of<2>(cplx);
+    case 3: return bn_of<3>(cplx);
+    case 4: return bn_of<4>(cplx);
+    default: return bn_of<1>(cplx);
+  }
 }
 
 template <bool C, int CFG>
@@ -665,14 +714,20 @@ static void launch_k3_t(const K3Args& a, int ntiles, cudaStream_t st) {
   k3_update<C, CFG><<<ntiles, Cf::NT, Cf::G::SMEM_BYTES, st>>>(a);
 }
 
+template <int CFG>
+static void launch_k3_c(bool cplx, const K3Args& a, int ntiles, cudaStream_t st) {
+  if (cplx) launch_k3_t<true, CFG>(a, ntiles, st);
+  else launch_k3_t<false, CFG>(a, ntiles, st);
+}
+
 void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st) {
   if (ntiles == 0) return;
-  if (cfg == 1) {
-    if (cplx) launch_k3_t<true, 1>(a, ntiles, st);
-    else launch_k3_t<false, 1>(a, ntiles, st);
-  } else {
-    if (cplx) launch_k3_t<true, 0>(a, ntiles, st);
-    else launch_k3_t<false, 0>(a, ntiles, st);
+  switch (cfg) {
+    case 0: launch_k3_c<0>(cplx, a, ntiles, st); break;
+    case 2: launch_k3_c<2>(cplx, a, ntiles, st); break;
+    case 3: launch_k3_c<3>(cplx, a, ntiles, st); break;
+    case 4: launch_k3_c<4>(cplx, a, ntiles, st); break;
+    default: launch_k3_c<1>(cplx, a, ntiles, st); break;
   }
 }
 

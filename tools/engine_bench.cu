@@ -1,0 +1,91 @@
+// Microbenchmark of the DMMA tile engine (paper_2002_05019_b200/csrc/gemm_core.cuh) on a dense
+// C -= A B^T (M = N = K = 8192), no sparsity, to separate engine efficiency from the
+// block-sparse workload's tile structure.  Build + run (GPU box):
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2002_05019_b200/csrc \
+//        tools/engine_bench.cu -o /tmp/engine_bench && /tmp/engine_bench
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <vector>
+
+#include "gemm_core.cuh"
+
+using namespace ddk;
+
+template <class G, bool C, int BM, int BN>
+__global__ void __launch_bounds__(G::NTHR) dense(const double* A, const double* B, double* Cm, int M, int N, int K,
+                                                 int64_t aim, int64_t bim, int64_t cim, int ksplit) {
+  extern __shared__ __align__(16) double smem[];
+  const int tm = blockIdx.x % (M / BM), tn = blockIdx.x / (M / BM);
+  typename G::Acc acc;
+  G::zero(acc);
+  // K split into segments of ksplit columns (exercises the gathered-K path like k3_update)
+  auto segfn = [&](int q) {
+    Seg s;
+    s.a = A + (int64_t)q * ksplit * M;
+    s.b = B + (int64_t)q * ksplit * N;
+    s.acol = nullptr;
+    s.lda = M;
+    s.ldb = N;
+    s.K = ksplit;
+    return s;
+  };
+  G::run(segfn, K / ksplit, tm * BM, tn * BN, M, N, aim, bim, smem, acc);
+  double* Cb = Cm + (int64_t)tm * BM + (int64_t)tn * BN * M;
+  G::for_each(acc, [&](int r, int c, double vr, double vi) {
+    int64_t e = (int64_t)r + (int64_t)c * M;
+    Cb[e] -= vr;
+    if (C) Cb[e + cim] -= vi;
+  });
+}
+
+template <class G, bool C, int BM, int BN>
+void run(const char* name, int M, int K, int ksplit) {
+  const int N = M;
+  const int pl = C ? 2 : 1;
+  double *A, *B, *Cm;
+  cudaMalloc(&A, (size_t)M * K * pl * 8);
+  cudaMalloc(&B, (size_t)N * K * pl * 8);
+  cudaMalloc(&Cm, (size_t)M * N * pl * 8);
+  cudaMemset(A, 0, (size_t)M * K * pl * 8);
+  cudaMemset(B, 0, (size_t)N * K * pl * 8);
+  cudaMemset(Cm, 0, (size_t)M * N * pl * 8);
+  auto kern = dense<G, C, BM, BN>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_BYTES);
+  int grid = (M / BM) * (N / BN);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::NTHR, G::SMEM_BYTES);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int it = 0; it < 2; ++it)
+    kern<<<grid, G::NTHR, G::SMEM_BYTES>>>(A, B, Cm, M, N, K, (int64_t)M * K, (int64_t)N * K, (int64_t)M * N, ksplit);
+  cudaEventRecord(e0);
+  const int reps = 3;
+  for (int it = 0; it < reps; ++it)
+    kern<<<grid, G::NTHR, G::SMEM_BYTES>>>(A, B, Cm, M, N, K, (int64_t)M * K, (int64_t)N * K, (int64_t)M * N, ksplit);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  double flops = 2.0 * M * N * (double)K * (C ? 4 : 1) * reps;
+  printf("%-34s M=N=%d K=%d ksplit=%d occ=%d/SM smem=%zuKB  %.2f TF/s  err=%s\n", name, M, K, ksplit, occ,
+         G::SMEM_BYTES / 1024, flops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(A);
+  cudaFree(B);
+  cudaFree(Cm);
+}
+
+int main() {
+  // configurations used by k3_update (see kernels_factor.cu K3Cfg)
+  run<Gemm<128, 64, 16, 2, 2, 3, false, false, false>, false, 128, 64>("real 128x64 4w 3st (cfg1)", 8192, 8192, 512);
+  run<Gemm<128, 64, 16, 2, 2, 4, false, false, false>, false, 128, 64>("real 128x64 4w 4st (cfg2)", 8192, 8192, 512);
+  run<Gemm<128, 128, 16, 2, 4, 4, false, false, false>, false, 128, 128>("real 128x128 8w 4st (cfg0)", 8192, 8192, 512);
+  run<Gemm<64, 64, 16, 2, 2, 3, false, false, false>, false, 64, 64>("real 64x64 4w 3st", 8192, 8192, 512);
+  run<Gemm<128, 64, 32, 2, 2, 3, false, false, false>, false, 128, 64>("real 128x64 4w BK32 3st", 8192, 8192, 512);
+  run<Gemm<64, 128, 16, 2, 2, 3, false, false, false>, false, 64, 128>("real 64x128 4w 3st", 8192, 8192, 512);
+  run<Gemm<64, 64, 16, 2, 2, 3, true, false, false>, true, 64, 64>("cplx 64x64 4w 3st (cfg1)", 8192, 4096, 512);
+  run<Gemm<64, 128, 16, 2, 4, 3, true, false, false>, true, 64, 128>("cplx 64x128 8w 3st (cfg0)", 8192, 4096, 512);
+  run<Gemm<128, 64, 16, 2, 2, 3, false, false, false>, false, 128, 64>("real 128x64 4w 3st ksplit 8192", 8192, 8192, 8192);
+  return 0;
+}
