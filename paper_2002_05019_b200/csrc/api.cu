@@ -349,8 +349,8 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   {
     const char* ev = getenv("DD_AUX_K3CFG");
     // default tile config per scalar type (measured on B200): real 64x64 at
-    // 4 CTAs/SM (least ragged-tile padding), complex 64x64 4M at 2 CTAs/SM
-    h->k3cfg = ev ? atoi(ev) : (h->cplx ? 1 : 4);
+    // 4 CTAs/SM (least ragged-tile padding), complex 64x32 4M, 2 stages, 4 CTAs/SM
+    h->k3cfg = ev ? atoi(ev) : (h->cplx ? 5 : 4);
     const char* la = getenv("DD_AUX_LOOKAHEAD");
     h->lookahead = la ? atoi(la) != 0 : true;
   }
@@ -840,7 +840,9 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
   a.nrows = h->n_pad;
   a.flag = flag;
   const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
-  for (const LevelRanges& R : h->lv) {
+  for (int l = 0; l < (int)h->lv.size(); ++l) {
+    const LevelRanges& R = h->lv[l];
+    h->cur_level = l;
     SolveArgs b = a;
     b.nodes = lvlnodes + R.n0;
     {
@@ -857,11 +859,13 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
   }
   {
     TraceScope ts(h, DD_PH_DSOLVE, 0.0, st);
-    launch_dsolve(C, a, st);
+    h->cur_level = -1;
+  launch_dsolve(C, a, st);
   }
   LAUNCH_CHECK("k_dsolve");
   for (int l = (int)h->lv.size() - 1; l >= 0; --l) {
     const LevelRanges& R = h->lv[l];
+    h->cur_level = l;
     SolveArgs b = a;
     b.btiles = a.btiles + R.b0;
     if (R.b1 > R.b0) {
@@ -876,6 +880,7 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
     }
     LAUNCH_CHECK("k_bdiag");
   }
+  h->cur_level = -1;
   return DD_OK;
 }
 

@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
         if (absakk >= alpha * colmax * (colmax / rowmax)) {
           kp = k;
         } else {
-          __threadfence();
+          __threadfence_block();
           const double aii = cabs1<C>(ld<C>(W, Wel(imax, kk + 1), wim));
           if (aii >= alpha * rowmax) {
             kp = imax;
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           if (kp != k + 1) ++nswap;
         }
       }
-      __threadfence();
+      __threadfence_block();  // consumers are this CTA's own plain loads (L1-coherent)
       __syncthreads();
       k += kstep;
     }
@@ -561,6 +561,17 @@ struct K3Cfg<true, 4> {
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 2;
 };
 
+template <>
+struct K3Cfg<false, 5> {  // real 64x32, 3 stages, 5 CTAs per SM
+  using G = Gemm<64, 32, 16, 2, 2, 3, false, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 5;
+};
+template <>
+struct K3Cfg<true, 5> {  // complex 64x32, 2 stages, 4 CTAs per SM (dense microbench: 94% of ZGEMM)
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
+};
+
 template <bool C, int CFG>
 __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_update(K3Args a) {
   using Cf = K3Cfg<C, CFG>;
@@ -694,6 +705,7 @@ int k3_bm(bool cplx, int cfg) {
     case 2: return bm_of<2>(cplx);
     case 3: return bm_of<3>(cplx);
     case 4: return bm_of<4>(cplx);
+    case 5: return bm_of<5>(cplx);
     default: return bm_of<1>(cplx);
   }
 }
@@ -703,6 +715,7 @@ int k3_bn(bool cplx, int cfg) {
     case 2: return bn_of<2>(cplx);
     case 3: return bn_of<3>(cplx);
     case 4: return bn_of<4>(cplx);
+    case 5: return bn_of<5>(cplx);
     default: return bn_of<1>(cplx);
   }
 }
@@ -727,6 +740,7 @@ void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st)
     case 2: launch_k3_c<2>(cplx, a, ntiles, st); break;
     case 3: launch_k3_c<3>(cplx, a, ntiles, st); break;
     case 4: launch_k3_c<4>(cplx, a, ntiles, st); break;
+    case 5: launch_k3_c<5>(cplx, a, ntiles, st); break;
     default: launch_k3_c<1>(cplx, a, ntiles, st); break;
   }
 }

@@ -33,7 +33,8 @@ constexpr int BUPD_MAX_PARTS = 320;  // split-K partial tiles of the backward up
 using FUpdR = Gemm<SUBM, SBN, 16, 2, 2, 3, false, false, true>;
 using FUpdC = Gemm<SUBM, SBN, 16, 2, 2, 3, true, false, true>;
 using BUpdR = Gemm<SUBM, SBN, 16, 2, 2, 3, false, true, true>;
-using BUpdC = Gemm<SUBM, SBN, 16, 2, 2, 3, true, true, true>;
+// complex KM x KN: 2 stages so two CTAs fit per SM (3 stages: 120 KB -> 1 CTA, 26 vs 33 TF dense)
+using BUpdC = Gemm<SUBM, SBN, 16, 2, 2, 2, true, true, true>;
 
 // ---------------------------------------------------------------------------- permutations
 template <bool C>

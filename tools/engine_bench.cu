@@ -12,7 +12,7 @@
 
 using namespace ddk;
 
-template <class G, bool C, int BM, int BN>
+template <class G, bool C, int BM, int BN, bool AKM = false, bool BKN = false>
 __global__ void __launch_bounds__(G::NTHR) dense(const double* A, const double* B, double* Cm, int M, int N, int K,
                                                  int64_t aim, int64_t bim, int64_t cim, int ksplit) {
   extern __shared__ __align__(16) double smem[];
@@ -22,11 +22,12 @@ __global__ void __launch_bounds__(G::NTHR) dense(const double* A, const double* 
   // K split into segments of ksplit columns (exercises the gathered-K path like k3_update)
   auto segfn = [&](int q) {
     Seg s;
-    s.a = A + (int64_t)q * ksplit * M;
-    s.b = B + (int64_t)q * ksplit * N;
+    // MK: a[m + k*M]; KM: a[k + m*K]  /  NK: b[n + k*N]; KN: b[k + n*K]
+    s.a = AKM ? A + (int64_t)q * ksplit : A + (int64_t)q * ksplit * M;
+    s.b = BKN ? B + (int64_t)q * ksplit : B + (int64_t)q * ksplit * N;
     s.acol = nullptr;
-    s.lda = M;
-    s.ldb = N;
+    s.lda = AKM ? K : M;
+    s.ldb = BKN ? K : N;
     s.K = ksplit;
     return s;
   };
@@ -39,7 +40,7 @@ __global__ void __launch_bounds__(G::NTHR) dense(const double* A, const double* 
   });
 }
 
-template <class G, bool C, int BM, int BN>
+template <class G, bool C, int BM, int BN, bool AKM = false, bool BKN = false>
 void run(const char* name, int M, int K, int ksplit) {
   const int N = M;
   const int pl = C ? 2 : 1;
@@ -50,7 +51,7 @@ void run(const char* name, int M, int K, int ksplit) {
   cudaMemset(A, 0, (size_t)M * K * pl * 8);
   cudaMemset(B, 0, (size_t)N * K * pl * 8);
   cudaMemset(Cm, 0, (size_t)M * N * pl * 8);
-  auto kern = dense<G, C, BM, BN>;
+  auto kern = dense<G, C, BM, BN, AKM, BKN>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM_BYTES);
   int grid = (M / BM) * (N / BN);
   int occ = 0;
@@ -87,5 +88,12 @@ int main() {
   run<Gemm<64, 64, 16, 2, 2, 3, true, false, false>, true, 64, 64>("cplx 64x64 4w 3st (cfg1)", 8192, 4096, 512);
   run<Gemm<64, 128, 16, 2, 4, 3, true, false, false>, true, 64, 128>("cplx 64x128 8w 3st (cfg0)", 8192, 4096, 512);
   run<Gemm<128, 64, 16, 2, 2, 3, false, false, false>, false, 128, 64>("real 128x64 4w 3st ksplit 8192", 8192, 8192, 8192);
+  // solve-kernel layouts (fupd: MK x KN, bupd: KM x KN)
+  run<Gemm<64, 64, 16, 2, 2, 3, true, false, true>, true, 64, 64, false, true>("cplx 64x64 MKxKN (fupd)", 8192, 4096, 512);
+  run<Gemm<64, 64, 16, 2, 2, 3, true, true, true>, true, 64, 64, true, true>("cplx 64x64 KMxKN (bupd)", 8192, 4096, 512);
+  run<Gemm<64, 64, 16, 2, 2, 3, false, false, true>, false, 64, 64, false, true>("real 64x64 MKxKN (fupd)", 8192, 8192, 512);
+  run<Gemm<64, 64, 16, 2, 2, 3, false, true, true>, false, 64, 64, true, true>("real 64x64 KMxKN (bupd)", 8192, 8192, 512);
+  run<Gemm<64, 64, 32, 2, 2, 3, true, true, true>, true, 64, 64, true, true>("cplx 64x64 KMxKN BK32", 8192, 4096, 512);
+  run<Gemm<64, 32, 16, 2, 2, 2, true, false, false>, true, 64, 32>("cplx 64x32 2st", 8192, 4096, 512);
   return 0;
 }
