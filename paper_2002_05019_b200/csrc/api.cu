@@ -67,6 +67,7 @@ struct LevelRanges {
   int f0, f1;     // forward-solve tiles
   int b0, b1;     // backward-solve tiles
   double fl_k1, fl_k2, fl_k3;      // algorithmic flops of the level's factor kernels
+  int max_s;                       // largest diagonal block of the level
   double fl_diag, fl_upd;          // solve flops per rhs: one diagonal sweep / one update sweep
 };
 
@@ -196,6 +197,10 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   if (!out) return fail(-7, "out is NULL");
   std::string msg = validate_pattern(nblk, blk_size, colptr, rowidx);
   if (!msg.empty()) return fail(DD_ERR_PATTERN, msg);
+  for (int64_t j = 0; j < nblk; ++j)
+    if (blk_size[j] > K1_MAX_BLOCK)
+      return fail(DD_ERR_PATTERN, "interface size " + std::to_string(blk_size[j]) + " exceeds the supported maximum " +
+                                      std::to_string(K1_MAX_BLOCK));
   dd_aux_options opt;
   dd_aux_default_options(&opt);
   if (opt_in) opt = *opt_in;
@@ -458,7 +463,9 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
     {
       const double mu = h->cplx ? 4.0 : 1.0;
       R.fl_k1 = R.fl_k2 = R.fl_k3 = R.fl_diag = R.fl_upd = 0;
+      R.max_s = 0;
       for (int t : L) {
+        R.max_s = std::max(R.max_s, (int)h->nodes[t].s);
         double sv = h->nodes[t].s, rv = 0;
         for (int q = 0; q < h->nodes[t].nst; ++q) rv += h->nodes[st_pos[h->nodes[t].st0 + q]].s;
         R.fl_k1 += mu * sv * sv * sv / 3.0;
@@ -729,7 +736,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     k1.nodes = lvlnodes + R.n0;
     {
       TraceScope ts(h, DD_PH_K1, R.fl_k1, sd);
-      launch_k1(C, k1, R.n1 - R.n0, sd);
+      launch_k1(C, k1, R.n1 - R.n0, R.max_s, sd);
     }
     LAUNCH_CHECK("k1_diag_bk");
     RowpermArgs r = rp;

@@ -49,6 +49,8 @@ __global__ void k0_load(const double* __restrict__ vals, const LoadBlock* __rest
 
 // ============================================================================ K1 diagonal BK
 constexpr int NT1 = 256;
+constexpr size_t K1_LP_BUDGET = 192 * 1024;  // shared-memory bytes for the K1 panel copy of L
+// rows per thread: s <= NT1 * MAXQ (4 -> 1024 on the fast path, 16 -> 4096 for larger interfaces)
 using K1GemmR = Gemm<64, 64, 16, 2, 4, 2, false, false, false>;
 using K1GemmC = Gemm<64, 64, 16, 2, 4, 2, true, false, false>;
 
@@ -87,15 +89,18 @@ __device__ __forceinline__ void block_argmax(double& v, int& i, double* shv, int
   __syncthreads();
 }
 
-template <bool C>
+template <bool C, int K1_MAXQ>
 __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
   using G = typename std::conditional<C, K1GemmC, K1GemmR>::type;
   extern __shared__ __align__(16) double smem[];
   __shared__ double shv[NT1 / 32];
   __shared__ int shi[NT1 / 32];
   __shared__ double wrow_r[K1NB], wrow_i[K1NB];
+  __shared__ double wt_r[K1NB][K1NB + 1];
+  __shared__ int s_swa[K1NB], s_swb[K1NB], s_nswp;
+  __shared__ double wt_i[C ? K1NB : 1][C ? K1NB + 1 : 1];
   __shared__ int s_kp, s_kstep, s_zero, s_imax;
-  __shared__ double s_absakk, s_colmax;
+  __shared__ double s_absakk2[2];  // parity-buffered: no barrier between a read and the next write
 
   const int t = a.nodes[blockIdx.x];
   const NodeDev nd = a.nd[t];
@@ -120,30 +125,52 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
   int n2x2 = 0, nswap = 0, zero_col = -1;
   __syncthreads();
 
+  // Panel width NB: the current panel's L columns live in shared memory (Lp, <= K1_LP_BUDGET
+  // bytes; aliased later by the trailing-update GEMM and the inverse staging) and reach
+  // global memory only at the panel end; W rows of the panel window [c0, c0+NB) are cached in
+  // wt.  Thread tid owns rows tid + q*NT1 (q < K1_MAXQ) for the whole factorization and keeps
+  // their current W values in registers, so a column without interchange costs two barriers.
+  // Interchanges of rows inside L columns of EARLIER panels (explicit form, L5) are deferred
+  // to the panel end (LAPACK xLASWP style): nothing in this kernel reads those columns before.
+  int NB = K1NB;
+  while (NB > 8 && (size_t)s * NB * (C ? 16 : 8) > K1_LP_BUDGET) NB = NB > 16 ? NB - 8 : NB / 2;
+  double* Lpr = smem;                       // Lp(i, m) = Lpr[m * s + i]
+  double* Lpi = smem + (size_t)s * NB;
+  auto LP = [&](int i, int m) { return (size_t)m * s + i; };
+  cz Ak[K1_MAXQ], wv[K1_MAXQ], wv2[K1_MAXQ];
+#pragma unroll
+  for (int q = 0; q < K1_MAXQ; ++q) {
+    const int i = tid + q * NT1;
+    Ak[q] = i < s ? ld<C>(A, Ael(i, 0), aim) : mk(0.0, 0.0);
+  }
+
   int k = 0;
   while (k < s) {
     const int c0 = k;
-    const bool last_panel = (s - c0) <= K1NB;
+    const bool last_panel = (s - c0) <= NB;
+    if (tid == 0) s_nswp = 0;
     // ------------------------------------------------------------ panel (left-looking)
     while (k < s) {
       const int kk = k - c0;
-      if (!last_panel && kk >= K1NB - 1) break;
-      // W(k, 0:kk) -> shared
-      for (int m = tid; m < kk; m += NT1) {
-        cz w = ld<C>(W, Wel(k, m), wim);
-        wrow_r[m] = w.r;
-        wrow_i[m] = w.i;
-      }
-      __syncthreads();
-      // updated column k:  W(k:s, kk) = A(k:s, k) - L(k:s, c0:k) W(k, 0:kk)^T
+      if (!last_panel && kk >= NB - 1) break;
+      // updated column k:  W(k:s, kk) = A(k:s, k) - Lp(k:s, 0:kk) W(k, 0:kk)^T  (W row k: window)
       double bv = -1.0;
       int bi = INT_MAX;
-      for (int i = k + tid; i < s; i += NT1) {
-        cz v = ld<C>(A, Ael(i, k), aim);
-        for (int m = 0; m < kk; ++m) v = fms<C>(v, ld<C>(A, Ael(i, c0 + m), aim), mk(wrow_r[m], wrow_i[m]));
+#pragma unroll
+      for (int q = 0; q < K1_MAXQ; ++q) {
+        const int i = tid + q * NT1;
+        if (i < k || i >= s) continue;
+        cz v = Ak[q];
+        for (int m = 0; m < kk; ++m)
+          v = fms<C>(v, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0), mk(wt_r[kk][m], C ? wt_i[kk][m] : 0.0));
+        wv[q] = v;
         st<C>(W, Wel(i, kk), wim, v);
+        if (i - c0 < NB) {
+          wt_r[i - c0][kk] = v.r;
+          if constexpr (C) wt_i[i - c0][kk] = v.i;
+        }
         double av = cabs1<C>(v);
-        if (i == k) s_absakk = av;
+        if (i == k) s_absakk2[k & 1] = av;
         else if (av > bv) {
           bv = av;
           bi = i;
@@ -151,7 +178,7 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
       }
       block_argmax(bv, bi, shv, shi);
       // ---- pivot decision (Bunch-Kaufman, LAPACK xSYTF2 order)
-      const double absakk = s_absakk;
+      const double absakk = s_absakk2[k & 1];
       const double colmax = bv > 0.0 ? bv : 0.0;
       const int imax = bi;
       int kp, kstep = 1;
@@ -163,18 +190,32 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
         kp = k;
       } else {
         // updated column imax -> W(:, kk+1) (symmetric access of the not-yet-updated trailing A)
-        for (int m = tid; m < kk; m += NT1) {
-          cz w = ld<C>(W, Wel(imax, m), wim);
-          wrow_r[m] = w.r;
-          wrow_i[m] = w.i;
+        const bool inwin = imax - c0 < NB;
+        if (!inwin) {
+          for (int m = tid; m < kk; m += NT1) {
+            cz w = ld<C>(W, Wel(imax, m), wim);
+            wrow_r[m] = w.r;
+            wrow_i[m] = w.i;
+          }
+          __syncthreads();
         }
-        __syncthreads();
         double rv = -1.0;
         int ri = INT_MAX;
-        for (int i = k + tid; i < s; i += NT1) {
+#pragma unroll
+        for (int q = 0; q < K1_MAXQ; ++q) {
+          const int i = tid + q * NT1;
+          if (i < k || i >= s) continue;
           cz v = (i < imax) ? ld<C>(A, Ael(imax, i), aim) : ld<C>(A, Ael(i, imax), aim);
-          for (int m = 0; m < kk; ++m) v = fms<C>(v, ld<C>(A, Ael(i, c0 + m), aim), mk(wrow_r[m], wrow_i[m]));
+          for (int m = 0; m < kk; ++m) {
+            const cz w = inwin ? mk(wt_r[imax - c0][m], C ? wt_i[imax - c0][m] : 0.0) : mk(wrow_r[m], wrow_i[m]);
+            v = fms<C>(v, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0), w);
+          }
+          wv2[q] = v;
           st<C>(W, Wel(i, kk + 1), wim, v);
+          if (i - c0 < NB) {
+            wt_r[i - c0][kk + 1] = v.r;
+            if constexpr (C) wt_i[i - c0][kk + 1] = v.i;
+          }
           if (i != imax) {
             double av = cabs1<C>(v);
             if (av > rv) {
@@ -188,52 +229,90 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
         if (absakk >= alpha * colmax * (colmax / rowmax)) {
           kp = k;
         } else {
-          __threadfence_block();
-          const double aii = cabs1<C>(ld<C>(W, Wel(imax, kk + 1), wim));
-          if (aii >= alpha * rowmax) {
-            kp = imax;
-            for (int i = k + tid; i < s; i += NT1) st<C>(W, Wel(i, kk), wim, ld<C>(W, Wel(i, kk + 1), wim));
+          const double aii = cabs1<C>(inwin ? mk(wt_r[imax - c0][kk + 1], C ? wt_i[imax - c0][kk + 1] : 0.0)
+                                            : ld<C>(W, Wel(imax, kk + 1), wim));
+          kp = imax;
+          if (aii >= alpha * rowmax) {  // 1x1 pivot on the imax column: it becomes column kk
+#pragma unroll
+            for (int q = 0; q < K1_MAXQ; ++q) {
+              const int i = tid + q * NT1;
+              if (i < k || i >= s) continue;
+              wv[q] = wv2[q];
+              st<C>(W, Wel(i, kk), wim, wv2[q]);
+              if (i - c0 < NB) {
+                wt_r[i - c0][kk] = wv2[q].r;
+                if constexpr (C) wt_i[i - c0][kk] = wv2[q].i;
+              }
+            }
           } else {
-            kp = imax;
             kstep = 2;
           }
         }
       }
-      __syncthreads();
       const int kkk = k + kstep - 1;
       if (kp != kkk) {
+        __syncthreads();
         // move the non-updated column kkk of the trailing block to position kp (dlasyf)
         if (tid == 0) st<C>(A, Ael(kp, kp), aim, ld<C>(A, Ael(kkk, kkk), aim));
         for (int j = kkk + 1 + tid; j < kp; j += NT1) st<C>(A, Ael(kp, j), aim, ld<C>(A, Ael(j, kkk), aim));
         for (int j = kp + 1 + tid; j < s; j += NT1) st<C>(A, Ael(j, kp), aim, ld<C>(A, Ael(j, kkk), aim));
-        // explicit form (L5): interchange rows kkk, kp in every computed L column 0..k-1
-        for (int j = tid; j < k; j += NT1) {
-          cz x = ld<C>(A, Ael(kkk, j), aim), y = ld<C>(A, Ael(kp, j), aim);
-          st<C>(A, Ael(kkk, j), aim, y);
-          st<C>(A, Ael(kp, j), aim, x);
+        // rows kkk, kp of the panel's L columns (shared copy) -- earlier panels: deferred
+        for (int m = tid; m < kk; m += NT1) {
+          double t0 = Lpr[LP(kkk, m)];
+          Lpr[LP(kkk, m)] = Lpr[LP(kp, m)];
+          Lpr[LP(kp, m)] = t0;
+          if constexpr (C) {
+            double t1 = Lpi[LP(kkk, m)];
+            Lpi[LP(kkk, m)] = Lpi[LP(kp, m)];
+            Lpi[LP(kp, m)] = t1;
+          }
         }
-        // rows kkk, kp of W columns 0..kk+kstep-1
+        // rows kkk, kp of W columns 0..kk+kstep-1 (global, and the window cache)
+        const bool kpwin = kp - c0 < NB;
         for (int m = tid; m < kk + kstep; m += NT1) {
           cz x = ld<C>(W, Wel(kkk, m), wim), y = ld<C>(W, Wel(kp, m), wim);
           st<C>(W, Wel(kkk, m), wim, y);
           st<C>(W, Wel(kp, m), wim, x);
+          wt_r[kkk - c0][m] = y.r;
+          if constexpr (C) wt_i[kkk - c0][m] = y.i;
+          if (kpwin) {
+            wt_r[kp - c0][m] = x.r;
+            if constexpr (C) wt_i[kp - c0][m] = x.i;
+          }
         }
         if (tid == 0) {
           int x = perm[kkk];
           perm[kkk] = perm[kp];
           perm[kp] = x;
+          s_swa[s_nswp] = kkk;
+          s_swb[s_nswp] = kp;
+          ++s_nswp;
+        }
+        __threadfence_block();
+        __syncthreads();
+        // register copies of the two exchanged rows
+#pragma unroll
+        for (int q = 0; q < K1_MAXQ; ++q) {
+          const int i = tid + q * NT1;
+          if (i == kkk || i == kp) {
+            wv[q] = ld<C>(W, Wel(i, kk), wim);
+            if (kstep == 2) wv2[q] = ld<C>(W, Wel(i, kk + 1), wim);
+          }
         }
       }
-      __syncthreads();
-      // ---- store L and D
+      // ---- L columns (shared panel copy) and D; the next column is prefetched
       if (kstep == 1) {
-        const cz D = ld<C>(W, Wel(k, kk), wim);
-        for (int i = k + 1 + tid; i < s; i += NT1) {
-          cz w = ld<C>(W, Wel(i, kk), wim);
-          st<C>(A, Ael(i, k), aim, zero ? w : dv<C>(w, D));
+        const cz D = mk(wt_r[kk][kk], C ? wt_i[kk][kk] : 0.0);
+        const cz rD = zero ? mk(1.0, 0.0) : dv<C>(mk(1.0, 0.0), D);
+#pragma unroll
+        for (int q = 0; q < K1_MAXQ; ++q) {
+          const int i = tid + q * NT1;
+          if (i <= k || i >= s) continue;
+          const cz l = mul<C>(wv[q], rD);
+          Lpr[LP(i, kk)] = l.r;
+          if constexpr (C) Lpi[LP(i, kk)] = l.i;
         }
         if (tid == 0) {
-          st<C>(A, Ael(k, k), aim, D);
           st<C>(dv_, 0 + k, aim, D);
           st<C>(ev_, 0 + k, aim, mk(0.0, 0.0));
           ipiv[k] = kp + 1;
@@ -241,21 +320,29 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           if (kp != k) ++nswap;
         }
       } else {
-        const cz w11 = ld<C>(W, Wel(k, kk), wim), w21 = ld<C>(W, Wel(k + 1, kk), wim),
-                 w22 = ld<C>(W, Wel(k + 1, kk + 1), wim);
+        const cz w11 = mk(wt_r[kk][kk], C ? wt_i[kk][kk] : 0.0), w21 = mk(wt_r[kk + 1][kk], C ? wt_i[kk + 1][kk] : 0.0),
+                 w22 = mk(wt_r[kk + 1][kk + 1], C ? wt_i[kk + 1][kk + 1] : 0.0);
         // LAPACK dlasyf scaled closed form of [W_k W_k+1] D^{-1}
         const cz d11 = dv<C>(w22, w21), d22 = dv<C>(w11, w21);
         const cz tt = dv<C>(mk(1.0, 0.0), mul<C>(d11, d22) - mk(1.0, 0.0));
         const cz d21 = dv<C>(tt, w21);
-        for (int i = k + 2 + tid; i < s; i += NT1) {
-          cz wk = ld<C>(W, Wel(i, kk), wim), wk1 = ld<C>(W, Wel(i, kk + 1), wim);
-          st<C>(A, Ael(i, k), aim, mul<C>(d21, mul<C>(d11, wk) - wk1));
-          st<C>(A, Ael(i, k + 1), aim, mul<C>(d21, mul<C>(d22, wk1) - wk));
+#pragma unroll
+        for (int q = 0; q < K1_MAXQ; ++q) {
+          const int i = tid + q * NT1;
+          if (i <= k || i >= s) continue;
+          cz l0 = mk(0.0, 0.0), l1 = mk(0.0, 0.0);  // row k+1: identity 2x2 block of L
+          if (i > k + 1) {
+            l0 = mul<C>(d21, mul<C>(d11, wv[q]) - wv2[q]);
+            l1 = mul<C>(d21, mul<C>(d22, wv2[q]) - wv[q]);
+          }
+          Lpr[LP(i, kk)] = l0.r;
+          Lpr[LP(i, kk + 1)] = l1.r;
+          if constexpr (C) {
+            Lpi[LP(i, kk)] = l0.i;
+            Lpi[LP(i, kk + 1)] = l1.i;
+          }
         }
         if (tid == 0) {
-          st<C>(A, Ael(k, k), aim, w11);
-          st<C>(A, Ael(k + 1, k), aim, mk(0.0, 0.0));  // L is unit lower with an identity 2x2 block
-          st<C>(A, Ael(k + 1, k + 1), aim, w22);
           st<C>(dv_, k, aim, w11);
           st<C>(dv_, k + 1, aim, w22);
           st<C>(ev_, k, aim, w21);
@@ -265,9 +352,35 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           if (kp != k + 1) ++nswap;
         }
       }
-      __threadfence_block();  // consumers are this CTA's own plain loads (L1-coherent)
-      __syncthreads();
       k += kstep;
+      if (k < s && !(kk + kstep >= NB - 1 && !last_panel)) {
+#pragma unroll
+        for (int q = 0; q < K1_MAXQ; ++q) {
+          const int i = tid + q * NT1;
+          if (i >= k && i < s) Ak[q] = ld<C>(A, Ael(i, k), aim);
+        }
+      }
+    }
+    // ------------------------------------------------------------ panel end
+    __syncthreads();
+    {
+      const int kb = k - c0;
+      // the panel's L columns and D diagonal to global memory
+      for (int m = 0; m < kb; ++m) {
+        const int col = c0 + m;
+        for (int i = col + 1 + tid; i < s; i += NT1)
+          st<C>(A, Ael(i, col), aim, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0));
+        if (tid == 0) st<C>(A, Ael(col, col), aim, ld<C>(dv_, col, aim));
+      }
+      // deferred interchanges in the L columns of earlier panels (in pivot order)
+      const int nsw = s_nswp;
+      for (int j = tid; j < c0; j += NT1)
+        for (int q = 0; q < nsw; ++q) {
+          const int r0 = s_swa[q], r1 = s_swb[q];
+          cz x = ld<C>(A, Ael(r0, j), aim), y = ld<C>(A, Ael(r1, j), aim);
+          st<C>(A, Ael(r0, j), aim, y);
+          st<C>(A, Ael(r1, j), aim, x);
+        }
     }
     // ------------------------------------------------------------ trailing update (DMMA)
     if (k < s) {
@@ -302,10 +415,17 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
         }
       __threadfence();
       __syncthreads();
+#pragma unroll
+      for (int q = 0; q < K1_MAXQ; ++q) {
+        const int i = tid + q * NT1;
+        if (i >= k && i < s) Ak[q] = ld<C>(A, Ael(i, k), aim);
+      }
     }
   }
 
   // ---------------------------------------------------------------- inverse diagonal tiles of L
+  __threadfence_block();
+  __syncthreads();
   {
     const int ntiles = (s + TB - 1) / TB;
     const int warp = tid >> 5, lane = tid & 31;
@@ -656,17 +776,24 @@ void launch_load(bool cplx, const double* vals, const LoadBlock* lb, int nblocks
 size_t k1_smem(bool cplx) {
   size_t g = cplx ? K1GemmC::SMEM_BYTES : K1GemmR::SMEM_BYTES;
   size_t inv = (size_t)(NT1 / 32) * 2 * TB * TB * sizeof(double);
-  return g > inv ? g : inv;
+  size_t m = g > inv ? g : inv;
+  return m > K1_LP_BUDGET ? m : K1_LP_BUDGET;
 }
 
-void launch_k1(bool cplx, const K1Args& a, int nnodes, cudaStream_t st) {
-  size_t sm = k1_smem(cplx);
-  if (cplx) {
-    set_smem(k1_diag_bk<true>, sm);
-    k1_diag_bk<true><<<nnodes, NT1, sm, st>>>(a);
+template <bool C, int Q>
+static void launch_k1_t(const K1Args& a, int nnodes, cudaStream_t st) {
+  const size_t sm = k1_smem(C);
+  set_smem(k1_diag_bk<C, Q>, sm);
+  k1_diag_bk<C, Q><<<nnodes, NT1, sm, st>>>(a);
+}
+
+void launch_k1(bool cplx, const K1Args& a, int nnodes, int max_s, cudaStream_t st) {
+  if (max_s <= NT1 * 4) {
+    if (cplx) launch_k1_t<true, 4>(a, nnodes, st);
+    else launch_k1_t<false, 4>(a, nnodes, st);
   } else {
-    set_smem(k1_diag_bk<false>, sm);
-    k1_diag_bk<false><<<nnodes, NT1, sm, st>>>(a);
+    if (cplx) launch_k1_t<true, 16>(a, nnodes, st);
+    else launch_k1_t<false, 16>(a, nnodes, st);
   }
 }
 

@@ -115,7 +115,8 @@ struct SpmvArgs {
 void launch_load(bool cplx, const double* vals, const LoadBlock* lb, int nblocks, int64_t max_elems, double* arena,
                  int64_t aim, cudaStream_t st);
 size_t k1_smem(bool cplx);
-void launch_k1(bool cplx, const K1Args& a, int nnodes, cudaStream_t st);
+void launch_k1(bool cplx, const K1Args& a, int nnodes, int max_s, cudaStream_t st);
+constexpr int K1_MAX_BLOCK = 4096;  // largest interface (diagonal block) size K1 supports
 void launch_rowperm(bool cplx, const RowpermArgs& a, int nlist, int max_s, cudaStream_t st);
 void launch_k2(bool cplx, const K2Args& a, int nstrips, cudaStream_t st);
 int k3_bm(bool cplx, int cfg);
