@@ -35,8 +35,8 @@ sys.path.insert(0, ROOT)
 import dd_inputs  # noqa: E402
 
 # bounded oracle samples: corner sub-grid of the same workload
-SAMPLE_GRID = {"cfg0": (2, 2, 1), "cfg1": (4, 4, 2), "cfg2": (3, 3, 2), "cfg3": (3, 3, 2), "cfg3alt": (3, 3, 2),
-               "cfg4": (3, 3, 2)}
+SAMPLE_GRID = {"cfg0": (2, 2, 1), "cfg1": (4, 4, 2), "cfg2": (3, 2, 2), "cfg3": (3, 2, 2), "cfg3alt": (3, 2, 2),
+               "cfg4": (3, 2, 2)}
 WORKLOAD_TXT = {
     "cfg0": "configs[0]: 2x2x1 grid, 4 x 32 real fp64, n=128",
     "cfg1": "configs[1]: 4x4x4 grid, 144 x 256 real fp64, n=36864, ND order",
