@@ -308,10 +308,12 @@ def gpu_arm(args, rank, world, local, dist):
     dom = max(trace, key=lambda p: trace[p]["ms"])
     dk = trace[dom]
     achieved = dk["flops"] / (dk["ms"] * 1e-3) / 1e12 if dk["ms"] > 0 else 0.0
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{cfg}.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(dom)
+    if os.path.exists(tpath):  # dram read+write bytes per launch from one ncu --set full capture
+        t = json.load(open(tpath)).get(dom)
+        if t:
+            traffic, traffic_src = t["dram_bytes_per_launch"], t["launch"]
     step_ms = total_ms / K
 
     # ---- e2e: host buffers through the public API (H2D inputs, D2H result inside the region)
@@ -364,7 +366,7 @@ def gpu_arm(args, rank, world, local, dist):
                      "pivots": {"n2x2": finfo["n2x2"], "nswaps": finfo["nswaps"]},
                      "inertia": None if cplx else [finfo["npos"], finfo["nneg"], finfo["nzero"]]},
         "roofline": {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": achieved / peak_tf, "traffic": traffic,
+                     "frac": achieved / peak_tf, "traffic": traffic, "traffic_src": traffic_src,
                      "peak_src": f"measured cuBLAS {'ZGEMM' if cplx else 'DGEMM'} 8192^3 ({peak_src})"},
         "phases": {p: {"ms_per_step": v["ms"] / K, "launches_per_step": v["launches"] / K,
                        "tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["ms"] > 0 and v["flops"] > 0 else None}
