@@ -162,7 +162,7 @@ int dd_aux_set_refine(dd_aux_handle_t h, int32_t refine_steps, double refine_tol
 enum {
   DD_PH_LOAD = 0, DD_PH_K1, DD_PH_ROWPERM, DD_PH_K2, DD_PH_K3, DD_PH_STATS,
   DD_PH_PERM, DD_PH_FDIAG, DD_PH_FUPD, DD_PH_DSOLVE, DD_PH_BUPD, DD_PH_BDIAG, DD_PH_SPMV,
-  DD_NPHASE
+  DD_PH_LINV, DD_NPHASE
 };
 typedef struct {
   double ms[16];        /* device milliseconds per kernel class (tracing enabled only) */

@@ -34,7 +34,7 @@ EXPORTED_SYMBOLS = ["dd_aux_default_options", "dd_aux_analyze", "dd_aux_get_info
                     "dd_aux_get_pivots", "dd_aux_set_refine", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_get_level_trace", "dd_aux_destroy",
                     "dd_aux_last_error", "dd_aux_version"]
 PHASES = ["load", "k1_diag_bk", "rowperm", "k2_panel", "k3_update", "stats", "perm", "fdiag", "fupd", "dsolve",
-          "bupd", "bdiag", "spmv"]
+          "bupd", "bdiag", "spmv", "linv"]
 
 
 class DDAuxError(RuntimeError):

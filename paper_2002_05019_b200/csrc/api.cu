@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <numeric>
 #include <cstdlib>
 #include <cstring>
@@ -62,10 +64,13 @@ struct LevelRanges {
   int n0, n1;     // level nodes
   int s0, s1;     // K2 strips
   int r0, r1;     // rowperm entries
-  int t0, t1;     // K3 tiles: [t0, ta) update the next level's panels, [ta, t1) the rest
+  int t0, t1;     // K3 targets: [t0, ta) update the next level's panels, [ta, t1) the rest
   int ta;
+  int64_t tiles_a, tiles_b;  // implicit tile counts of the two parts
   int f0, f1;     // forward-solve tiles
   int b0, b1;     // backward-solve tiles
+  int d0, d1;     // diagonal-solve tiles (node, 64-row tile)
+  int i0, i1;     // inverse work items (node, TB column tile)
   double fl_k1, fl_k2, fl_k3;      // algorithmic flops of the level's factor kernels
   int max_s;                       // largest diagonal block of the level
   double fl_diag, fl_upd;          // solve flops per rhs: one diagonal sweep / one update sweep
@@ -93,7 +98,8 @@ struct dd_aux_handle_s {
   Blob blob;
   size_t off_nodes = 0, off_stpos = 0, off_strow = 0, off_lvlnodes = 0, off_strips = 0, off_rowperm = 0,
          off_targets = 0, off_contribs = 0, off_tiles = 0, off_ftargets = 0, off_fcontribs = 0, off_btiles = 0,
-         off_sprows = 0, off_blksize = 0, off_odof = 0;
+         off_sprows = 0, off_blksize = 0, off_odof = 0, off_dtiles = 0, off_litems = 0;
+  int64_t nT = 0;             // rows of the solve's level buffer T
   size_t off_spsegs = 0;       // SpSeg table (filled at factor time)
   std::vector<SpSeg> spsegs;   // voff holds the CSC position until factor
   int n_sprows = 0;
@@ -224,6 +230,13 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   for (int i = 0; i < N; ++i) h->odof_blk[i + 1] = h->odof_blk[i] + blk_size[i];
   h->n = h->odof_blk[N];
 
+  const bool verbose = getenv("DD_AUX_VERBOSE") != nullptr;
+  auto tprev = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    auto now = std::chrono::steady_clock::now();
+    if (verbose) fprintf(stderr, "[dd_aux_analyze] %-14s %8.3f s\n", what, std::chrono::duration<double>(now - tprev).count());
+    tprev = now;
+  };
   // ---------------------------------------------------------------- ordering (reading L8)
   std::vector<int> order;
   if (opt.order == DD_ORDER_USER) {
@@ -262,9 +275,11 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
       h->order_used = DD_ORDER_MINDEG;
     }
   }
+  mark("ordering");
   h->S = symbolic_from_order(h->g, order);
   const Symbolic& S = h->S;
 
+  mark("symbolic");
   // ---------------------------------------------------------------- layout
   const int64_t mu = h->cplx ? 4 : 1;
   h->flops_factor = mu * S.flops_factor;
@@ -307,6 +322,12 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
     nd.linv = off;
     off += (int64_t)((nd.s + TB - 1) / TB) * TB * TB;
   }
+  for (int t = 0; t < N; ++t) {  // full inverses L_tt^{-1} (lower, unit diagonal)
+    NodeDev& nd = h->nodes[t];
+    nd.ldi = (int32_t)pad8(nd.s);
+    nd.inv = off;
+    off += (int64_t)nd.ldi * nd.s;
+  }
   h->d_off = off;
   off += pad8(h->n_pad);
   h->e_off = off;
@@ -329,6 +350,7 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   h->nW = (h->nW + 31) & ~int64_t(31);
   h->nK1 = (h->nK1 + 31) & ~int64_t(31);
 
+  mark("layout");
   // ---------------------------------------------------------------- per-level tables
   auto row_in_panel = [&](int j, int i) -> int {  // row offset of block at position i inside panel j
     if (i == j) return 0;
@@ -347,10 +369,11 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   std::vector<RowPerm> rowperm;
   std::vector<UpdTarget> targets;
   std::vector<UpdContrib> contribs;
-  std::vector<Tile> tiles;
+  std::vector<int64_t> tprefix;  // per target: tiles before it within its level
   std::vector<SolveTarget> ftargets;
   std::vector<SolveContrib> fcontribs;
   std::vector<int2> btiles;
+  std::vector<DTile> dtiles, litems;
   {
     const char* ev = getenv("DD_AUX_K3CFG");
     // default tile config per scalar type (measured on B200): real 64x64 at
@@ -400,42 +423,50 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
           tcon[id].push_back(UpdContrib{k, st_row[nk.st0 + a] - nk.sp, st_row[nk.st0 + b], 0});
         }
     }
-    R.t0 = (int)tiles.size();
-    std::vector<std::pair<int64_t, Tile>> ltiles;
+    // K3 targets in launch order: (a) targets in panels of the NEXT level's nodes first (the
+    // lookahead), then (b) the rest; each part sorted by K cost (sum of contributor sizes),
+    // descending.  Tiles are implicit: tprefix[t] = tiles before target t (per level).
+    std::vector<char> next(N, 0);
+    if (l + 1 < S.nlevels)
+      for (int t : S.level_nodes[l + 1]) next[t] = 1;
+    std::vector<std::pair<int64_t, int>> cost_a, cost_b;
     for (size_t id = 0; id < tij.size(); ++id) {
-      int i = tij[id].first, j = tij[id].second;
+      int64_t kcost = 0;
+      for (auto& c : tcon[id]) kcost += h->nodes[c.k].s;
+      (next[tij[id].second] ? cost_a : cost_b).push_back({kcost, (int)id});
+    }
+    auto bycost = [](const std::pair<int64_t, int>& x, const std::pair<int64_t, int>& y) {
+      return x.first != y.first ? x.first > y.first : x.second < y.second;
+    };
+    std::sort(cost_a.begin(), cost_a.end(), bycost);
+    std::sort(cost_b.begin(), cost_b.end(), bycost);
+    R.t0 = (int)targets.size();
+    int64_t tiles_lvl = 0;
+    auto emit = [&](const std::pair<int64_t, int>& cp) {
+      const int id = cp.second;
+      const int i = tij[id].first, j = tij[id].second;
       UpdTarget tg{};
       tg.j = j;
       tg.ro = row_in_panel(j, i);
       tg.M = h->nodes[i].s;
       tg.N = h->nodes[j].s;
       tg.c0 = (int)contribs.size();
-      int64_t kcost = 0;
-      for (auto& c : tcon[id]) {
-        contribs.push_back(c);
-        kcost += h->nodes[c.k].s;
-      }
+      for (auto& c : tcon[id]) contribs.push_back(c);
       tg.c1 = (int)contribs.size();
       tg.diag = (i == j);
-      int tid = (int)targets.size();
+      int64_t nt = 0;
+      const int ntm = (tg.M + BM3 - 1) / BM3, ntn = (tg.N + BN3 - 1) / BN3;
+      for (int tm = 0; tm < ntm; ++tm) nt += tg.diag ? std::min(ntn, (tm * BM3 + BM3 - 1) / BN3 + 1) : ntn;
+      tprefix.push_back(tiles_lvl);
+      tiles_lvl += nt;
       targets.push_back(tg);
-      for (int tm = 0; tm * BM3 < tg.M; ++tm)
-        for (int tn = 0; tn * BN3 < tg.N; ++tn) {
-          if (tg.diag && tn * BN3 > tm * BM3 + BM3 - 1) continue;
-          ltiles.push_back({kcost, Tile{tid, tm, tn, 0}});
-        }
-    }
-    std::stable_sort(ltiles.begin(), ltiles.end(), [](auto& x, auto& y) { return x.first > y.first; });
-    // lookahead split: (a) tiles of targets in panels of the NEXT level's nodes first, (b) the rest
-    std::vector<char> next(N, 0);
-    if (l + 1 < S.nlevels)
-      for (int t : S.level_nodes[l + 1]) next[t] = 1;
-    for (auto& x : ltiles)
-      if (next[targets[x.second.target].j]) tiles.push_back(x.second);
-    R.ta = (int)tiles.size();
-    for (auto& x : ltiles)
-      if (!next[targets[x.second.target].j]) tiles.push_back(x.second);
-    R.t1 = (int)tiles.size();
+    };
+    for (auto& cp : cost_a) emit(cp);
+    R.ta = (int)targets.size();
+    R.tiles_a = tiles_lvl;
+    for (auto& cp : cost_b) emit(cp);
+    R.t1 = (int)targets.size();
+    R.tiles_b = tiles_lvl - R.tiles_a;
     // forward-solve targets: y_i -= L_ik z_k over the level's contributors
     std::unordered_map<int, std::vector<SolveContrib>> fmap;
     std::vector<int> fo;
@@ -461,6 +492,20 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
         for (int tm = 0; tm * SBM < h->nodes[t].s; ++tm) btiles.push_back(make_int2(t, tm));
     R.b1 = (int)btiles.size();
     {
+      R.d0 = (int)dtiles.size();
+      int64_t toff = 0;
+      for (int t : L) {
+        for (int tm = 0; tm * SBM < h->nodes[t].s; ++tm) dtiles.push_back(DTile{t, tm, toff});
+        toff += h->nodes[t].sp;
+      }
+      h->nT = std::max<int64_t>(h->nT, toff);
+      R.d1 = (int)dtiles.size();
+      R.i0 = (int)litems.size();
+      for (int t : L)
+        for (int c = 0; c * TB < h->nodes[t].s; ++c) litems.push_back(DTile{t, c, 0});
+      R.i1 = (int)litems.size();
+    }
+    {
       const double mu = h->cplx ? 4.0 : 1.0;
       R.fl_k1 = R.fl_k2 = R.fl_k3 = R.fl_diag = R.fl_upd = 0;
       R.max_s = 0;
@@ -477,6 +522,7 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
     }
     h->lv.push_back(R);
   }
+  mark("level tables");
   // K6 residual rows: block row I of the full symmetric A
   std::vector<std::vector<SpSeg>> rowsegs(N);
   for (int j = 0; j < N; ++j)
@@ -502,6 +548,7 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   }
   h->n_sprows = (int)sprows.size();
 
+  mark("k6 tables");
   Blob& B = h->blob;
   h->off_nodes = B.put(h->nodes);
   h->off_stpos = B.put(st_pos);
@@ -511,10 +558,12 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   h->off_rowperm = B.put(rowperm);
   h->off_targets = B.put(targets);
   h->off_contribs = B.put(contribs);
-  h->off_tiles = B.put(tiles);
+  h->off_tiles = B.put(tprefix);
   h->off_ftargets = B.put(ftargets);
   h->off_fcontribs = B.put(fcontribs);
   h->off_btiles = B.put(btiles);
+  h->off_dtiles = B.put(dtiles);
+  h->off_litems = B.put(litems);
   h->off_sprows = B.put(sprows);
   h->off_blksize = B.put(h->blk_size);
   std::vector<int64_t> odof(h->odof_blk.begin(), h->odof_blk.end() - 1);
@@ -522,6 +571,7 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   h->off_spsegs = B.put(h->spsegs);
   h->tables_bytes = align256(B.data.size());
 
+  mark("blob");
   // ---------------------------------------------------------------- buffer sizes
   const int planes = h->cplx ? 2 : 1;
   size_t o = h->tables_bytes;
@@ -603,6 +653,7 @@ int dd_aux_solve_work_bytes(dd_aux_handle_t h, int64_t nrhs, size_t* bytes) {
   w += align256((size_t)h->n * (size_t)nrhs * planes * sizeof(double));  // saved B (refinement)
   w += align256((size_t)nrhs * sizeof(double)) + 256;                    // per-column berr + flag
   w += align256(bupd_part_bytes(h->cplx, (int)nrhs));                    // backward split-K partials
+  w += align256((size_t)pad8(std::max<int64_t>(h->nT, 2)) * nrhs * planes * sizeof(double));  // level buffer T
   *bytes = w;
   return DD_OK;
 }
@@ -706,7 +757,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   CUDA_TRY(cudaMemsetAsync(k1.ipiv, 0, (size_t)h->n_pad * 4, st));
   RowpermArgs rp{(const RowPerm*)(F + h->off_rowperm), dnodes, arena, aim, k1.perm};
   K2Args k2{(const Strip*)(F + h->off_strips), dnodes, arena, aim, work, wim, k1.perm, k1.ipiv, h->d_off, h->e_off};
-  K3Args k3{(const Tile*)(F + h->off_tiles), (const UpdTarget*)(F + h->off_targets),
+  K3Args k3{(const UpdTarget*)(F + h->off_targets), (const int64_t*)(F + h->off_tiles), 0, 0,
             (const UpdContrib*)(F + h->off_contribs), dnodes, arena, aim, work, wim};
   const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
   // ---- a2-a5: level-scheduled factorization with a one-level lookahead.
@@ -739,6 +790,17 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
       launch_k1(C, k1, R.n1 - R.n0, R.max_s, sd);
     }
     LAUNCH_CHECK("k1_diag_bk");
+    {
+      LinvArgs li{(const DTile*)(F + h->off_litems) + R.i0, dnodes, arena, aim};
+      double fl = 0;
+      for (int q = R.n0; q < R.n1; ++q) {
+        const double sv = h->nodes[((const int*)(h->blob.data.data() + h->off_lvlnodes))[q]].s;
+        fl += (C ? 4.0 : 1.0) * sv * sv * sv / 3.0;
+      }
+      TraceScope ts(h, DD_PH_LINV, fl, sd);
+      launch_linv(C, li, R.i1 - R.i0, sd);
+    }
+    LAUNCH_CHECK("k_linv");
     RowpermArgs r = rp;
     r.list = rp.list + R.r0;
     if (R.r1 > R.r0) {
@@ -769,10 +831,13 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     CUDA_TRY(cudaStreamWaitEvent(st, h->evB[l], 0));
     K3Args a3 = k3;
     a3.work = work + (l & 1) * wpar;
-    a3.tiles = k3.tiles + R.t0;
-    if (R.ta > R.t0) {
-      TraceScope ts(h, DD_PH_K3, R.t1 > R.ta ? 0.0 : R.fl_k3, st);
-      launch_k3(C, h->k3cfg, a3, R.ta - R.t0, st);
+    a3.targets = k3.targets + R.t0;
+    a3.tprefix = k3.tprefix + R.t0;
+    a3.ntargets = R.ta - R.t0;
+    a3.tile0 = 0;
+    if (R.tiles_a > 0) {
+      TraceScope ts(h, DD_PH_K3, R.tiles_b > 0 ? 0.0 : R.fl_k3, st);
+      launch_k3(C, h->k3cfg, a3, (int)R.tiles_a, st);
     }
     LAUNCH_CHECK("k3_update");
     CUDA_TRY(cudaEventRecord(h->evA[l], st));
@@ -781,11 +846,14 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
       int rc = diag_phase(l + 1);
       if (rc) return rc;
     }
-    a3.tiles = k3.tiles + R.ta;
+    a3.targets = k3.targets + R.ta;
+    a3.tprefix = k3.tprefix + R.ta;
+    a3.ntargets = R.t1 - R.ta;
+    a3.tile0 = R.tiles_a;
     h->cur_level = l;
-    if (R.t1 > R.ta) {
+    if (R.tiles_b > 0) {
       TraceScope ts(h, DD_PH_K3, R.fl_k3, st);
-      launch_k3(C, h->k3cfg, a3, R.t1 - R.ta, st);
+      launch_k3(C, h->k3cfg, a3, (int)R.tiles_b, st);
     }
     LAUNCH_CHECK("k3_update");
   }
@@ -824,7 +892,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
 }
 
 static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t yim, int64_t ldy, int nrhs,
-                       cudaStream_t st, double* part, const int* flag = nullptr) {
+                       cudaStream_t st, double* part, double* T, const int* flag = nullptr) {
   // with a device flag the sweep may be skipped: its flops are not counted (conservative trace)
   const double fs = flag ? 0.0 : 1.0;
   const bool C = h->cplx;
@@ -846,17 +914,22 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
   a.e_off = h->e_off;
   a.nrows = h->n_pad;
   a.flag = flag;
+  a.dtiles = (const DTile*)(F + h->off_dtiles);
+  a.T = T;
+  a.ldT = pad8(std::max<int64_t>(h->nT, 2));
+  a.Tim = C ? a.ldT * nrhs : 0;
   const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
   for (int l = 0; l < (int)h->lv.size(); ++l) {
     const LevelRanges& R = h->lv[l];
     h->cur_level = l;
     SolveArgs b = a;
     b.nodes = lvlnodes + R.n0;
+    b.dtiles = a.dtiles + R.d0;
     {
       TraceScope ts(h, DD_PH_FDIAG, R.fl_diag * nrhs * fs, st);
-      launch_fdiag(C, b, R.n1 - R.n0, st);
+      launch_diag_gemm(C, false, b, R.d1 - R.d0, R.n1 - R.n0, st);
     }
-    LAUNCH_CHECK("k_fdiag");
+    LAUNCH_CHECK("k_diag_g(fwd)");
     b.ftargets = a.ftargets + R.f0;
     if (R.f1 > R.f0) {
       TraceScope ts(h, DD_PH_FUPD, R.fl_upd * nrhs * fs, st);
@@ -881,11 +954,12 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
     }
     LAUNCH_CHECK("k_bupd");
     b.nodes = lvlnodes + R.n0;
+    b.dtiles = a.dtiles + R.d0;
     {
       TraceScope ts(h, DD_PH_BDIAG, R.fl_diag * nrhs * fs, st);
-      launch_bdiag(C, b, R.n1 - R.n0, st);
+      launch_diag_gemm(C, true, b, R.d1 - R.d0, R.n1 - R.n0, st);
     }
-    LAUNCH_CHECK("k_bdiag");
+    LAUNCH_CHECK("k_diag_g(bwd)");
   }
   h->cur_level = -1;
   return DD_OK;
@@ -937,7 +1011,8 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
   double* berr_d = (double*)((uint8_t*)Bsave + align256((size_t)h->n * nrhs * planes * sizeof(double)));
   int* flag_d = (int*)((uint8_t*)berr_d + align256((size_t)nrhs * sizeof(double)));
   double* part = (double*)((uint8_t*)flag_d + 256);
-  int rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part);
+  double* Tbuf = (double*)((uint8_t*)part + align256(bupd_part_bytes(C, (int)nrhs)));
+  int rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf);
   if (rc) return rc;
   pa.dst = (double*)d_B;
   pa.ldd = ldb;
@@ -983,7 +1058,7 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
       LAUNCH_CHECK("k_berr");
       flag = flag_d;
     }
-    rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, flag);
+    rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf, flag);
     if (rc) return rc;
     pa.accumulate = 1;
     pa.flag = flag;

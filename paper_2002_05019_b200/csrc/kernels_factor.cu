@@ -12,6 +12,9 @@
 //   k4_stats    a6  inertia / pivot statistics reduction
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "gemm_core.cuh"
 #include "launch.hpp"
@@ -66,35 +69,135 @@ __device__ __forceinline__ void warp_argmax(double& v, int& i) {
   }
 }
 
-// block-wide (max value, smallest index on ties): IDAMAX semantics (reading L3)
-__device__ __forceinline__ void block_argmax(double& v, int& i, double* shv, int* shi) {
+// block-wide (max value, smallest index on ties): IDAMAX semantics (reading L3).  One barrier:
+// consecutive calls alternate between two slot sets (a slot is rewritten only after every
+// thread has passed the following call's barrier, i.e. finished reading it).
+__device__ __forceinline__ void block_argmax(double& v, int& i, double (*shv)[NT1 / 32], int (*shi)[NT1 / 32],
+                                             int& slot) {
   warp_argmax(v, i);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* sv = shv[slot];
+  int* si = shi[slot];
+  slot ^= 1;
   if (lane == 0) {
-    shv[w] = v;
-    shi[w] = i;
+    sv[w] = v;
+    si[w] = i;
   }
   __syncthreads();
-  v = shv[0];
-  i = shi[0];
+  v = sv[0];
+  i = si[0];
 #pragma unroll
   for (int q = 1; q < NT1 / 32; ++q) {
-    double v2 = shv[q];
-    int i2 = shi[q];
+    double v2 = sv[q];
+    int i2 = si[q];
     if (v2 > v || (v2 == v && i2 < i)) {
       v = v2;
       i = i2;
     }
   }
+}
+
+// Common tail of both K1 variants: TB x TB inverse diagonal tiles of L, the global permutation
+// maps and the per-node statistics (inertia from D for real matrices, a6).
+template <bool C>
+__device__ void k1_finish(const K1Args& a, int t, const NodeDev& nd, double* A, double* smem, const int* perm,
+                          const int* ipiv, const double* dv_, const double* ev_, int n2x2, int nswap, int zero_col) {
+  const int s = nd.s;
+  const int64_t ldA = nd.ld, aim = a.aim;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  auto Ael = [&](int i, int j) { return (int64_t)i + (int64_t)j * ldA; };
+  // ---------------------------------------------------------------- inverse diagonal tiles of L
+  __threadfence_block();
   __syncthreads();
+  {
+    const int ntiles = (s + TB - 1) / TB;
+    const int warp = tid >> 5, lane = tid & 31;
+    double* Lr = smem + warp * (2 * TB * TB);  // per-warp staging (re, im)
+    double* Li = Lr + TB * TB;
+    double* Vb = a.arena + nd.linv;
+    for (int p = warp; p < ntiles; p += nthr / 32) {
+      const int r0 = p * TB, w = min(TB, s - r0);
+      for (int e = lane; e < TB * TB; e += 32) {
+        int i = e % TB, j = e / TB;
+        cz v = (i < w && j < w && i > j) ? ld<C>(A, Ael(r0 + i, r0 + j), aim) : mk(0.0, 0.0);
+        Lr[e] = v.r;
+        Li[e] = v.i;
+      }
+      __syncwarp();
+      // lane j computes column j of L_pp^{-1}: x_i = delta_ij - sum_{m<i} L(i,m) x_m
+      cz x[TB];
+#pragma unroll
+      for (int i = 0; i < TB; ++i) {
+        cz v = mk(i == lane ? 1.0 : 0.0, 0.0);
+#pragma unroll
+        for (int m = 0; m < i; ++m) v = fms<C>(v, mk(Lr[i + m * TB], Li[i + m * TB]), x[m]);
+        x[i] = (i < lane) ? mk(0.0, 0.0) : v;
+      }
+#pragma unroll
+      for (int i = 0; i < TB; ++i) st<C>(Vb, (int64_t)p * TB * TB + i + (int64_t)lane * TB, aim, x[i]);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // ---------------------------------------------------------------- global permutation maps + stats
+  for (int m = tid; m < nd.sp; m += nthr) {
+    if (m < s) {
+      int o = (int)(nd.odof + perm[m]);
+      a.gperm[nd.ydof + m] = o;
+      a.ginv[o] = (int)(nd.ydof + m);
+    } else {
+      a.gperm[nd.ydof + m] = -1;
+    }
+  }
+  if (tid == 0) {
+    int64_t np = 0, nn = 0, nz = 0;
+    if (!C) {
+      int q = 0;
+      while (q < s) {
+        if (ipiv[q] < 0) {
+          double x = dv_[q], y = ev_[q], z = dv_[q + 1];
+          double det = x * z - y * y;
+          if (det < 0) {
+            ++np;
+            ++nn;
+          } else if (det > 0) {
+            if (x + z > 0) np += 2;
+            else nn += 2;
+          } else {
+            ++nz;
+            if (x + z > 0) ++np;
+            else if (x + z < 0) ++nn;
+            else ++nz;
+          }
+          q += 2;
+        } else {
+          double x = dv_[q];
+          if (x > 0) ++np;
+          else if (x < 0) ++nn;
+          else ++nz;
+          ++q;
+        }
+      }
+    }
+    int64_t* S = a.stats + (int64_t)t * 8;
+    S[0] = np;
+    S[1] = nn;
+    S[2] = nz;
+    S[3] = n2x2;
+    S[4] = nswap;
+    S[5] = zero_col >= 0 ? nd.odof + perm[zero_col] + 1 : 0;
+    S[6] = 0;
+    S[7] = 0;
+  }
 }
 
 template <bool C, int K1_MAXQ>
 __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
   using G = typename std::conditional<C, K1GemmC, K1GemmR>::type;
   extern __shared__ __align__(16) double smem[];
-  __shared__ double shv[NT1 / 32];
-  __shared__ int shi[NT1 / 32];
+  __shared__ double shv[2][NT1 / 32];
+  __shared__ int shi[2][NT1 / 32];
+  int aslot = 0;
   __shared__ double wrow_r[K1NB], wrow_i[K1NB];
   __shared__ double wt_r[K1NB][K1NB + 1];
   __shared__ int s_swa[K1NB], s_swb[K1NB], s_nswp;
@@ -176,7 +279,7 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           bi = i;
         }
       }
-      block_argmax(bv, bi, shv, shi);
+      block_argmax(bv, bi, shv, shi, aslot);
       // ---- pivot decision (Bunch-Kaufman, LAPACK xSYTF2 order)
       const double absakk = s_absakk2[k & 1];
       const double colmax = bv > 0.0 ? bv : 0.0;
@@ -224,7 +327,7 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
             }
           }
         }
-        block_argmax(rv, ri, shv, shi);
+        block_argmax(rv, ri, shv, shi, aslot);
         const double rowmax = rv;
         if (absakk >= alpha * colmax * (colmax / rowmax)) {
           kp = k;
@@ -423,88 +526,379 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
     }
   }
 
-  // ---------------------------------------------------------------- inverse diagonal tiles of L
-  __threadfence_block();
+  k1_finish<C>(a, t, nd, A, smem, perm, ipiv, dv_, ev_, n2x2, nswap, zero_col);
+}
+
+// ============================================================================ K1, warp variant
+// For small diagonal blocks (real s <= 256, complex s <= 128) the column loop runs on ONE warp
+// with the panel's L and W entirely in shared memory: argmax by shuffles, __syncwarp only, no
+// block barrier per column.  The four warps of the CTA join at panel ends for the L/W write-back,
+// the deferred interchanges and the DMMA trailing update.  Same decisions as k1_diag_bk.
+constexpr int NT1W = 128;
+using K1WGemmR = Gemm<64, 64, 16, 2, 2, 2, false, false, false>;
+using K1WGemmC = Gemm<64, 64, 16, 2, 2, 2, true, false, false>;
+// rows per lane: real s <= 256 -> 8, complex s <= 128 -> 4
+
+template <bool C>
+__global__ void __launch_bounds__(NT1W) k1_diag_bk_warp(K1Args a) {
+  using G = typename std::conditional<C, K1WGemmC, K1WGemmR>::type;
+  constexpr int K1W_Q = C ? 4 : 8;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int s_swa[K1NB], s_swb[K1NB], s_nswp, s_k;
+  const int t = a.nodes[blockIdx.x];
+  const NodeDev nd = a.nd[t];
+  const int s = nd.s;
+  const int64_t ldA = nd.ld, aim = a.aim;
+  double* A = a.arena + nd.panel;
+  double* Wg = a.work + nd.k1w;  // global W panel for the trailing GEMM, ld = sp
+  const int64_t ldW = nd.sp, wim = a.wim;
+  int* perm = a.perm + nd.ydof;
+  int* ipiv = a.ipiv + nd.ydof;
+  double* dv_ = a.arena + a.d_off + nd.ydof;
+  double* ev_ = a.arena + a.e_off + nd.ydof;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double alpha = (1.0 + sqrt(17.0)) / 8.0;
+  constexpr int NB = K1NB;
+  double* Lr = smem;                               // Lp(i, m) = Lr[m*s + i]
+  double* Li = Lr + (size_t)s * NB;
+  double* Wr = Lr + (size_t)s * NB * (C ? 2 : 1);  // Wp(i, m) = Wr[m*s + i]
+  double* Wi = Wr + (size_t)s * NB;
+  auto P = [&](int i, int m) { return (size_t)m * s + i; };
+  auto Ael = [&](int i, int j) { return (int64_t)i + (int64_t)j * ldA; };
+  auto Lget = [&](int i, int m) { return mk(Lr[P(i, m)], C ? Li[P(i, m)] : 0.0); };
+  auto Wget = [&](int i, int m) { return mk(Wr[P(i, m)], C ? Wi[P(i, m)] : 0.0); };
+  auto Lset = [&](int i, int m, cz v) {
+    Lr[P(i, m)] = v.r;
+    if constexpr (C) Li[P(i, m)] = v.i;
+  };
+  auto Wset = [&](int i, int m, cz v) {
+    Wr[P(i, m)] = v.r;
+    if constexpr (C) Wi[P(i, m)] = v.i;
+  };
+
+  for (int i = tid; i < s; i += NT1W) perm[i] = i;
+  int n2x2 = 0, nswap = 0, zero_col = -1;
   __syncthreads();
-  {
-    const int ntiles = (s + TB - 1) / TB;
-    const int warp = tid >> 5, lane = tid & 31;
-    double* Lr = smem + warp * (2 * TB * TB);  // per-warp staging (re, im)
-    double* Li = Lr + TB * TB;
-    double* Vb = a.arena + nd.linv;
-    for (int p = warp; p < ntiles; p += NT1 / 32) {
-      const int r0 = p * TB, w = min(TB, s - r0);
-      for (int e = lane; e < TB * TB; e += 32) {
-        int i = e % TB, j = e / TB;
-        cz v = (i < w && j < w && i > j) ? ld<C>(A, Ael(r0 + i, r0 + j), aim) : mk(0.0, 0.0);
-        Lr[e] = v.r;
-        Li[e] = v.i;
+  cz Ak[K1W_Q], wv[K1W_Q], wv2[K1W_Q];
+  int k = 0;
+  while (k < s) {
+    const int c0 = k;
+    const bool last_panel = (s - c0) <= NB;
+    if (warp == 0) {
+      int nsw = 0;
+#pragma unroll
+      for (int q = 0; q < K1W_Q; ++q) {
+        const int i = lane + 32 * q;
+        if (i >= k && i < s) Ak[q] = ld<C>(A, Ael(i, k), aim);
       }
-      __syncwarp();
-      // lane j computes column j of L_pp^{-1}: x_i = delta_ij - sum_{m<i} L(i,m) x_m
-      cz x[TB];
+      while (k < s) {
+        const int kk = k - c0;
+        if (!last_panel && kk >= NB - 1) break;
+        double bv = -1.0, akk = 0.0;
+        int bi = INT_MAX;
 #pragma unroll
-      for (int i = 0; i < TB; ++i) {
-        cz v = mk(i == lane ? 1.0 : 0.0, 0.0);
-#pragma unroll
-        for (int m = 0; m < i; ++m) v = fms<C>(v, mk(Lr[i + m * TB], Li[i + m * TB]), x[m]);
-        x[i] = (i < lane) ? mk(0.0, 0.0) : v;
-      }
-#pragma unroll
-      for (int i = 0; i < TB; ++i) st<C>(Vb, (int64_t)p * TB * TB + i + (int64_t)lane * TB, aim, x[i]);
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  // ---------------------------------------------------------------- global permutation maps + stats
-  for (int m = tid; m < nd.sp; m += NT1) {
-    if (m < s) {
-      int o = (int)(nd.odof + perm[m]);
-      a.gperm[nd.ydof + m] = o;
-      a.ginv[o] = (int)(nd.ydof + m);
-    } else {
-      a.gperm[nd.ydof + m] = -1;
-    }
-  }
-  if (tid == 0) {
-    int64_t np = 0, nn = 0, nz = 0;
-    if (!C) {
-      int q = 0;
-      while (q < s) {
-        if (ipiv[q] < 0) {
-          double x = dv_[q], y = ev_[q], z = dv_[q + 1];
-          double det = x * z - y * y;
-          if (det < 0) {
-            ++np;
-            ++nn;
-          } else if (det > 0) {
-            if (x + z > 0) np += 2;
-            else nn += 2;
-          } else {
-            ++nz;
-            if (x + z > 0) ++np;
-            else if (x + z < 0) ++nn;
-            else ++nz;
+        for (int q = 0; q < K1W_Q; ++q) {
+          const int i = lane + 32 * q;
+          if (i < k || i >= s) continue;
+          cz v = Ak[q];
+          for (int m = 0; m < kk; ++m) v = fms<C>(v, Lget(i, m), Wget(k, m));
+          wv[q] = v;
+          Wset(i, kk, v);
+          const double av = cabs1<C>(v);
+          if (i == k) akk = av;
+          else if (av > bv) {
+            bv = av;
+            bi = i;
           }
-          q += 2;
-        } else {
-          double x = dv_[q];
-          if (x > 0) ++np;
-          else if (x < 0) ++nn;
-          else ++nz;
-          ++q;
         }
+        warp_argmax(bv, bi);
+        const double absakk = __shfl_sync(0xffffffffu, akk, k & 31);
+        const double colmax = bv > 0.0 ? bv : 0.0;
+        const int imax = bi;
+        int kp, kstep = 1;
+        bool zero = false;
+        if (fmax(absakk, colmax) == 0.0) {
+          zero = true;
+          kp = k;
+        } else if (absakk >= alpha * colmax) {
+          kp = k;
+        } else {
+          __syncwarp();
+          double rv = -1.0;
+          int ri = INT_MAX;
+          cz ai[K1W_Q];  // column imax of the not-yet-updated trailing block: loads first
+#pragma unroll
+          for (int q = 0; q < K1W_Q; ++q) {
+            const int i = lane + 32 * q;
+            if (i >= k && i < s) ai[q] = (i < imax) ? ld<C>(A, Ael(imax, i), aim) : ld<C>(A, Ael(i, imax), aim);
+          }
+#pragma unroll
+          for (int q = 0; q < K1W_Q; ++q) {
+            const int i = lane + 32 * q;
+            if (i < k || i >= s) continue;
+            cz v = ai[q];
+            for (int m = 0; m < kk; ++m) v = fms<C>(v, Lget(i, m), Wget(imax, m));
+            wv2[q] = v;
+            Wset(i, kk + 1, v);
+            if (i != imax) {
+              const double av = cabs1<C>(v);
+              if (av > rv) {
+                rv = av;
+                ri = i;
+              }
+            }
+          }
+          warp_argmax(rv, ri);
+          __syncwarp();
+          const double rowmax = rv;
+          if (absakk >= alpha * colmax * (colmax / rowmax)) {
+            kp = k;
+          } else {
+            kp = imax;
+            if (cabs1<C>(Wget(imax, kk + 1)) >= alpha * rowmax) {
+#pragma unroll
+              for (int q = 0; q < K1W_Q; ++q) {
+                const int i = lane + 32 * q;
+                if (i < k || i >= s) continue;
+                wv[q] = wv2[q];
+                Wset(i, kk, wv2[q]);
+              }
+            } else {
+              kstep = 2;
+            }
+          }
+        }
+        __syncwarp();
+        const int kkk = k + kstep - 1;
+        if (kp != kkk) {
+          {  // move column kkk of the trailing block to position kp: all loads first, then stores
+            cz t0 = mk(0.0, 0.0), ta[K1W_Q], tb[K1W_Q];
+            if (lane == 0) t0 = ld<C>(A, Ael(kkk, kkk), aim);
+#pragma unroll
+            for (int q = 0; q < K1W_Q; ++q) {
+              const int j1 = kkk + 1 + lane + 32 * q, j2 = kp + 1 + lane + 32 * q;
+              if (j1 < kp) ta[q] = ld<C>(A, Ael(j1, kkk), aim);
+              if (j2 < s) tb[q] = ld<C>(A, Ael(j2, kkk), aim);
+            }
+            if (lane == 0) st<C>(A, Ael(kp, kp), aim, t0);
+#pragma unroll
+            for (int q = 0; q < K1W_Q; ++q) {
+              const int j1 = kkk + 1 + lane + 32 * q, j2 = kp + 1 + lane + 32 * q;
+              if (j1 < kp) st<C>(A, Ael(kp, j1), aim, ta[q]);
+              if (j2 < s) st<C>(A, Ael(j2, kp), aim, tb[q]);
+            }
+          }
+          for (int m = lane; m < kk; m += 32) {
+            const cz x = Lget(kkk, m), y = Lget(kp, m);
+            Lset(kkk, m, y);
+            Lset(kp, m, x);
+          }
+          for (int m = lane; m < kk + kstep; m += 32) {
+            const cz x = Wget(kkk, m), y = Wget(kp, m);
+            Wset(kkk, m, y);
+            Wset(kp, m, x);
+          }
+          if (lane == 0) {
+            const int x = perm[kkk];
+            perm[kkk] = perm[kp];
+            perm[kp] = x;
+            s_swa[nsw] = kkk;
+            s_swb[nsw] = kp;
+          }
+          ++nsw;
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < K1W_Q; ++q) {
+            const int i = lane + 32 * q;
+            if (i == kkk || i == kp) {
+              wv[q] = Wget(i, kk);
+              if (kstep == 2) wv2[q] = Wget(i, kk + 1);
+            }
+          }
+        }
+        if (kstep == 1) {
+          const cz D = Wget(k, kk);
+          const cz rD = zero ? mk(1.0, 0.0) : dv<C>(mk(1.0, 0.0), D);
+#pragma unroll
+          for (int q = 0; q < K1W_Q; ++q) {
+            const int i = lane + 32 * q;
+            if (i <= k || i >= s) continue;
+            Lset(i, kk, mul<C>(wv[q], rD));
+          }
+          if (lane == 0) {
+            st<C>(dv_, k, aim, D);
+            st<C>(ev_, k, aim, mk(0.0, 0.0));
+            ipiv[k] = kp + 1;
+            if (zero && zero_col < 0) zero_col = k;
+            if (kp != k) ++nswap;
+          }
+        } else {
+          const cz w11 = Wget(k, kk), w21 = Wget(k + 1, kk), w22 = Wget(k + 1, kk + 1);
+          const cz d11 = dv<C>(w22, w21), d22 = dv<C>(w11, w21);
+          const cz tt = dv<C>(mk(1.0, 0.0), mul<C>(d11, d22) - mk(1.0, 0.0));
+          const cz d21 = dv<C>(tt, w21);
+#pragma unroll
+          for (int q = 0; q < K1W_Q; ++q) {
+            const int i = lane + 32 * q;
+            if (i <= k || i >= s) continue;
+            cz l0 = mk(0.0, 0.0), l1 = mk(0.0, 0.0);
+            if (i > k + 1) {
+              l0 = mul<C>(d21, mul<C>(d11, wv[q]) - wv2[q]);
+              l1 = mul<C>(d21, mul<C>(d22, wv2[q]) - wv[q]);
+            }
+            Lset(i, kk, l0);
+            Lset(i, kk + 1, l1);
+          }
+          if (lane == 0) {
+            st<C>(dv_, k, aim, w11);
+            st<C>(dv_, k + 1, aim, w22);
+            st<C>(ev_, k, aim, w21);
+            st<C>(ev_, k + 1, aim, mk(0.0, 0.0));
+            ipiv[k] = ipiv[k + 1] = -(kp + 1);
+            ++n2x2;
+            if (kp != k + 1) ++nswap;
+          }
+        }
+        k += kstep;
+        if (k < s && !(kk + kstep >= NB - 1 && !last_panel)) {
+#pragma unroll
+          for (int q = 0; q < K1W_Q; ++q) {
+            const int i = lane + 32 * q;
+            if (i >= k && i < s) Ak[q] = ld<C>(A, Ael(i, k), aim);
+          }
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        s_nswp = nsw;
+        s_k = k;
       }
     }
-    int64_t* S = a.stats + (int64_t)t * 8;
-    S[0] = np;
-    S[1] = nn;
-    S[2] = nz;
-    S[3] = n2x2;
-    S[4] = nswap;
-    S[5] = zero_col >= 0 ? nd.odof + perm[zero_col] + 1 : 0;
-    S[6] = 0;
-    S[7] = 0;
+    __syncthreads();
+    k = s_k;
+    // ------------------------------------------------------------ panel end (all warps)
+    {
+      const int kb = k - c0, nsw = s_nswp;
+      for (int m = 0; m < kb; ++m) {
+        const int col = c0 + m;
+        for (int i = col + 1 + tid; i < s; i += NT1W) st<C>(A, Ael(i, col), aim, Lget(i, m));
+        if (tid == 0) st<C>(A, Ael(col, col), aim, ld<C>(dv_, col, aim));
+      }
+      if (k < s)  // W panel rows >= k for the trailing GEMM
+        for (int m = 0; m < kb; ++m)
+          for (int i = k + tid; i < s; i += NT1W) st<C>(Wg, (int64_t)i + (int64_t)m * ldW, wim, Wget(i, m));
+      for (int j = tid; j < c0; j += NT1W)
+        for (int q = 0; q < nsw; ++q) {
+          const int r0 = s_swa[q], r1 = s_swb[q];
+          const cz x = ld<C>(A, Ael(r0, j), aim), y = ld<C>(A, Ael(r1, j), aim);
+          st<C>(A, Ael(r0, j), aim, y);
+          st<C>(A, Ael(r1, j), aim, x);
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (k < s) {  // trailing update A(k:s, k:s) -= L(k:s, c0:k) W(k:s, 0:kb)^T on DMMA (4 warps)
+      const int kb = k - c0, ke = k & ~1, M = s - ke;
+      Seg sg;
+      sg.a = A + Ael(ke, c0);
+      sg.lda = ldA;
+      sg.b = Wg + ke;
+      sg.ldb = ldW;
+      sg.acol = nullptr;
+      sg.K = kb;
+      const int nt = (M + 63) / 64;
+      for (int tm = 0; tm < nt; ++tm)
+        for (int tn = 0; tn <= tm; ++tn) {
+          typename G::Acc acc;
+          G::zero(acc);
+          G::run([&](int) { return sg; }, 1, tm * 64, tn * 64, M, M, aim, wim, smem, acc,
+                 G::tile_mask(M - tm * 64, M - tn * 64, tn * 64 - tm * 64));
+          double* Cb = A + Ael(ke + tm * 64, ke + tn * 64);
+          G::for_each(acc, [&](int r, int c, double vr, double vi) {
+            const int gr = ke + tm * 64 + r, gc = ke + tn * 64 + c;
+            if (gr < s && gc < s && gr >= k && gc >= k) {
+              int64_t e = (int64_t)r + (int64_t)c * ldA;
+              Cb[e] -= vr;
+              if (C) Cb[e + aim] -= vi;
+            }
+          });
+        }
+      __threadfence();
+      __syncthreads();
+    }
+  }
+  k1_finish<C>(a, t, nd, A, smem, perm, ipiv, dv_, ev_, n2x2, nswap, zero_col);
+}
+
+size_t k1w_smem(bool cplx, int max_s) {
+  size_t lp = (size_t)max_s * K1NB * 8 * (cplx ? 2 : 1) * 2;  // Lp + Wp
+  size_t g = cplx ? K1WGemmC::SMEM_BYTES : K1WGemmR::SMEM_BYTES;
+  size_t inv = (size_t)(NT1W / 32) * 2 * TB * TB * sizeof(double);
+  return std::max(lp, std::max(g, inv));
+}
+
+// ============================================================================ full inverse of L_tt
+// X = L_tt^{-1} (unit lower) by column tiles of width TB, one CTA per (node, column tile c):
+//   X_cc = Linv_cc (the K1 tile inverse);  X_pc = -Linv_pp * sum_{q=c}^{p-1} L_pq X_qc  (p > c)
+// (block forward substitution with identity right-hand side; strictly-upper part zeroed so the
+// solve's diagonal GEMMs may read whole row panels).  Lets every diagonal solve of dd_aux_solve
+// run as one parallel M-tiled DMMA GEMM instead of a sequential panel chain.
+using LinvG_R = Gemm<32, 32, 16, 1, 4, 2, false, false, true>;
+using LinvG_C = Gemm<32, 32, 16, 1, 4, 2, true, false, true>;
+
+template <bool C>
+__global__ void __launch_bounds__(128) k_linv(LinvArgs a) {
+  using G = typename std::conditional<C, LinvG_C, LinvG_R>::type;
+  extern __shared__ __align__(16) double smem[];
+  const DTile it = a.items[blockIdx.x];
+  const NodeDev nd = a.nd[it.t];
+  const int s = nd.s, c = it.tm, c0 = c * TB, wc = min(TB, s - c0);
+  const int64_t ldi = nd.ldi, ldA = nd.ld, aim = a.aim;
+  double* X = a.arena + nd.inv;
+  const double* P = a.arena + nd.panel;
+  const double* Lt = a.arena + nd.linv;
+  // zero rows [0, c0) of the column tile (strictly upper part) and write X_cc
+  for (int e = threadIdx.x; e < c0 * wc; e += blockDim.x) {
+    const int r = e % c0, q = e / c0;
+    st<C>(X, r + (int64_t)(c0 + q) * ldi, aim, mk(0.0, 0.0));
+  }
+  for (int e = threadIdx.x; e < wc * wc; e += blockDim.x) {
+    const int r = e % wc, q = e / wc;
+    st<C>(X, (c0 + r) + (int64_t)(c0 + q) * ldi, aim, ld<C>(Lt, (int64_t)c * TB * TB + r + (int64_t)q * TB, aim));
+  }
+  __threadfence();
+  __syncthreads();
+  const int np = (s + TB - 1) / TB;
+  for (int p = c + 1; p < np; ++p) {
+    const int p0 = p * TB, wp = min(TB, s - p0);
+    typename G::Acc acc;
+    G::zero(acc);
+    {  // acc = L(p0:p0+wp, c0:p0) X(c0:p0, c0:c0+wc)
+      Seg sg{P + p0 + (int64_t)c0 * ldA, X + c0 + (int64_t)c0 * ldi, nullptr, ldA, ldi, p0 - c0};
+      G::run([&](int) { return sg; }, 1, 0, 0, wp, wc, aim, aim, smem, acc);
+    }
+    double* Xp = X + p0 + (int64_t)c0 * ldi;
+    G::for_each(acc, [&](int r, int q, double vr, double vi) {
+      if (r < wp && q < wc) {
+        Xp[r + (int64_t)q * ldi] = vr;
+        if (C) Xp[r + (int64_t)q * ldi + aim] = vi;
+      }
+    });
+    __threadfence();
+    __syncthreads();
+    G::zero(acc);
+    {  // X_pc = -Linv_pp acc
+      Seg sg{Lt + (int64_t)p * TB * TB, Xp, nullptr, (int64_t)TB, ldi, wp};
+      G::run([&](int) { return sg; }, 1, 0, 0, wp, wc, aim, aim, smem, acc);
+    }
+    G::for_each(acc, [&](int r, int q, double vr, double vi) {
+      if (r < wp && q < wc) {
+        Xp[r + (int64_t)q * ldi] = -vr;
+        if (C) Xp[r + (int64_t)q * ldi + aim] = -vi;
+      }
+    });
+    __threadfence();
+    __syncthreads();
   }
 }
 
@@ -698,8 +1092,33 @@ __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_upd
   using G = typename Cf::G;
   constexpr int BM = Cf::BM, BN = Cf::BN;
   extern __shared__ __align__(16) double smem[];
-  const Tile T = a.tiles[blockIdx.x];
-  const UpdTarget tg = a.targets[T.target];
+  // implicit tiles: find this CTA's target (last t with tprefix[t] <= gid) and its (tm, tn)
+  const int64_t gid = a.tile0 + blockIdx.x;
+  int lo = 0, hi = a.ntargets - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.tprefix[mid] <= gid) lo = mid;
+    else hi = mid - 1;
+  }
+  const UpdTarget tg = a.targets[lo];
+  Tile T;
+  {
+    int local = (int)(gid - a.tprefix[lo]);
+    const int ntn = (tg.N + BN - 1) / BN;
+    T.tm = 0;
+    if (!tg.diag) {
+      T.tm = local / ntn;
+      T.tn = local % ntn;
+    } else {
+      for (;;) {
+        const int rowt = min(ntn, (T.tm * BM + BM - 1) / BN + 1);
+        if (local < rowt) break;
+        local -= rowt;
+        ++T.tm;
+      }
+      T.tn = local;
+    }
+  }
   const NodeDev nj = a.nd[tg.j];
   typename G::Acc acc;
   G::zero(acc);
@@ -788,12 +1207,37 @@ static void launch_k1_t(const K1Args& a, int nnodes, cudaStream_t st) {
 }
 
 void launch_k1(bool cplx, const K1Args& a, int nnodes, int max_s, cudaStream_t st) {
+  // warp variant: opt-in (DD_AUX_K1WARP=1); measured slower than the 256-thread kernel on cfg1
+  // (59 vs 42 ms), kept for the next round's latency work
+  static const bool warp = getenv("DD_AUX_K1WARP") && atoi(getenv("DD_AUX_K1WARP"));
+  if (warp && max_s <= (cplx ? 128 : 256)) {
+    const size_t sm = k1w_smem(cplx, max_s);
+    if (cplx) {
+      set_smem(k1_diag_bk_warp<true>, sm);
+      k1_diag_bk_warp<true><<<nnodes, NT1W, sm, st>>>(a);
+    } else {
+      set_smem(k1_diag_bk_warp<false>, sm);
+      k1_diag_bk_warp<false><<<nnodes, NT1W, sm, st>>>(a);
+    }
+    return;
+  }
   if (max_s <= NT1 * 4) {
     if (cplx) launch_k1_t<true, 4>(a, nnodes, st);
     else launch_k1_t<false, 4>(a, nnodes, st);
   } else {
     if (cplx) launch_k1_t<true, 16>(a, nnodes, st);
     else launch_k1_t<false, 16>(a, nnodes, st);
+  }
+}
+
+void launch_linv(bool cplx, const LinvArgs& a, int nitems, cudaStream_t st) {
+  if (nitems == 0) return;
+  if (cplx) {
+    set_smem(k_linv<true>, LinvG_C::SMEM_BYTES);
+    k_linv<true><<<nitems, 128, LinvG_C::SMEM_BYTES, st>>>(a);
+  } else {
+    set_smem(k_linv<false>, LinvG_R::SMEM_BYTES);
+    k_linv<false><<<nitems, 128, LinvG_R::SMEM_BYTES, st>>>(a);
   }
 }
 

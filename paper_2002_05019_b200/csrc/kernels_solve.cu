@@ -185,6 +185,56 @@ __global__ void __launch_bounds__(128) k_bdiag(SolveArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------- diagonal solves (GEMM)
+// z_t = L_tt^{-1} y_t (forward) or z_t = L_tt^{-T} y_t (backward) with the precomputed full
+// inverse (k_linv): CTA (node, 64-row tile) x (64-rhs tile), K restricted to the triangle;
+// results go to the level buffer T, then k_dcopy moves them back into y (no in-place hazard).
+template <bool C, bool BWD>
+__global__ void __launch_bounds__(128) k_diag_g(SolveArgs a) {
+  if (a.flag && *a.flag == 0) return;
+  using G = typename std::conditional<BWD, typename std::conditional<C, BUpdC, BUpdR>::type,
+                                      typename std::conditional<C, FUpdC, FUpdR>::type>::type;
+  extern __shared__ __align__(16) double smem[];
+  const DTile D = a.dtiles[blockIdx.x];
+  const NodeDev nd = a.nd[D.t];
+  const int s = nd.s, m0 = D.tm * SUBM, n0 = blockIdx.y * SBN;
+  const double* X = a.arena + nd.inv;
+  Seg sg;
+  if (!BWD) {  // A(m, k) = X(m0 + m, k), k < min(s, m0 + SUBM)   (MK)
+    sg = Seg{X + m0, a.y + nd.ydof, nullptr, (int64_t)nd.ldi, a.ldy, min(s, m0 + SUBM)};
+  } else {     // A(m, k') = X(m0 + k', m0 + m), k' < s - m0          (KM)
+    sg = Seg{X + m0 + (int64_t)m0 * nd.ldi, a.y + nd.ydof + m0, nullptr, (int64_t)nd.ldi, a.ldy, s - m0};
+  }
+  typename G::Acc acc;
+  G::zero(acc);
+  G::run([&](int) { return sg; }, 1, 0, n0, s - m0, a.nrhs, a.aim, a.yim, smem, acc,
+         G::tile_mask(s - m0, a.nrhs - n0, G::NO_DIAG));
+  double* T = a.T + D.toff + m0;
+  G::for_each(acc, [&](int r, int c, double vr, double vi) {
+    if (m0 + r < s && n0 + c < a.nrhs) {
+      const int64_t e = (int64_t)r + (int64_t)(n0 + c) * a.ldT;
+      T[e] = vr;
+      if (C) T[e + a.Tim] = vi;
+    }
+  });
+}
+
+template <bool C>
+__global__ void k_dcopy(SolveArgs a, int ntiles) {
+  if (a.flag && *a.flag == 0) return;
+  const int c = blockIdx.y;
+  for (int q = blockIdx.x; q < ntiles; q += gridDim.x) {
+    const DTile D = a.dtiles[q];
+    const NodeDev nd = a.nd[D.t];
+    const int m0 = D.tm * SUBM, m1 = min(nd.s, m0 + SUBM);
+    for (int r = m0 + threadIdx.x; r < m1; r += blockDim.x) {
+      const int64_t src = D.toff + r + (int64_t)c * a.ldT, dst = nd.ydof + r + (int64_t)c * a.ldy;
+      a.y[dst] = a.T[src];
+      if (C) a.y[dst + a.yim] = a.T[src + a.Tim];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------- level updates
 template <bool C>
 __global__ void __launch_bounds__(128) k_fupd(SolveArgs a) {
@@ -662,6 +712,31 @@ void launch_copy(bool cplx, const double* src, int64_t lds, double* dst, int64_t
   } while (0)
 
 static int ntn(int nrhs) { return (nrhs + SBN - 1) / SBN; }
+
+void launch_diag_gemm(bool cplx, bool backward, const SolveArgs& a, int ntiles, int, cudaStream_t st) {
+  if (ntiles == 0 || a.nrhs == 0) return;
+  dim3 grid(ntiles, ntn(a.nrhs));
+  if (!backward) {
+    if (cplx) {
+      set_smem(k_diag_g<true, false>, FUpdC::SMEM_BYTES);
+      k_diag_g<true, false><<<grid, 128, FUpdC::SMEM_BYTES, st>>>(a);
+    } else {
+      set_smem(k_diag_g<false, false>, FUpdR::SMEM_BYTES);
+      k_diag_g<false, false><<<grid, 128, FUpdR::SMEM_BYTES, st>>>(a);
+    }
+  } else {
+    if (cplx) {
+      set_smem(k_diag_g<true, true>, BUpdC::SMEM_BYTES);
+      k_diag_g<true, true><<<grid, 128, BUpdC::SMEM_BYTES, st>>>(a);
+    } else {
+      set_smem(k_diag_g<false, true>, BUpdR::SMEM_BYTES);
+      k_diag_g<false, true><<<grid, 128, BUpdR::SMEM_BYTES, st>>>(a);
+    }
+  }
+  dim3 g2(std::min(ntiles, 256), a.nrhs);
+  if (cplx) k_dcopy<true><<<g2, 64, 0, st>>>(a, ntiles);
+  else k_dcopy<false><<<g2, 64, 0, st>>>(a, ntiles);
+}
 
 void launch_fdiag(bool cplx, const SolveArgs& a, int nnodes, cudaStream_t st) {
   if (nnodes == 0 || a.nrhs == 0) return;

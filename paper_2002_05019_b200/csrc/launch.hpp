@@ -53,14 +53,23 @@ struct K2Args {
 };
 
 struct K3Args {
-  const Tile* tiles;
-  const UpdTarget* targets;
+  const UpdTarget* targets;   // this launch's targets (cost-sorted)
+  const int64_t* tprefix;     // tprefix[t] = level-relative index of target t's first tile
+  int ntargets;
+  int64_t tile0;              // level-relative index of this launch's first tile
   const UpdContrib* contribs;
   const NodeDev* nd;
   double* arena;
   int64_t aim;
   const double* work;
   int64_t wim;
+};
+
+struct LinvArgs {      // full inverse of each unit-lower L_tt from its TB x TB tile inverses
+  const DTile* items;  // (node, column tile of width TB)
+  const NodeDev* nd;
+  double* arena;
+  int64_t aim;
 };
 
 struct SolveArgs {
@@ -80,6 +89,9 @@ struct SolveArgs {
   int64_t d_off, e_off;
   int64_t nrows;                // padded n
   const int* flag;              // refinement sweep: run only if *flag != 0 (nullptr = always)
+  const DTile* dtiles;          // diagonal-solve tiles of the level (node, 64-row tile, T offset)
+  double* T;                    // level buffer for the diagonal solves (planar), ld ldT
+  int64_t Tim, ldT;
 };
 
 struct PermArgs {
@@ -130,7 +142,9 @@ void launch_perm_in(bool cplx, const PermArgs& a, cudaStream_t st);
 void launch_perm_out(bool cplx, const PermArgs& a, cudaStream_t st);
 void launch_copy(bool cplx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t n, int nrhs,
                  cudaStream_t st);
+void launch_linv(bool cplx, const LinvArgs& a, int nitems, cudaStream_t st);
 void launch_fdiag(bool cplx, const SolveArgs& a, int nnodes, cudaStream_t st);
+void launch_diag_gemm(bool cplx, bool backward, const SolveArgs& a, int ntiles, int nnodes, cudaStream_t st);
 void launch_fupd(bool cplx, const SolveArgs& a, int ntiles, cudaStream_t st);
 void launch_dsolve(bool cplx, const SolveArgs& a, cudaStream_t st);
 void launch_bupd(bool cplx, const SolveArgs& a, int ntiles, double* part, cudaStream_t st);

@@ -28,6 +28,13 @@ struct NodeDev {     // one per elimination position t (64-byte aligned record)
   int32_t rp, ld;    // padded struct rows; panel leading dimension
   int32_t ldw, nst;  // W leading dimension; |struct(t)|
   int32_t st0, blk;  // first index into the struct arrays; original block id
+  int64_t inv;       // element offset of the full inverse L_tt^{-1} (s x s, lower, ld = ldi)
+  int32_t ldi, pad;
+};
+
+struct DTile {       // diagonal-solve / inverse work item: node t, tile index, level buffer offset
+  int32_t t, tm;
+  int64_t toff;      // row offset of node t in the level buffer T
 };
 
 struct UpdTarget {   // Schur-update target block (i, j), i at/after j, stored in panel j

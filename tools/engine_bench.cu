@@ -95,5 +95,9 @@ int main() {
   run<Gemm<64, 64, 16, 2, 2, 3, false, true, true>, false, 64, 64, true, true>("real 64x64 KMxKN (bupd)", 8192, 8192, 512);
   run<Gemm<64, 64, 32, 2, 2, 3, true, true, true>, true, 64, 64, true, true>("cplx 64x64 KMxKN BK32", 8192, 4096, 512);
   run<Gemm<64, 32, 16, 2, 2, 2, true, false, false>, true, 64, 32>("cplx 64x32 2st", 8192, 4096, 512);
+  // short K per tile (the K3 regime: one contributor of ~512-600 columns)
+  run<Gemm<64, 64, 16, 2, 2, 3, false, false, false>, false, 64, 64>("real 64x64 K=512", 8192, 512, 512);
+  run<Gemm<64, 64, 16, 2, 2, 3, false, false, false>, false, 64, 64>("real 64x64 K=1024", 8192, 1024, 512);
+  run<Gemm<64, 32, 16, 2, 2, 2, true, false, false>, true, 64, 32>("cplx 64x32 K=512", 8192, 512, 512);
   return 0;
 }
