@@ -272,6 +272,29 @@ def build_problem(nx, ny, nz, sizes_fn, *, complex_=False, seed=0, topology="fac
             S = S + sigma * torch.eye(m, dtype=tdt, device=device)
             S = 0.5 * (S + S.transpose(0, 1))
         offs = np.concatenate([[0], np.cumsum([blk_size[I] for I in members])])
+        if backend == "torch":
+            # one scatter per clique: destination offset of every (row, col) of S whose block
+            # (I, J) has I >= J (a clique never repeats an interface, so indices are unique)
+            import torch
+            rows, cols = [], []
+            for a, I in enumerate(members):
+                for b, J in enumerate(members):
+                    if I < J:
+                        continue
+                    si, sj = int(blk_size[I]), int(blk_size[J])
+                    base = int(val_offset[pos[(I, J)]])
+                    r = np.arange(si)
+                    c = np.arange(sj)
+                    rows.append((offs[a] + r[:, None] + 0 * c[None, :]).ravel())
+                    cols.append((offs[b] + c[None, :] + 0 * r[:, None]).ravel())
+                    rows[-1] = np.stack([rows[-1], (base + r[:, None] + c[None, :] * si).ravel()])
+            src_r = np.concatenate([x[0] for x in rows])
+            dst = np.concatenate([x[1] for x in rows])
+            src_c = np.concatenate(cols)
+            sr = torch.from_numpy(src_r).to(S.device)
+            sc = torch.from_numpy(src_c).to(S.device)
+            values.index_add_(0, torch.from_numpy(dst).to(S.device), S[sr, sc])
+            continue
         for a, I in enumerate(members):
             for b, J in enumerate(members):
                 if I < J:
@@ -279,11 +302,8 @@ def build_problem(nx, ny, nz, sizes_fn, *, complex_=False, seed=0, topology="fac
                 blk = S[offs[a]:offs[a + 1], offs[b]:offs[b + 1]]
                 pp = pos[(I, J)]
                 si, sj = int(blk_size[I]), int(blk_size[J])
-                if backend == "torch":
-                    values[val_offset[pp]:val_offset[pp] + si * sj].view(sj, si).add_(blk.transpose(0, 1))
-                else:
-                    dst = values[val_offset[pp]:val_offset[pp] + si * sj].reshape(sj, si).T
-                    dst += blk
+                dst = values[val_offset[pp]:val_offset[pp] + si * sj].reshape(sj, si).T
+                dst += blk
     prob = Problem(blk_size, colptr, rowidx, values, val_offset, cliques, name)
     prob.pairs = pairs
     prob.grid = (nx, ny, nz)

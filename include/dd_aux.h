@@ -66,7 +66,9 @@ typedef struct {
   int32_t use_graphs;         /* reserved (CUDA-graph capture of the level loop), default 0 */
   double refine_tol;          /* a refinement step is skipped (on the device, no host sync) when
                                  every column already has berr <= refine_tol; 0 = always refine */
-  int32_t reserved[2];
+  int32_t complex_3m;         /* complex Schur update with 3 real products (Gauss/3M) instead of
+                                 4 (default 0); flop counts stay in the standard 8-flop convention */
+  int32_t reserved;
 } dd_aux_options;
 
 typedef struct {

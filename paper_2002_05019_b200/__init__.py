@@ -46,7 +46,7 @@ class DDAuxError(RuntimeError):
 class dd_aux_options(ctypes.Structure):
     _fields_ = [("order", ctypes.c_int32), ("user_order", ctypes.POINTER(ctypes.c_int32)),
                 ("refine_steps", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("refine_tol", ctypes.c_double),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("complex_3m", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class dd_aux_info(ctypes.Structure):
@@ -137,10 +137,12 @@ def dd_aux_version() -> str:
     return _lib.dd_aux_version().decode()
 
 
-def dd_aux_default_options(order=DD_ORDER_AUTO, refine_steps=1, user_order=None, refine_tol=None) -> dd_aux_options:
+def dd_aux_default_options(order=DD_ORDER_AUTO, refine_steps=1, user_order=None, refine_tol=None,
+                           complex_3m=False) -> dd_aux_options:
     o = dd_aux_options()
     _lib.dd_aux_default_options(ctypes.byref(o))
     o.order = int(order)
+    o.complex_3m = int(bool(complex_3m))
     o.refine_steps = int(refine_steps)
     if refine_tol is not None:
         o.refine_tol = float(refine_tol)
@@ -265,11 +267,11 @@ class AuxSolver:
     """
 
     def __init__(self, blk_size, colptr, rowidx, complex_=False, order=DD_ORDER_AUTO, refine_steps=1,
-                 user_order=None, device="cuda", refine_tol=None):
+                 user_order=None, device="cuda", refine_tol=None, complex_3m=False):
         import torch
         self.torch = torch
         self.cplx = bool(complex_)
-        self.opt = dd_aux_default_options(order, refine_steps, user_order, refine_tol)
+        self.opt = dd_aux_default_options(order, refine_steps, user_order, refine_tol, complex_3m)
         self.h = dd_aux_analyze(blk_size, colptr, rowidx, DD_COMPLEX128 if self.cplx else DD_REAL64, self.opt)
         self.info = dd_aux_get_info(self.h)
         self.device = device

@@ -378,7 +378,7 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
     const char* ev = getenv("DD_AUX_K3CFG");
     // default tile config per scalar type (measured on B200): real 64x64 at
     // 4 CTAs/SM (least ragged-tile padding), complex 64x32 4M, 2 stages, 4 CTAs/SM
-    h->k3cfg = ev ? atoi(ev) : (h->cplx ? 5 : 4);
+    h->k3cfg = ev ? atoi(ev) : (h->cplx ? (opt.complex_3m ? 6 : 5) : 4);
     const char* la = getenv("DD_AUX_LOOKAHEAD");
     h->lookahead = la ? atoi(la) != 0 : true;
   }

@@ -54,7 +54,12 @@ __device__ __forceinline__ double dneg(double x) {  // sign flip on the integer 
   return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ull);
 }
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool CPLX, bool A_KM, bool B_KN>
+// C3M (complex only): 3M / Gauss formulation -- T1 = Ar Br, T2 = Ai Bi, T3 = (Ar+Ai)(Br+Bi),
+// Cr = T1 - T2, Ci = T3 - T1 - T2: three real DMMA products instead of four.
+// FINE: per-16x8-sub-tile DMMA masking (one predicate per mma) vs coarse per-warp masking (a warp
+// whose whole warp tile is outside the valid region skips the stage; otherwise branch-free).
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool CPLX, bool A_KM, bool B_KN,
+          bool C3M = false, bool FINE = true>
 struct Gemm {
   static constexpr int NTHR = WARPS_M * WARPS_N * 32;
   static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
@@ -69,9 +74,11 @@ struct Gemm {
   static_assert(WTM % 16 == 0 && WTN % 8 == 0 && BK % 4 == 0, "tile shape");
   static_assert((A_LD % 16) == 4 && (B_LD % 16) == 4, "bank-conflict-free padding");
 
+  static_assert(!C3M || CPLX, "3M needs complex operands");
   struct Acc {
-    double r[MI][NI][4];
-    double i[CPLX ? MI : 1][CPLX ? NI : 1][4];
+    double r[MI][NI][4];                       // real part (4M) / T1 (3M)
+    double i[CPLX ? MI : 1][CPLX ? NI : 1][4];  // imaginary part (4M) / T2 (3M)
+    double t[C3M ? MI : 1][C3M ? NI : 1][4];    // T3 (3M)
   };
 
   __device__ static void zero(Acc& acc) {
@@ -83,6 +90,7 @@ struct Gemm {
         for (int v = 0; v < 4; ++v) {
           acc.r[a][b][v] = 0.0;
           if constexpr (CPLX) acc.i[a][b][v] = 0.0;
+          if constexpr (C3M) acc.t[a][b][v] = 0.0;
         }
   }
 
@@ -100,7 +108,12 @@ struct Gemm {
         for (int v = 0; v < 4; ++v) {
           int row = wm * WTM + a * 16 + g + ((v >> 1) << 3);
           int col = wn * WTN + b * 8 + 2 * tg + (v & 1);
-          f(row, col, acc.r[a][b][v], CPLX ? acc.i[CPLX ? a : 0][CPLX ? b : 0][v] : 0.0);
+          if constexpr (C3M) {
+            const double t1 = acc.r[a][b][v], t2 = acc.i[a][b][v], t3 = acc.t[a][b][v];
+            f(row, col, t1 - t2, t3 - t1 - t2);
+          } else {
+            f(row, col, acc.r[a][b][v], CPLX ? acc.i[CPLX ? a : 0][CPLX ? b : 0][v] : 0.0);
+          }
         }
   }
 
@@ -182,6 +195,10 @@ struct Gemm {
   }
 
   __device__ static void compute_stage(const double* st, Acc& acc, unsigned mask = ~0u) {
+    if constexpr (!FINE) {
+      if (mask == 0u) return;  // warp-uniform
+      mask = ~0u;              // constant from here on: the per-mma predicates fold away
+    }
     const double* As = st;
     const double* Bs = st + NPL * A_TILE;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -213,6 +230,32 @@ struct Gemm {
       }
       // Issue order: every product class over all (a, b) before the next class, so two
       // DMMAs into the same accumulator are MI*NI instructions apart (no dependency stall).
+      if constexpr (C3M) {
+        double sa[MI][2], sb[NI];
+#pragma unroll
+        for (int a = 0; a < MI; ++a) {
+          sa[a][0] = ar[a][0] + ai[a][0];
+          sa[a][1] = ar[a][1] + ai[a][1];
+        }
+#pragma unroll
+        for (int b = 0; b < NI; ++b) sb[b] = br[b] + bi[b];
+#pragma unroll
+        for (int a = 0; a < MI; ++a)
+#pragma unroll
+          for (int b = 0; b < NI; ++b)
+            if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.r[a][b], ar[a][0], ar[a][1], br[b]);
+#pragma unroll
+        for (int a = 0; a < MI; ++a)
+#pragma unroll
+          for (int b = 0; b < NI; ++b)
+            if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.i[a][b], ai[a][0], ai[a][1], bi[b]);
+#pragma unroll
+        for (int a = 0; a < MI; ++a)
+#pragma unroll
+          for (int b = 0; b < NI; ++b)
+            if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.t[a][b], sa[a][0], sa[a][1], sb[b]);
+        continue;
+      }
 #pragma unroll
       for (int a = 0; a < MI; ++a)
 #pragma unroll

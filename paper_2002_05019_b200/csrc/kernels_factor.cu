@@ -1086,6 +1086,38 @@ struct K3Cfg<true, 5> {  // complex 64x32, 2 stages, 4 CTAs per SM (dense microb
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
 
+template <>
+struct K3Cfg<false, 6> {
+  using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
+};
+template <>
+struct K3Cfg<true, 6> {  // complex 64x32 3M (Gauss): 3 real DMMA products per complex product
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
+};
+
+template <>
+struct K3Cfg<false, 7> {  // real 64x64, coarse (per-warp) masking
+  using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
+};
+template <>
+struct K3Cfg<true, 7> {  // complex 64x32 4M, coarse masking
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
+};
+template <>
+struct K3Cfg<false, 8> {
+  using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
+};
+template <>
+struct K3Cfg<true, 8> {  // complex 64x32 3M, coarse masking
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, false>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
+};
+
 template <bool C, int CFG>
 __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_update(K3Args a) {
   using Cf = K3Cfg<C, CFG>;
@@ -1277,6 +1309,9 @@ int k3_bm(bool cplx, int cfg) {
     case 3: return bm_of<3>(cplx);
     case 4: return bm_of<4>(cplx);
     case 5: return bm_of<5>(cplx);
+    case 6: return bm_of<6>(cplx);
+    case 7: return bm_of<7>(cplx);
+    case 8: return bm_of<8>(cplx);
     default: return bm_of<1>(cplx);
   }
 }
@@ -1287,6 +1322,9 @@ int k3_bn(bool cplx, int cfg) {
     case 3: return bn_of<3>(cplx);
     case 4: return bn_of<4>(cplx);
     case 5: return bn_of<5>(cplx);
+    case 6: return bn_of<6>(cplx);
+    case 7: return bn_of<7>(cplx);
+    case 8: return bn_of<8>(cplx);
     default: return bn_of<1>(cplx);
   }
 }
@@ -1312,6 +1350,9 @@ void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st)
     case 3: launch_k3_c<3>(cplx, a, ntiles, st); break;
     case 4: launch_k3_c<4>(cplx, a, ntiles, st); break;
     case 5: launch_k3_c<5>(cplx, a, ntiles, st); break;
+    case 6: launch_k3_c<6>(cplx, a, ntiles, st); break;
+    case 7: launch_k3_c<7>(cplx, a, ntiles, st); break;
+    case 8: launch_k3_c<8>(cplx, a, ntiles, st); break;
     default: launch_k3_c<1>(cplx, a, ntiles, st); break;
   }
 }

@@ -210,3 +210,23 @@ def test_adaptive_refinement_policy():
     np.testing.assert_array_equal(out["skip"], out["plain"])     # converged -> no correction applied
     np.testing.assert_array_equal(out["tight"], out["always"])   # not converged -> same as always
     assert residual_berr(p, out["always"], B).max() <= TOL_BERR
+
+
+def test_complex_3m_parity():
+    """Complex Schur update with the 3M (Gauss) product: same tolerances as 4M."""
+    import torch
+    import paper_2002_05019_b200 as dd
+    from tests._gpu import to_dev_colmajor
+    p = dd_inputs.config("cfg3", grid=(3, 2, 2), sizes=100)
+    B = random_rhs(p.n, 5, True, 2)
+    s = dd.AuxSolver(p.blk_size, p.colptr, p.rowidx, complex_=True, complex_3m=True)
+    s.factor(torch.from_numpy(p.values).cuda(), p.val_offset)
+    b = to_dev_colmajor(B, torch)
+    s.solve_(b)
+    torch.cuda.synchronize()
+    X = b.cpu().numpy()
+    F = oracle.block_factor(p, list(s.order()))
+    s.close()
+    Xo, _, _ = oracle.refine_solve(p, F, B, 1)
+    assert residual_berr(p, X, B).max() <= TOL_BERR
+    assert rel_diff(X, Xo) <= TOL_REL
