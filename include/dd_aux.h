@@ -66,8 +66,8 @@ typedef struct {
   int32_t use_graphs;         /* reserved (CUDA-graph capture of the level loop), default 0 */
   double refine_tol;          /* a refinement step is skipped (on the device, no host sync) when
                                  every column already has berr <= refine_tol; 0 = always refine */
-  int32_t complex_3m;         /* complex Schur update with 3 real products (Gauss/3M) instead of
-                                 4 (default 0); flop counts stay in the standard 8-flop convention */
+  int32_t complex_3m;         /* complex Schur update with 3 real products (Gauss/3M, default 1) or
+                                 4 (0); flop counts stay in the standard 8-flop convention */
   int32_t reserved;
 } dd_aux_options;
 
@@ -89,7 +89,7 @@ typedef struct {
   float ms_load, ms_factor;     /* device time of the load and factor phases (CUDA events)     */
 } dd_aux_factor_info;
 
-/* Default options: AUTO order, 1 refinement step. */
+/* Default options: AUTO order, 1 refinement step, 3M complex products. */
 void dd_aux_default_options(dd_aux_options* opt);
 
 /* Host-only symbolic phase ("very fast symbolic factorization step").

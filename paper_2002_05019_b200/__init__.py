@@ -138,7 +138,7 @@ def dd_aux_version() -> str:
 
 
 def dd_aux_default_options(order=DD_ORDER_AUTO, refine_steps=1, user_order=None, refine_tol=None,
-                           complex_3m=False) -> dd_aux_options:
+                           complex_3m=True) -> dd_aux_options:
     o = dd_aux_options()
     _lib.dd_aux_default_options(ctypes.byref(o))
     o.order = int(order)
@@ -267,7 +267,7 @@ class AuxSolver:
     """
 
     def __init__(self, blk_size, colptr, rowidx, complex_=False, order=DD_ORDER_AUTO, refine_steps=1,
-                 user_order=None, device="cuda", refine_tol=None, complex_3m=False):
+                 user_order=None, device="cuda", refine_tol=None, complex_3m=True):
         import torch
         self.torch = torch
         self.cplx = bool(complex_)

@@ -188,6 +188,7 @@ void dd_aux_default_options(dd_aux_options* opt) {
   std::memset(opt, 0, sizeof(*opt));
   opt->order = DD_ORDER_AUTO;
   opt->refine_steps = 1;
+  opt->complex_3m = 1;
 }
 
 const char* dd_aux_last_error(void) { return g_err.c_str(); }
@@ -377,8 +378,9 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   {
     const char* ev = getenv("DD_AUX_K3CFG");
     // default tile config per scalar type (measured on B200): real 64x64 at
-    // 4 CTAs/SM (least ragged-tile padding), complex 64x32 4M, 2 stages, 4 CTAs/SM
-    h->k3cfg = ev ? atoi(ev) : (h->cplx ? (opt.complex_3m ? 6 : 5) : 4);
+    // 4 CTAs/SM with per-warp masking; complex 64x32, 2 stages, 4 CTAs/SM: 3M (Gauss) by default,
+    // 4M with per-warp masking when complex_3m = 0
+    h->k3cfg = ev ? atoi(ev) : (h->cplx ? (opt.complex_3m ? 6 : 7) : 7);
     const char* la = getenv("DD_AUX_LOOKAHEAD");
     h->lookahead = la ? atoi(la) != 0 : true;
   }

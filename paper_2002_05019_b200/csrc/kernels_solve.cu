@@ -30,11 +30,12 @@ using BDiagR = Gemm<TB, SBN, 16, 1, 4, 3, false, true, true>;
 using BDiagC = Gemm<TB, SBN, 16, 1, 4, 3, true, true, true>;
 constexpr int SUBM = 64;
 constexpr int BUPD_MAX_PARTS = 320;  // split-K partial tiles of the backward update (workspace bound)
-using FUpdR = Gemm<SUBM, SBN, 16, 2, 2, 3, false, false, true>;
-using FUpdC = Gemm<SUBM, SBN, 16, 2, 2, 3, true, false, true>;
-using BUpdR = Gemm<SUBM, SBN, 16, 2, 2, 3, false, true, true>;
+// per-warp (coarse) DMMA masking throughout: per-mma predicates cost WARPSYNCs
+using FUpdR = Gemm<SUBM, SBN, 16, 2, 2, 3, false, false, true, false, false>;
+using FUpdC = Gemm<SUBM, SBN, 16, 2, 2, 3, true, false, true, false, false>;
+using BUpdR = Gemm<SUBM, SBN, 16, 2, 2, 3, false, true, true, false, false>;
 // complex KM x KN: 2 stages so two CTAs fit per SM (3 stages: 120 KB -> 1 CTA, 26 vs 33 TF dense)
-using BUpdC = Gemm<SUBM, SBN, 16, 2, 2, 2, true, true, true>;
+using BUpdC = Gemm<SUBM, SBN, 16, 2, 2, 2, true, true, true>;  // complex: fine masking measured faster
 
 // ---------------------------------------------------------------------------- permutations
 template <bool C>
