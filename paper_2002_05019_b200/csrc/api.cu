@@ -118,6 +118,7 @@ struct dd_aux_handle_s {
   // lookahead: high-priority side stream + per-level events
   cudaStream_t side = nullptr;
   bool norm_valid = false;  // ||A||_inf of the current factorization's d_vals computed on device
+  bool m3 = false;         // complex products in the 3M form (options.complex_3m)
   int k3cfg = 1;           // K3 tile configuration (env DD_AUX_K3CFG, read at analyze)
   bool lookahead = true;   // env DD_AUX_LOOKAHEAD=0 disables the side-stream overlap
   std::vector<cudaEvent_t> evA, evB;
@@ -381,6 +382,7 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
     // 4 CTAs/SM with per-warp masking; complex 64x32, 2 stages, 4 CTAs/SM: 3M (Gauss) by default,
     // 4M with per-warp masking when complex_3m = 0
     h->k3cfg = ev ? atoi(ev) : (h->cplx ? (opt.complex_3m ? 6 : 7) : 7);
+    h->m3 = h->cplx && opt.complex_3m;
     const char* la = getenv("DD_AUX_LOOKAHEAD");
     h->lookahead = la ? atoi(la) != 0 : true;
   }
@@ -929,13 +931,13 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
     b.dtiles = a.dtiles + R.d0;
     {
       TraceScope ts(h, DD_PH_FDIAG, R.fl_diag * nrhs * fs, st);
-      launch_diag_gemm(C, false, b, R.d1 - R.d0, R.n1 - R.n0, st);
+      launch_diag_gemm(C, h->m3, false, b, R.d1 - R.d0, st);
     }
     LAUNCH_CHECK("k_diag_g(fwd)");
     b.ftargets = a.ftargets + R.f0;
     if (R.f1 > R.f0) {
       TraceScope ts(h, DD_PH_FUPD, R.fl_upd * nrhs * fs, st);
-      launch_fupd(C, b, R.f1 - R.f0, st);
+      launch_fupd(C, h->m3, b, R.f1 - R.f0, st);
     }
     LAUNCH_CHECK("k_fupd");
   }
@@ -952,14 +954,14 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
     b.btiles = a.btiles + R.b0;
     if (R.b1 > R.b0) {
       TraceScope ts(h, DD_PH_BUPD, R.fl_upd * nrhs * fs, st);
-      launch_bupd(C, b, R.b1 - R.b0, part, st);
+      launch_bupd(C, h->m3, b, R.b1 - R.b0, part, st);
     }
     LAUNCH_CHECK("k_bupd");
     b.nodes = lvlnodes + R.n0;
     b.dtiles = a.dtiles + R.d0;
     {
       TraceScope ts(h, DD_PH_BDIAG, R.fl_diag * nrhs * fs, st);
-      launch_diag_gemm(C, true, b, R.d1 - R.d0, R.n1 - R.n0, st);
+      launch_diag_gemm(C, h->m3, true, b, R.d1 - R.d0, st);
     }
     LAUNCH_CHECK("k_diag_g(bwd)");
   }

@@ -23,19 +23,20 @@ using namespace ddaux;
 
 namespace ddk {
 
-constexpr int SBN = 64;  // rhs tile for every solve GEMM
-using FDiagR = Gemm<TB, SBN, 16, 1, 4, 3, false, false, true>;
-using FDiagC = Gemm<TB, SBN, 16, 1, 4, 3, true, false, true>;
-using BDiagR = Gemm<TB, SBN, 16, 1, 4, 3, false, true, true>;
-using BDiagC = Gemm<TB, SBN, 16, 1, 4, 3, true, true, true>;
+// Solve GEMM configurations: 64-row tiles; rhs tile 64 (real) / 32 (complex, so the 3M form's
+// three accumulator sets fit at 4 CTAs per SM).  Real: per-warp masking; complex: per-sub-tile.
 constexpr int SUBM = 64;
 constexpr int BUPD_MAX_PARTS = 320;  // split-K partial tiles of the backward update (workspace bound)
-// per-warp (coarse) DMMA masking throughout: per-mma predicates cost WARPSYNCs
-using FUpdR = Gemm<SUBM, SBN, 16, 2, 2, 3, false, false, true, false, false>;
-using FUpdC = Gemm<SUBM, SBN, 16, 2, 2, 3, true, false, true, false, false>;
-using BUpdR = Gemm<SUBM, SBN, 16, 2, 2, 3, false, true, true, false, false>;
-// complex KM x KN: 2 stages so two CTAs fit per SM (3 stages: 120 KB -> 1 CTA, 26 vs 33 TF dense)
-using BUpdC = Gemm<SUBM, SBN, 16, 2, 2, 2, true, true, true>;  // complex: fine masking measured faster
+template <bool C>
+struct SolveN {
+  static constexpr int value = C ? 32 : 64;
+};
+template <bool C, bool M3>
+struct SolveG {
+  static constexpr int BN = SolveN<C>::value;
+  using FU = Gemm<SUBM, BN, 16, 2, 2, C ? 2 : 3, C, false, true, C && M3, C>;  // MK x KN (FINE = C)
+  using BU = Gemm<SUBM, BN, 16, 2, 2, C ? 2 : 3, C, true, true, C && M3, C>;   // KM x KN
+};
 
 // ---------------------------------------------------------------------------- permutations
 template <bool C>
@@ -91,110 +92,15 @@ __global__ void k_copy(const double* __restrict__ src, int64_t lds, double* __re
     dst[r + (int64_t)c * ldd * w] = src[r + (int64_t)c * lds * w];
 }
 
-// ---------------------------------------------------------------------------- diagonal solves
-template <bool C>
-__global__ void __launch_bounds__(128) k_fdiag(SolveArgs a) {
-  if (a.flag && *a.flag == 0) return;
-  using G = typename std::conditional<C, FDiagC, FDiagR>::type;
-  extern __shared__ __align__(16) double smem[];
-  const int t = a.nodes[blockIdx.x];
-  const NodeDev nd = a.nd[t];
-  const int s = nd.s, n0 = blockIdx.y * SBN;
-  const double* P = a.arena + nd.panel;
-  const double* Linv = a.arena + nd.linv;
-  double* y = a.y + nd.ydof;  // y(k, n) = y[k + n*ldy]
-  const int64_t ldy = a.ldy, yim = a.yim;
-  const int np = (s + TB - 1) / TB;
-  for (int p = 0; p < np; ++p) {
-    const int c0 = p * TB, w = min(TB, s - c0);
-    typename G::Acc acc;
-    G::zero(acc);
-    if (c0 > 0) {  // acc = L(c0:c0+w, 0:c0) z(0:c0)
-      Seg sg{P + c0, y, nullptr, (int64_t)nd.ld, ldy, c0};
-      G::run([&](int) { return sg; }, 1, 0, n0, w, a.nrhs, a.aim, yim, smem, acc);
-    }
-    G::for_each(acc, [&](int r, int c, double vr, double vi) {
-      if (r < w && n0 + c < a.nrhs) {
-        int64_t e = (int64_t)(c0 + r) + (int64_t)(n0 + c) * ldy;
-        y[e] -= vr;
-        if (C) y[e + yim] -= vi;
-      }
-    });
-    __threadfence();
-    __syncthreads();
-    G::zero(acc);
-    {
-      Seg sg{Linv + (int64_t)p * TB * TB, y + c0, nullptr, (int64_t)TB, ldy, w};
-      G::run([&](int) { return sg; }, 1, 0, n0, w, a.nrhs, a.aim, yim, smem, acc);
-    }
-    G::for_each(acc, [&](int r, int c, double vr, double vi) {
-      if (r < w && n0 + c < a.nrhs) {
-        int64_t e = (int64_t)(c0 + r) + (int64_t)(n0 + c) * ldy;
-        y[e] = vr;
-        if (C) y[e + yim] = vi;
-      }
-    });
-    __threadfence();
-    __syncthreads();
-  }
-}
-
-template <bool C>
-__global__ void __launch_bounds__(128) k_bdiag(SolveArgs a) {
-  if (a.flag && *a.flag == 0) return;
-  using G = typename std::conditional<C, BDiagC, BDiagR>::type;
-  extern __shared__ __align__(16) double smem[];
-  const int t = a.nodes[blockIdx.x];
-  const NodeDev nd = a.nd[t];
-  const int s = nd.s, n0 = blockIdx.y * SBN;
-  const double* P = a.arena + nd.panel;
-  const double* Linv = a.arena + nd.linv;
-  double* y = a.y + nd.ydof;
-  const int64_t ldy = a.ldy, yim = a.yim, ldA = nd.ld;
-  const int np = (s + TB - 1) / TB;
-  for (int p = np - 1; p >= 0; --p) {
-    const int c0 = p * TB, w = min(TB, s - c0), c1 = c0 + w;
-    typename G::Acc acc;
-    G::zero(acc);
-    if (c1 < s) {  // acc = L(c1:s, c0:c1)^T z(c1:s)
-      Seg sg{P + c1 + (int64_t)c0 * ldA, y + c1, nullptr, ldA, ldy, s - c1};
-      G::run([&](int) { return sg; }, 1, 0, n0, w, a.nrhs, a.aim, yim, smem, acc);
-    }
-    G::for_each(acc, [&](int r, int c, double vr, double vi) {
-      if (r < w && n0 + c < a.nrhs) {
-        int64_t e = (int64_t)(c0 + r) + (int64_t)(n0 + c) * ldy;
-        y[e] -= vr;
-        if (C) y[e + yim] -= vi;
-      }
-    });
-    __threadfence();
-    __syncthreads();
-    G::zero(acc);
-    {
-      Seg sg{Linv + (int64_t)p * TB * TB, y + c0, nullptr, (int64_t)TB, ldy, w};
-      G::run([&](int) { return sg; }, 1, 0, n0, w, a.nrhs, a.aim, yim, smem, acc);
-    }
-    G::for_each(acc, [&](int r, int c, double vr, double vi) {
-      if (r < w && n0 + c < a.nrhs) {
-        int64_t e = (int64_t)(c0 + r) + (int64_t)(n0 + c) * ldy;
-        y[e] = vr;
-        if (C) y[e + yim] = vi;
-      }
-    });
-    __threadfence();
-    __syncthreads();
-  }
-}
-
 // ---------------------------------------------------------------------------- diagonal solves (GEMM)
 // z_t = L_tt^{-1} y_t (forward) or z_t = L_tt^{-T} y_t (backward) with the precomputed full
 // inverse (k_linv): CTA (node, 64-row tile) x (64-rhs tile), K restricted to the triangle;
 // results go to the level buffer T, then k_dcopy moves them back into y (no in-place hazard).
-template <bool C, bool BWD>
+template <bool C, bool BWD, bool M3>
 __global__ void __launch_bounds__(128) k_diag_g(SolveArgs a) {
   if (a.flag && *a.flag == 0) return;
-  using G = typename std::conditional<BWD, typename std::conditional<C, BUpdC, BUpdR>::type,
-                                      typename std::conditional<C, FUpdC, FUpdR>::type>::type;
+  using G = typename std::conditional<BWD, typename SolveG<C, M3>::BU, typename SolveG<C, M3>::FU>::type;
+  constexpr int SBN = SolveN<C>::value;
   extern __shared__ __align__(16) double smem[];
   const DTile D = a.dtiles[blockIdx.x];
   const NodeDev nd = a.nd[D.t];
@@ -237,10 +143,11 @@ __global__ void k_dcopy(SolveArgs a, int ntiles) {
 }
 
 // ---------------------------------------------------------------------------- level updates
-template <bool C>
+template <bool C, bool M3>
 __global__ void __launch_bounds__(128) k_fupd(SolveArgs a) {
   if (a.flag && *a.flag == 0) return;
-  using G = typename std::conditional<C, FUpdC, FUpdR>::type;
+  using G = typename SolveG<C, M3>::FU;
+  constexpr int SBN = SolveN<C>::value;
   extern __shared__ __align__(16) double smem[];
   const SolveTarget T = a.ftargets[blockIdx.x];
   const NodeDev ni = a.nd[T.i];
@@ -269,10 +176,11 @@ __global__ void __launch_bounds__(128) k_fupd(SolveArgs a) {
 // Backward pull update y_t -= sum_{i in struct(t)} L_it^T y_i.  With split-K (G > 1) CTA
 // (tile, g) sums the g-th contiguous chunk of struct(t) into a partial buffer and
 // k_bupd_reduce subtracts the G partials in fixed order g = 0..G-1 (deterministic).
-template <bool C>
+template <bool C, bool M3>
 __global__ void __launch_bounds__(128) k_bupd(SolveArgs a, int G, double* part, int64_t pim) {
   if (a.flag && *a.flag == 0) return;
-  using G_ = typename std::conditional<C, BUpdC, BUpdR>::type;
+  using G_ = typename SolveG<C, M3>::BU;
+  constexpr int SBN = SolveN<C>::value;
   extern __shared__ __align__(16) double smem[];
   const int tile = blockIdx.x / G, g = blockIdx.x % G;
   const int2 T = a.btiles[tile];  // (t, tm)
@@ -676,7 +584,6 @@ static void set_smem(K kern, size_t bytes) {
 
 int solve_bm(bool) { return SUBM; }
 size_t bupd_part_bytes(bool cplx, int nrhs) { return (size_t)BUPD_MAX_PARTS * SUBM * nrhs * (cplx ? 2 : 1) * 8; }
-int solve_bn(bool) { return SBN; }
 int spmv_bm() { return SPM; }
 
 static dim3 rows_grid(int64_t nrows, int nrhs) {
@@ -701,86 +608,72 @@ void launch_copy(bool cplx, const double* src, int64_t lds, double* dst, int64_t
   k_copy<<<rows_grid(n * w, nrhs), 256, 0, st>>>(src, lds, dst, ldd, n, w);
 }
 
-#define DD_LAUNCH_GEMM_KERNEL(KER, GR, GC, GRID, THREADS)                   \
-  do {                                                                      \
-    if (cplx) {                                                             \
-      set_smem(KER<true>, GC::SMEM_BYTES);                                  \
-      KER<true><<<GRID, THREADS, GC::SMEM_BYTES, st>>>(a);                  \
-    } else {                                                                \
-      set_smem(KER<false>, GR::SMEM_BYTES);                                 \
-      KER<false><<<GRID, THREADS, GR::SMEM_BYTES, st>>>(a);                 \
-    }                                                                       \
-  } while (0)
+static int ntn(bool cplx, int nrhs) {
+  const int bn = cplx ? SolveN<true>::value : SolveN<false>::value;
+  return (nrhs + bn - 1) / bn;
+}
 
-static int ntn(int nrhs) { return (nrhs + SBN - 1) / SBN; }
+template <class K>
+static void launch_g(K kern, size_t smem, dim3 grid, cudaStream_t st, const SolveArgs& a) {
+  set_smem(kern, smem);
+  kern<<<grid, 128, smem, st>>>(a);
+}
 
-void launch_diag_gemm(bool cplx, bool backward, const SolveArgs& a, int ntiles, int, cudaStream_t st) {
-  if (ntiles == 0 || a.nrhs == 0) return;
-  dim3 grid(ntiles, ntn(a.nrhs));
-  if (!backward) {
-    if (cplx) {
-      set_smem(k_diag_g<true, false>, FUpdC::SMEM_BYTES);
-      k_diag_g<true, false><<<grid, 128, FUpdC::SMEM_BYTES, st>>>(a);
-    } else {
-      set_smem(k_diag_g<false, false>, FUpdR::SMEM_BYTES);
-      k_diag_g<false, false><<<grid, 128, FUpdR::SMEM_BYTES, st>>>(a);
-    }
-  } else {
-    if (cplx) {
-      set_smem(k_diag_g<true, true>, BUpdC::SMEM_BYTES);
-      k_diag_g<true, true><<<grid, 128, BUpdC::SMEM_BYTES, st>>>(a);
-    } else {
-      set_smem(k_diag_g<false, true>, BUpdR::SMEM_BYTES);
-      k_diag_g<false, true><<<grid, 128, BUpdR::SMEM_BYTES, st>>>(a);
-    }
-  }
+template <bool C, bool M3>
+static void diag_t(bool backward, const SolveArgs& a, int ntiles, cudaStream_t st) {
+  dim3 grid(ntiles, ntn(C, a.nrhs));
+  if (!backward) launch_g(k_diag_g<C, false, M3>, SolveG<C, M3>::FU::SMEM_BYTES, grid, st, a);
+  else launch_g(k_diag_g<C, true, M3>, SolveG<C, M3>::BU::SMEM_BYTES, grid, st, a);
   dim3 g2(std::min(ntiles, 256), a.nrhs);
-  if (cplx) k_dcopy<true><<<g2, 64, 0, st>>>(a, ntiles);
-  else k_dcopy<false><<<g2, 64, 0, st>>>(a, ntiles);
+  k_dcopy<C><<<g2, 64, 0, st>>>(a, ntiles);
 }
 
-void launch_fdiag(bool cplx, const SolveArgs& a, int nnodes, cudaStream_t st) {
-  if (nnodes == 0 || a.nrhs == 0) return;
-  dim3 grid(nnodes, ntn(a.nrhs));
-  DD_LAUNCH_GEMM_KERNEL(k_fdiag, FDiagR, FDiagC, grid, 128);
-}
-void launch_bdiag(bool cplx, const SolveArgs& a, int nnodes, cudaStream_t st) {
-  if (nnodes == 0 || a.nrhs == 0) return;
-  dim3 grid(nnodes, ntn(a.nrhs));
-  DD_LAUNCH_GEMM_KERNEL(k_bdiag, BDiagR, BDiagC, grid, 128);
-}
-void launch_fupd(bool cplx, const SolveArgs& a, int ntiles, cudaStream_t st) {
+void launch_diag_gemm(bool cplx, bool m3, bool backward, const SolveArgs& a, int ntiles, cudaStream_t st) {
   if (ntiles == 0 || a.nrhs == 0) return;
-  dim3 grid(ntiles, ntn(a.nrhs));
-  DD_LAUNCH_GEMM_KERNEL(k_fupd, FUpdR, FUpdC, grid, 128);
+  if (!cplx) diag_t<false, false>(backward, a, ntiles, st);
+  else if (m3) diag_t<true, true>(backward, a, ntiles, st);
+  else diag_t<true, false>(backward, a, ntiles, st);
 }
-int bupd_split(int ntiles, int nrhs) {
+
+void launch_fupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, cudaStream_t st) {
+  if (ntiles == 0 || a.nrhs == 0) return;
+  dim3 grid(ntiles, ntn(cplx, a.nrhs));
+  if (!cplx) launch_g(k_fupd<false, false>, SolveG<false, false>::FU::SMEM_BYTES, grid, st, a);
+  else if (m3) launch_g(k_fupd<true, true>, SolveG<true, true>::FU::SMEM_BYTES, grid, st, a);
+  else launch_g(k_fupd<true, false>, SolveG<true, false>::FU::SMEM_BYTES, grid, st, a);
+}
+
+int bupd_split(bool cplx, int ntiles, int nrhs) {
   // enough CTAs for two per SM; partial buffer bounded by BUPD_MAX_PARTS tiles
-  const int ctas = ntiles * ntn(nrhs);
+  const int ctas = ntiles * ntn(cplx, nrhs);
   if (ctas >= 2 * 148) return 1;
   int G = (2 * 148 + ctas - 1) / ctas;
   G = std::min(G, std::max(1, BUPD_MAX_PARTS / std::max(ntiles, 1)));
   return std::max(1, std::min(G, 16));
 }
 
-void launch_bupd(bool cplx, const SolveArgs& a, int ntiles, double* part, cudaStream_t st) {
+template <bool C, bool M3>
+static void bupd_t(const SolveArgs& a, int ntiles, int G, double* part, int64_t pim, cudaStream_t st) {
+  using GB = typename SolveG<C, M3>::BU;
+  dim3 grid(ntiles * G, ntn(C, a.nrhs));
+  set_smem(k_bupd<C, M3>, GB::SMEM_BYTES);
+  k_bupd<C, M3><<<grid, 128, GB::SMEM_BYTES, st>>>(a, G, part, pim);
+}
+
+void launch_bupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, double* part, cudaStream_t st) {
   if (ntiles == 0 || a.nrhs == 0) return;
-  const int G = part ? bupd_split(ntiles, a.nrhs) : 1;
+  const int G = part ? bupd_split(cplx, ntiles, a.nrhs) : 1;
   const int64_t pim = (int64_t)BUPD_MAX_PARTS * SUBM * a.nrhs;
-  dim3 grid(ntiles * G, ntn(a.nrhs));
-  if (cplx) {
-    set_smem(k_bupd<true>, BUpdC::SMEM_BYTES);
-    k_bupd<true><<<grid, 128, BUpdC::SMEM_BYTES, st>>>(a, G, part, pim);
-  } else {
-    set_smem(k_bupd<false>, BUpdR::SMEM_BYTES);
-    k_bupd<false><<<grid, 128, BUpdR::SMEM_BYTES, st>>>(a, G, part, pim);
-  }
+  if (!cplx) bupd_t<false, false>(a, ntiles, G, part, pim, st);
+  else if (m3) bupd_t<true, true>(a, ntiles, G, part, pim, st);
+  else bupd_t<true, false>(a, ntiles, G, part, pim, st);
   if (G > 1) {
     dim3 g2(ntiles, std::min(64, (SUBM * a.nrhs + 255) / 256));
     if (cplx) k_bupd_reduce<true><<<g2, 256, 0, st>>>(a, G, part, pim);
     else k_bupd_reduce<false><<<g2, 256, 0, st>>>(a, G, part, pim);
   }
 }
+
 void launch_dsolve(bool cplx, const SolveArgs& a, cudaStream_t st) {
   if (a.nrhs == 0) return;
   if (cplx) k_dsolve<true><<<rows_grid(a.nrows, a.nrhs), 256, 0, st>>>(a);

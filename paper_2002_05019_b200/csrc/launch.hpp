@@ -137,19 +137,17 @@ void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st)
 void launch_k4(const int64_t* node_stats, int nnodes, int64_t* out, cudaStream_t st);
 
 int solve_bm(bool cplx);   // row tile of the forward/backward update kernels
-int solve_bn(bool cplx);   // rhs tile
 void launch_perm_in(bool cplx, const PermArgs& a, cudaStream_t st);
 void launch_perm_out(bool cplx, const PermArgs& a, cudaStream_t st);
 void launch_copy(bool cplx, const double* src, int64_t lds, double* dst, int64_t ldd, int64_t n, int nrhs,
                  cudaStream_t st);
 void launch_linv(bool cplx, const LinvArgs& a, int nitems, cudaStream_t st);
-void launch_fdiag(bool cplx, const SolveArgs& a, int nnodes, cudaStream_t st);
-void launch_diag_gemm(bool cplx, bool backward, const SolveArgs& a, int ntiles, int nnodes, cudaStream_t st);
-void launch_fupd(bool cplx, const SolveArgs& a, int ntiles, cudaStream_t st);
+// m3: complex products in the 3M (Gauss) form
+void launch_diag_gemm(bool cplx, bool m3, bool backward, const SolveArgs& a, int ntiles, cudaStream_t st);
+void launch_fupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, cudaStream_t st);
 void launch_dsolve(bool cplx, const SolveArgs& a, cudaStream_t st);
-void launch_bupd(bool cplx, const SolveArgs& a, int ntiles, double* part, cudaStream_t st);
+void launch_bupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, double* part, cudaStream_t st);
 size_t bupd_part_bytes(bool cplx, int nrhs);
-void launch_bdiag(bool cplx, const SolveArgs& a, int nnodes, cudaStream_t st);
 int spmv_bm();
 // ||A||_inf of the caller's original blocks (max row sum of moduli) -> *out (bits of a double)
 void launch_norm_a(bool cplx, const SpmvArgs& a, int nrow_tiles, unsigned long long* out, cudaStream_t st);
