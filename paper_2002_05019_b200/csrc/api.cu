@@ -62,7 +62,8 @@ struct Blob {  // host image of the device table region
 
 struct LevelRanges {
   int n0, n1;     // level nodes
-  int s0, s1;     // K2 strips
+  int s0, s1;     // K2 strips (L = W D^{-1})
+  int k0, k1;     // K2 GEMM tiles
   int r0, r1;     // rowperm entries
   int t0, t1;     // K3 targets: [t0, ta) update the next level's panels, [ta, t1) the rest
   int ta;
@@ -98,7 +99,7 @@ struct dd_aux_handle_s {
   Blob blob;
   size_t off_nodes = 0, off_stpos = 0, off_strow = 0, off_lvlnodes = 0, off_strips = 0, off_rowperm = 0,
          off_targets = 0, off_contribs = 0, off_tiles = 0, off_ftargets = 0, off_fcontribs = 0, off_btiles = 0,
-         off_sprows = 0, off_blksize = 0, off_odof = 0, off_dtiles = 0, off_litems = 0;
+         off_sprows = 0, off_blksize = 0, off_odof = 0, off_dtiles = 0, off_litems = 0, off_k2items = 0;
   int64_t nT = 0;             // rows of the solve's level buffer T
   size_t off_spsegs = 0;       // SpSeg table (filled at factor time)
   std::vector<SpSeg> spsegs;   // voff holds the CSC position until factor
@@ -368,6 +369,7 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
 
   std::vector<int32_t> lvl_nodes;
   std::vector<Strip> strips;
+  std::vector<Tile> k2items;
   std::vector<RowPerm> rowperm;
   std::vector<UpdTarget> targets;
   std::vector<UpdContrib> contribs;
@@ -400,6 +402,13 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
       for (int r0 = 0; r0 < nd.rp; r0 += K2BM) strips.push_back(Strip{t, r0, std::min(K2BM, nd.rp - r0), 0});
     }
     R.s1 = (int)strips.size();
+    R.k0 = (int)k2items.size();
+    for (int t : L) {
+      const NodeDev& nd = h->nodes[t];
+      for (int tm = 0; tm * BM3 < nd.rp; ++tm)
+        for (int tn = 0; tn * BN3 < nd.s; ++tn) k2items.push_back(Tile{t, tm, tn, 0});
+    }
+    R.k1 = (int)k2items.size();
     R.r0 = (int)rowperm.size();
     for (int t : L)
       for (auto& kr : appears[t]) rowperm.push_back(RowPerm{t, kr.first, kr.second, 0});
@@ -559,6 +568,7 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   h->off_strow = B.put(st_row);
   h->off_lvlnodes = B.put(lvl_nodes);
   h->off_strips = B.put(strips);
+  h->off_k2items = B.put(k2items);
   h->off_rowperm = B.put(rowperm);
   h->off_targets = B.put(targets);
   h->off_contribs = B.put(contribs);
@@ -760,7 +770,8 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   k1.stats = (int64_t*)(F + h->off_stats);
   CUDA_TRY(cudaMemsetAsync(k1.ipiv, 0, (size_t)h->n_pad * 4, st));
   RowpermArgs rp{(const RowPerm*)(F + h->off_rowperm), dnodes, arena, aim, k1.perm};
-  K2Args k2{(const Strip*)(F + h->off_strips), dnodes, arena, aim, work, wim, k1.perm, k1.ipiv, h->d_off, h->e_off};
+  K2Args k2{(const Tile*)(F + h->off_k2items), (const Strip*)(F + h->off_strips), dnodes, arena, aim, work, wim,
+            k1.perm, k1.ipiv, h->d_off, h->e_off};
   K3Args k3{(const UpdTarget*)(F + h->off_targets), (const int64_t*)(F + h->off_tiles), 0, 0,
             (const UpdContrib*)(F + h->off_contribs), dnodes, arena, aim, work, wim};
   const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
@@ -814,10 +825,11 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     LAUNCH_CHECK("k_rowperm");
     K2Args a2 = k2;
     a2.strips = k2.strips + R.s0;
+    a2.items = k2.items + R.k0;
     a2.work = work + (l & 1) * wpar;
     if (R.s1 > R.s0) {
       TraceScope ts(h, DD_PH_K2, R.fl_k2, sd);
-      launch_k2(C, a2, R.s1 - R.s0, sd);
+      launch_k2(C, h->k3cfg, a2, R.k1 - R.k0, R.s1 - R.s0, sd);
     }
     LAUNCH_CHECK("k2_panel");
     CUDA_TRY(cudaEventRecord(h->evB[l], sd));

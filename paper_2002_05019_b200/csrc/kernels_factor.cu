@@ -930,91 +930,6 @@ __global__ void k_rowperm(RowpermArgs a) {
   }
 }
 
-// ============================================================================ K2 panel TRSM
-constexpr int NT2 = 128;
-using K2GemmR = Gemm<64, TB, 16, 2, 2, 3, false, false, false>;
-using K2GemmC = Gemm<64, TB, 16, 2, 2, 3, true, false, false>;
-
-template <bool C>
-__global__ void __launch_bounds__(NT2) k2_panel(K2Args a) {
-  using G = typename std::conditional<C, K2GemmC, K2GemmR>::type;
-  extern __shared__ __align__(16) double smem[];
-  const Strip S = a.strips[blockIdx.x];
-  const NodeDev nd = a.nd[S.t];
-  const int s = nd.s;
-  const int64_t ldA = nd.ld, ldW = nd.ldw;
-  double* P = a.arena + nd.panel;                 // panel t
-  double* Ahat = P + nd.sp + S.row0;             // strip rows of A_struct,t (before permutation)
-  double* W = a.work + nd.w + S.row0;            // strip rows of W_t
-  const int* perm = a.perm + nd.ydof;
-  const double* Linv = a.arena + nd.linv;
-  const int64_t aim = a.aim, wim = a.wim;
-  const int M = S.nrows;
-  const int np = (s + TB - 1) / TB;
-  for (int p = 0; p < np; ++p) {
-    const int c0 = p * TB, w = min(TB, s - c0);
-    typename G::Acc acc;
-    G::zero(acc);
-    if (c0 > 0) {  // acc = W(:, 0:c0) L(c0:c0+w, 0:c0)^T
-      Seg sg{W, P + c0, nullptr, ldW, ldA, c0};
-      G::run([&](int) { return sg; }, 1, 0, 0, M, w, wim, aim, smem, acc);
-    }
-    // T = Ahat(:, perm[c0:c0+w]) - acc  -> W(:, c0:c0+w)
-    G::for_each(acc, [&](int r, int c, double vr, double vi) {
-      if (r < M && c < w) {
-        int64_t src = (int64_t)r + (int64_t)perm[c0 + c] * ldA;
-        int64_t dst = (int64_t)r + (int64_t)(c0 + c) * ldW;
-        W[dst] = Ahat[src] - vr;
-        if (C) W[dst + wim] = Ahat[src + aim] - vi;
-      }
-    });
-    __threadfence();
-    __syncthreads();
-    // W(:, c0:c0+w) = T Linv_pp^T
-    G::zero(acc);
-    {
-      Seg sg{W + (int64_t)c0 * ldW, Linv + (int64_t)p * TB * TB, nullptr, ldW, TB, w};
-      G::run([&](int) { return sg; }, 1, 0, 0, M, w, wim, aim, smem, acc);
-    }
-    G::for_each(acc, [&](int r, int c, double vr, double vi) {
-      if (r < M && c < w) {
-        int64_t dst = (int64_t)r + (int64_t)(c0 + c) * ldW;
-        W[dst] = vr;
-        if (C) W[dst + wim] = vi;
-      }
-    });
-    __threadfence();
-    __syncthreads();
-  }
-  // L = W D^{-1} (1x1 / 2x2 closed form) -> panel rows (overwrites A_struct,t)
-  const double* dv_ = a.arena + a.d_off + nd.ydof;
-  const double* ev_ = a.arena + a.e_off + nd.ydof;
-  const int* ipiv = a.ipiv + nd.ydof;
-  for (int c = 0; c < s; ++c) {
-    const bool two = ipiv[c] < 0;
-    // a 2x2 pivot is only taken when colmax > 0, so e != 0 exactly on the first column of a pair
-    const cz e0 = ld<C>(ev_, c, aim);
-    const int c1 = (two && (e0.r != 0.0 || e0.i != 0.0)) ? c : c - 1;  // first column of the pair
-    for (int r = threadIdx.x; r < M; r += NT2) {
-      int64_t e = (int64_t)r + (int64_t)c * ldW;
-      cz wv = ld<C>(W, e, wim);
-      cz out;
-      if (!two) {
-        cz d = ld<C>(dv_, c, aim);
-        out = (d.r == 0.0 && d.i == 0.0) ? wv : dv<C>(wv, d);
-      } else {
-        cz d11 = ld<C>(dv_, c1, aim), d22 = ld<C>(dv_, c1 + 1, aim), d21 = ld<C>(ev_, c1, aim);
-        cz wk = ld<C>(W, (int64_t)r + (int64_t)c1 * ldW, wim), wk1 = ld<C>(W, (int64_t)r + (int64_t)(c1 + 1) * ldW, wim);
-        cz a11 = dv<C>(d22, d21), a22 = dv<C>(d11, d21);
-        cz tt = dv<C>(mk(1.0, 0.0), mul<C>(a11, a22) - mk(1.0, 0.0));
-        cz s21 = dv<C>(tt, d21);
-        out = (c == c1) ? mul<C>(s21, mul<C>(a11, wk) - wk1) : mul<C>(s21, mul<C>(a22, wk1) - wk);
-      }
-      st<C>(Ahat, (int64_t)r + (int64_t)c * ldA, aim, out);
-    }
-  }
-}
-
 // ============================================================================ K3 Schur update
 // Tile configurations (selected at analyze time; env DD_AUX_K3CFG):
 //   0: real 128x128 / complex 64x128, 8 warps, 1 CTA per SM
@@ -1181,6 +1096,80 @@ __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_upd
   });
 }
 
+// ============================================================================ K2 panel TRSM
+// W_t = (A_struct,t P_t^T) L_tt^{-T} as ONE tiled DMMA GEMM per level using the full inverse
+// X = L_tt^{-1} from k_linv: W(m, n) = sum_{k <= n} Ahat(m, perm[k]) X(n, k) -- the column
+// permutation P_t^T is a gather in the A loader, the triangle of X bounds K per column tile.
+// Then k2_dinv forms L = W D^{-1} (1x1 / 2x2, LAPACK scaled form) in place of A_struct,t.
+template <bool C, int CFG>
+__global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k2_gemm(K2Args a) {
+  using Cf = K3Cfg<C, CFG>;
+  using G = typename Cf::G;
+  constexpr int BM = Cf::BM, BN = Cf::BN;
+  extern __shared__ __align__(16) double smem[];
+  const Tile T = a.items[blockIdx.x];
+  const NodeDev nd = a.nd[T.target];
+  const int s = nd.s, m0 = T.tm * BM, n0 = T.tn * BN;
+  Seg sg;
+  sg.a = a.arena + nd.panel + nd.sp;   // Ahat rows (struct part), columns gathered by perm
+  sg.lda = nd.ld;
+  sg.acol = a.perm + nd.ydof;
+  sg.b = a.arena + nd.inv;             // B(k, n) = X(n, k)
+  sg.ldb = nd.ldi;
+  sg.K = min(s, n0 + BN);
+  typename G::Acc acc;
+  G::zero(acc);
+  const int mlim = nd.rp - m0, nlim = s - n0;
+  G::run([&](int) { return sg; }, 1, m0, n0, nd.rp, s, a.aim, a.aim, smem, acc,
+         G::tile_mask(mlim, nlim, G::NO_DIAG));
+  double* W = a.work + nd.w + m0 + (int64_t)n0 * nd.ldw;
+  const int64_t ldw = nd.ldw, wim = a.wim;
+  G::for_each(acc, [&](int r, int c, double vr, double vi) {
+    if (r < mlim && c < nlim) {
+      const int64_t e = (int64_t)r + (int64_t)c * ldw;
+      W[e] = vr;
+      if (C) W[e + wim] = vi;
+    }
+  });
+}
+
+constexpr int NT2 = 128;
+template <bool C>
+__global__ void __launch_bounds__(NT2) k2_dinv(K2Args a) {
+  const Strip S = a.strips[blockIdx.x];
+  const NodeDev nd = a.nd[S.t];
+  const int s = nd.s, M = S.nrows;
+  const int64_t ldA = nd.ld, ldW = nd.ldw, aim = a.aim, wim = a.wim;
+  double* Ahat = a.arena + nd.panel + nd.sp + S.row0;
+  const double* W = a.work + nd.w + S.row0;
+  const double* dv_ = a.arena + a.d_off + nd.ydof;
+  const double* ev_ = a.arena + a.e_off + nd.ydof;
+  const int* ipiv = a.ipiv + nd.ydof;
+  for (int c = blockIdx.y; c < s; c += gridDim.y) {
+    const bool two = ipiv[c] < 0;
+    // a 2x2 pivot is only taken when colmax > 0, so e != 0 exactly on the first column of a pair
+    const cz e0 = ld<C>(ev_, c, aim);
+    const int c1 = (two && (e0.r != 0.0 || e0.i != 0.0)) ? c : c - 1;
+    for (int r = threadIdx.x; r < M; r += NT2) {
+      const int64_t e = (int64_t)r + (int64_t)c * ldW;
+      cz out;
+      if (!two) {
+        const cz d = ld<C>(dv_, c, aim), wv = ld<C>(W, e, wim);
+        out = (d.r == 0.0 && d.i == 0.0) ? wv : dv<C>(wv, d);
+      } else {
+        const cz d11 = ld<C>(dv_, c1, aim), d22 = ld<C>(dv_, c1 + 1, aim), d21 = ld<C>(ev_, c1, aim);
+        const cz wk = ld<C>(W, (int64_t)r + (int64_t)c1 * ldW, wim),
+                 wk1 = ld<C>(W, (int64_t)r + (int64_t)(c1 + 1) * ldW, wim);
+        const cz a11 = dv<C>(d22, d21), a22 = dv<C>(d11, d21);
+        const cz tt = dv<C>(mk(1.0, 0.0), mul<C>(a11, a22) - mk(1.0, 0.0));
+        const cz s21 = dv<C>(tt, d21);
+        out = (c == c1) ? mul<C>(s21, mul<C>(a11, wk) - wk1) : mul<C>(s21, mul<C>(a22, wk1) - wk);
+      }
+      st<C>(Ahat, (int64_t)r + (int64_t)c * ldA, aim, out);
+    }
+  }
+}
+
 // ============================================================================ K4 stats
 __global__ void k4_stats(const int64_t* __restrict__ node_stats, int nnodes, int64_t* __restrict__ out) {
   __shared__ int64_t sh[8][8];
@@ -1286,17 +1275,6 @@ void launch_rowperm(bool cplx, const RowpermArgs& a, int nlist, int max_s, cudaS
   }
 }
 
-void launch_k2(bool cplx, const K2Args& a, int nstrips, cudaStream_t st) {
-  if (nstrips == 0) return;
-  if (cplx) {
-    set_smem(k2_panel<true>, K2GemmC::SMEM_BYTES);
-    k2_panel<true><<<nstrips, NT2, K2GemmC::SMEM_BYTES, st>>>(a);
-  } else {
-    set_smem(k2_panel<false>, K2GemmR::SMEM_BYTES);
-    k2_panel<false><<<nstrips, NT2, K2GemmR::SMEM_BYTES, st>>>(a);
-  }
-}
-
 template <int CFG>
 static int bm_of(bool cplx) { return cplx ? K3Cfg<true, CFG>::BM : K3Cfg<false, CFG>::BM; }
 template <int CFG>
@@ -1354,6 +1332,30 @@ void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st)
     case 7: launch_k3_c<7>(cplx, a, ntiles, st); break;
     case 8: launch_k3_c<8>(cplx, a, ntiles, st); break;
     default: launch_k3_c<1>(cplx, a, ntiles, st); break;
+  }
+}
+
+template <bool C, int CFG>
+static void launch_k2_t(const K2Args& a, int nitems, cudaStream_t st) {
+  using Cf = K3Cfg<C, CFG>;
+  set_smem(k2_gemm<C, CFG>, Cf::G::SMEM_BYTES);
+  k2_gemm<C, CFG><<<nitems, Cf::NT, Cf::G::SMEM_BYTES, st>>>(a);
+}
+
+void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, cudaStream_t st) {
+  if (nitems > 0) {
+    switch (cfg) {  // same tile shapes as the Schur update
+      case 6: cplx ? launch_k2_t<true, 6>(a, nitems, st) : launch_k2_t<false, 6>(a, nitems, st); break;
+      case 5: cplx ? launch_k2_t<true, 5>(a, nitems, st) : launch_k2_t<false, 5>(a, nitems, st); break;
+      case 4: cplx ? launch_k2_t<true, 4>(a, nitems, st) : launch_k2_t<false, 4>(a, nitems, st); break;
+      case 1: cplx ? launch_k2_t<true, 1>(a, nitems, st) : launch_k2_t<false, 1>(a, nitems, st); break;
+      default: cplx ? launch_k2_t<true, 7>(a, nitems, st) : launch_k2_t<false, 7>(a, nitems, st); break;
+    }
+  }
+  if (nstrips > 0) {
+    dim3 grid(nstrips, 8);
+    if (cplx) k2_dinv<true><<<grid, NT2, 0, st>>>(a);
+    else k2_dinv<false><<<grid, NT2, 0, st>>>(a);
   }
 }
 

@@ -41,7 +41,8 @@ struct RowpermArgs {
 };
 
 struct K2Args {
-  const Strip* strips;
+  const Tile* items;      // GEMM tiles (node, row strip, column tile)
+  const Strip* strips;    // row strips for L = W D^{-1}
   const NodeDev* nd;
   double* arena;
   int64_t aim;
@@ -130,7 +131,7 @@ size_t k1_smem(bool cplx);
 void launch_k1(bool cplx, const K1Args& a, int nnodes, int max_s, cudaStream_t st);
 constexpr int K1_MAX_BLOCK = 4096;  // largest interface (diagonal block) size K1 supports
 void launch_rowperm(bool cplx, const RowpermArgs& a, int nlist, int max_s, cudaStream_t st);
-void launch_k2(bool cplx, const K2Args& a, int nstrips, cudaStream_t st);
+void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, cudaStream_t st);
 int k3_bm(bool cplx, int cfg);
 int k3_bn(bool cplx, int cfg);
 void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st);
