@@ -344,7 +344,7 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
       nd.w = w;
       w += (int64_t)nd.ldw * nd.s;
       nd.k1w = k1;
-      k1 += (int64_t)nd.sp * K1NB;
+      k1 += (int64_t)nd.sp * K1NB_MAX;
     }
     h->nW = std::max(h->nW, w);
     h->nK1 = std::max(h->nK1, k1);
@@ -768,6 +768,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   k1.d_off = h->d_off;
   k1.e_off = h->e_off;
   k1.stats = (int64_t*)(F + h->off_stats);
+  k1.nb = getenv("DD_AUX_K1NB") ? atoi(getenv("DD_AUX_K1NB")) : 0;
   CUDA_TRY(cudaMemsetAsync(k1.ipiv, 0, (size_t)h->n_pad * 4, st));
   RowpermArgs rp{(const RowPerm*)(F + h->off_rowperm), dnodes, arena, aim, k1.perm};
   K2Args k2{(const Tile*)(F + h->off_k2items), (const Strip*)(F + h->off_strips), dnodes, arena, aim, work, wim,

@@ -52,7 +52,19 @@ __global__ void k0_load(const double* __restrict__ vals, const LoadBlock* __rest
 
 // ============================================================================ K1 diagonal BK
 constexpr int NT1 = 256;
-constexpr size_t K1_LP_BUDGET = 192 * 1024;  // shared-memory bytes for the K1 panel copy of L
+constexpr size_t K1_SMEM_BUDGET = 210 * 1024;  // dynamic smem for the panel copy of L + W window
+
+// Panel width: the widest of 64, 56, ..., 8 whose shared panel copy of L (s x NB) plus the W
+// window cache (NB x (NB+1)) fits the budget; an explicit override (8..64) wins if it fits.
+__host__ __device__ inline size_t k1_panel_bytes(int s, bool cplx, int nb) {
+  return ((size_t)s * nb + (size_t)nb * (nb + 1)) * (cplx ? 16 : 8);
+}
+__host__ __device__ inline int k1_panel_nb(int s, bool cplx, int req) {
+  if (req >= 8 && req <= K1NB_MAX && k1_panel_bytes(s, cplx, req) <= K1_SMEM_BUDGET) return req;
+  int nb = K1NB_MAX;
+  while (nb > 8 && k1_panel_bytes(s, cplx, nb) > K1_SMEM_BUDGET) nb -= 8;
+  return nb;
+}
 // rows per thread: s <= NT1 * MAXQ (4 -> 1024 on the fast path, 16 -> 4096 for larger interfaces)
 using K1GemmR = Gemm<64, 64, 16, 2, 4, 2, false, false, false>;
 using K1GemmC = Gemm<64, 64, 16, 2, 4, 2, true, false, false>;
@@ -198,10 +210,8 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
   __shared__ double shv[2][NT1 / 32];
   __shared__ int shi[2][NT1 / 32];
   int aslot = 0;
-  __shared__ double wrow_r[K1NB], wrow_i[K1NB];
-  __shared__ double wt_r[K1NB][K1NB + 1];
-  __shared__ int s_swa[K1NB], s_swb[K1NB], s_nswp;
-  __shared__ double wt_i[C ? K1NB : 1][C ? K1NB + 1 : 1];
+  __shared__ double wrow_r[K1NB_MAX], wrow_i[K1NB_MAX];
+  __shared__ int s_swa[K1NB_MAX], s_swb[K1NB_MAX], s_nswp;
   __shared__ int s_kp, s_kstep, s_zero, s_imax;
   __shared__ double s_absakk2[2];  // parity-buffered: no barrier between a read and the next write
 
@@ -235,10 +245,13 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
   // their current W values in registers, so a column without interchange costs two barriers.
   // Interchanges of rows inside L columns of EARLIER panels (explicit form, L5) are deferred
   // to the panel end (LAPACK xLASWP style): nothing in this kernel reads those columns before.
-  int NB = K1NB;
-  while (NB > 8 && (size_t)s * NB * (C ? 16 : 8) > K1_LP_BUDGET) NB = NB > 16 ? NB - 8 : NB / 2;
+  const int NB = k1_panel_nb(s, C, a.nb);
   double* Lpr = smem;                       // Lp(i, m) = Lpr[m * s + i]
   double* Lpi = smem + (size_t)s * NB;
+  // W window cache wt(r, m) = W(c0 + r, m), row stride NB+1 (after the panel copy of L)
+  double* wtr = smem + (size_t)s * NB * (C ? 2 : 1);
+  double* wti = wtr + (size_t)NB * (NB + 1);
+  const int WLD = NB + 1;
   auto LP = [&](int i, int m) { return (size_t)m * s + i; };
   cz Ak[K1_MAXQ], wv[K1_MAXQ], wv2[K1_MAXQ];
 #pragma unroll
@@ -265,12 +278,12 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
         if (i < k || i >= s) continue;
         cz v = Ak[q];
         for (int m = 0; m < kk; ++m)
-          v = fms<C>(v, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0), mk(wt_r[kk][m], C ? wt_i[kk][m] : 0.0));
+          v = fms<C>(v, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0), mk(wtr[(kk) * WLD + (m)], C ? wti[(kk) * WLD + (m)] : 0.0));
         wv[q] = v;
         st<C>(W, Wel(i, kk), wim, v);
         if (i - c0 < NB) {
-          wt_r[i - c0][kk] = v.r;
-          if constexpr (C) wt_i[i - c0][kk] = v.i;
+          wtr[(i - c0) * WLD + (kk)] = v.r;
+          if constexpr (C) wti[(i - c0) * WLD + (kk)] = v.i;
         }
         double av = cabs1<C>(v);
         if (i == k) s_absakk2[k & 1] = av;
@@ -310,14 +323,14 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           if (i < k || i >= s) continue;
           cz v = (i < imax) ? ld<C>(A, Ael(imax, i), aim) : ld<C>(A, Ael(i, imax), aim);
           for (int m = 0; m < kk; ++m) {
-            const cz w = inwin ? mk(wt_r[imax - c0][m], C ? wt_i[imax - c0][m] : 0.0) : mk(wrow_r[m], wrow_i[m]);
+            const cz w = inwin ? mk(wtr[(imax - c0) * WLD + (m)], C ? wti[(imax - c0) * WLD + (m)] : 0.0) : mk(wrow_r[m], wrow_i[m]);
             v = fms<C>(v, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0), w);
           }
           wv2[q] = v;
           st<C>(W, Wel(i, kk + 1), wim, v);
           if (i - c0 < NB) {
-            wt_r[i - c0][kk + 1] = v.r;
-            if constexpr (C) wt_i[i - c0][kk + 1] = v.i;
+            wtr[(i - c0) * WLD + (kk + 1)] = v.r;
+            if constexpr (C) wti[(i - c0) * WLD + (kk + 1)] = v.i;
           }
           if (i != imax) {
             double av = cabs1<C>(v);
@@ -332,7 +345,7 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
         if (absakk >= alpha * colmax * (colmax / rowmax)) {
           kp = k;
         } else {
-          const double aii = cabs1<C>(inwin ? mk(wt_r[imax - c0][kk + 1], C ? wt_i[imax - c0][kk + 1] : 0.0)
+          const double aii = cabs1<C>(inwin ? mk(wtr[(imax - c0) * WLD + (kk + 1)], C ? wti[(imax - c0) * WLD + (kk + 1)] : 0.0)
                                             : ld<C>(W, Wel(imax, kk + 1), wim));
           kp = imax;
           if (aii >= alpha * rowmax) {  // 1x1 pivot on the imax column: it becomes column kk
@@ -343,8 +356,8 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
               wv[q] = wv2[q];
               st<C>(W, Wel(i, kk), wim, wv2[q]);
               if (i - c0 < NB) {
-                wt_r[i - c0][kk] = wv2[q].r;
-                if constexpr (C) wt_i[i - c0][kk] = wv2[q].i;
+                wtr[(i - c0) * WLD + (kk)] = wv2[q].r;
+                if constexpr (C) wti[(i - c0) * WLD + (kk)] = wv2[q].i;
               }
             }
           } else {
@@ -376,11 +389,11 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           cz x = ld<C>(W, Wel(kkk, m), wim), y = ld<C>(W, Wel(kp, m), wim);
           st<C>(W, Wel(kkk, m), wim, y);
           st<C>(W, Wel(kp, m), wim, x);
-          wt_r[kkk - c0][m] = y.r;
-          if constexpr (C) wt_i[kkk - c0][m] = y.i;
+          wtr[(kkk - c0) * WLD + (m)] = y.r;
+          if constexpr (C) wti[(kkk - c0) * WLD + (m)] = y.i;
           if (kpwin) {
-            wt_r[kp - c0][m] = x.r;
-            if constexpr (C) wt_i[kp - c0][m] = x.i;
+            wtr[(kp - c0) * WLD + (m)] = x.r;
+            if constexpr (C) wti[(kp - c0) * WLD + (m)] = x.i;
           }
         }
         if (tid == 0) {
@@ -405,7 +418,7 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
       }
       // ---- L columns (shared panel copy) and D; the next column is prefetched
       if (kstep == 1) {
-        const cz D = mk(wt_r[kk][kk], C ? wt_i[kk][kk] : 0.0);
+        const cz D = mk(wtr[(kk) * WLD + (kk)], C ? wti[(kk) * WLD + (kk)] : 0.0);
         const cz rD = zero ? mk(1.0, 0.0) : dv<C>(mk(1.0, 0.0), D);
 #pragma unroll
         for (int q = 0; q < K1_MAXQ; ++q) {
@@ -423,8 +436,8 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           if (kp != k) ++nswap;
         }
       } else {
-        const cz w11 = mk(wt_r[kk][kk], C ? wt_i[kk][kk] : 0.0), w21 = mk(wt_r[kk + 1][kk], C ? wt_i[kk + 1][kk] : 0.0),
-                 w22 = mk(wt_r[kk + 1][kk + 1], C ? wt_i[kk + 1][kk + 1] : 0.0);
+        const cz w11 = mk(wtr[(kk) * WLD + (kk)], C ? wti[(kk) * WLD + (kk)] : 0.0), w21 = mk(wtr[(kk + 1) * WLD + (kk)], C ? wti[(kk + 1) * WLD + (kk)] : 0.0),
+                 w22 = mk(wtr[(kk + 1) * WLD + (kk + 1)], C ? wti[(kk + 1) * WLD + (kk + 1)] : 0.0);
         // LAPACK dlasyf scaled closed form of [W_k W_k+1] D^{-1}
         const cz d11 = dv<C>(w22, w21), d22 = dv<C>(w11, w21);
         const cz tt = dv<C>(mk(1.0, 0.0), mul<C>(d11, d22) - mk(1.0, 0.0));
@@ -1213,16 +1226,18 @@ void launch_load(bool cplx, const double* vals, const LoadBlock* lb, int nblocks
   else k0_load<false><<<grid, 256, 0, st>>>(vals, lb, nblocks, arena, aim);
 }
 
-size_t k1_smem(bool cplx) {
+size_t k1_smem(bool cplx, int max_s, int nb_req) {
   size_t g = cplx ? K1GemmC::SMEM_BYTES : K1GemmR::SMEM_BYTES;
   size_t inv = (size_t)(NT1 / 32) * 2 * TB * TB * sizeof(double);
   size_t m = g > inv ? g : inv;
-  return m > K1_LP_BUDGET ? m : K1_LP_BUDGET;
+  // the budget covers the largest block of the launch; smaller blocks pick widths that fit it too
+  const size_t lp = k1_panel_bytes(max_s, cplx, k1_panel_nb(max_s, cplx, nb_req));
+  return std::max<size_t>(std::max(m, lp), (size_t)K1_SMEM_BUDGET);
 }
 
 template <bool C, int Q>
-static void launch_k1_t(const K1Args& a, int nnodes, cudaStream_t st) {
-  const size_t sm = k1_smem(C);
+static void launch_k1_t(const K1Args& a, int nnodes, int max_s, cudaStream_t st) {
+  const size_t sm = k1_smem(C, max_s, a.nb);
   set_smem(k1_diag_bk<C, Q>, sm);
   k1_diag_bk<C, Q><<<nnodes, NT1, sm, st>>>(a);
 }
@@ -1243,11 +1258,11 @@ void launch_k1(bool cplx, const K1Args& a, int nnodes, int max_s, cudaStream_t s
     return;
   }
   if (max_s <= NT1 * 4) {
-    if (cplx) launch_k1_t<true, 4>(a, nnodes, st);
-    else launch_k1_t<false, 4>(a, nnodes, st);
+    if (cplx) launch_k1_t<true, 4>(a, nnodes, max_s, st);
+    else launch_k1_t<false, 4>(a, nnodes, max_s, st);
   } else {
-    if (cplx) launch_k1_t<true, 16>(a, nnodes, st);
-    else launch_k1_t<false, 16>(a, nnodes, st);
+    if (cplx) launch_k1_t<true, 16>(a, nnodes, max_s, st);
+    else launch_k1_t<false, 16>(a, nnodes, max_s, st);
   }
 }
 

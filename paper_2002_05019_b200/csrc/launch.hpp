@@ -30,6 +30,7 @@ struct K1Args {
   int* ginv;
   int64_t d_off, e_off;
   int64_t* stats;
+  int nb;  // K1 panel width override (0 = automatic; env DD_AUX_K1NB, A/B only)
 };
 
 struct RowpermArgs {
@@ -127,7 +128,7 @@ struct SpmvArgs {
 
 void launch_load(bool cplx, const double* vals, const LoadBlock* lb, int nblocks, int64_t max_elems, double* arena,
                  int64_t aim, cudaStream_t st);
-size_t k1_smem(bool cplx);
+size_t k1_smem(bool cplx, int max_s, int nb_req);
 void launch_k1(bool cplx, const K1Args& a, int nnodes, int max_s, cudaStream_t st);
 constexpr int K1_MAX_BLOCK = 4096;  // largest interface (diagonal block) size K1 supports
 void launch_rowperm(bool cplx, const RowpermArgs& a, int nlist, int max_s, cudaStream_t st);

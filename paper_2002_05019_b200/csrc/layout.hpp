@@ -12,7 +12,8 @@
 namespace ddaux {
 
 constexpr int TB = 32;     // diagonal-tile size of the precomputed L_kk^{-1} tiles (TRSM via GEMM)
-constexpr int K1NB = 32;   // panel width of the blocked in-block Bunch-Kaufman (dlasyf-style)
+constexpr int K1NB = 32;      // panel width of the blocked in-block Bunch-Kaufman (dlasyf-style)
+constexpr int K1NB_MAX = 64;  // widest K1 panel (real blocks small enough for a 64-column smem panel)
 
 inline int64_t pad2(int64_t x) { return (x + 1) & ~int64_t(1); }
 inline int64_t pad8(int64_t x) { return (x + 7) & ~int64_t(7); }
