@@ -117,6 +117,53 @@ struct Gemm {
         }
   }
 
+  // Epilogue through shared memory: the accumulator tile is staged in the (idle) pipeline buffers
+  // and written back column-coalesced with all loads of a batch in flight before the stores
+  // (the fragment-order read-modify-write serialised ~32 dependent L2 round trips per tile).
+  // MODE 0: C = acc, 1: C -= acc.  Call after run() (which ends with a barrier); ends with one.
+  static constexpr int ELD = BM + 2;
+  static_assert((size_t)BN * ELD * (CPLX ? 2 : 1) <= (size_t)STAGES * STAGE, "epilogue tile fits the pipeline smem");
+  template <int MODE>
+  __device__ static void store_tile(const Acc& acc, double* smem, double* C, int64_t ldc, int64_t cim, int mlim,
+                                    int nlim) {
+    double* Sr = smem;
+    double* Si = smem + BN * ELD;
+    for_each(acc, [&](int r, int c, double vr, double vi) {
+      Sr[c * ELD + r] = vr;
+      if constexpr (CPLX) Si[c * ELD + r] = vi;
+    });
+    __syncthreads();
+    constexpr int PER = (BM * BN + NTHR - 1) / NTHR;
+    constexpr int BATCH = PER < 8 ? PER : 8;
+#pragma unroll 1
+    for (int q0 = 0; q0 < PER; q0 += BATCH) {
+      double old_r[BATCH], old_i[CPLX ? BATCH : 1];
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u) {
+        const int e = threadIdx.x + (q0 + u) * NTHR;
+        const int r = e % BM, c = e / BM;
+        if (MODE == 1 && q0 + u < PER && c < BN && r < mlim && c < nlim) {
+          old_r[u] = C[r + (int64_t)c * ldc];
+          if constexpr (CPLX) old_i[u] = C[r + (int64_t)c * ldc + cim];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u) {
+        const int e = threadIdx.x + (q0 + u) * NTHR;
+        const int r = e % BM, c = e / BM;
+        if (q0 + u < PER && c < BN && r < mlim && c < nlim) {
+          const double vr = Sr[c * ELD + r];
+          C[r + (int64_t)c * ldc] = MODE == 1 ? old_r[u] - vr : vr;
+          if constexpr (CPLX) {
+            const double vi = Si[c * ELD + r];
+            C[r + (int64_t)c * ldc + cim] = MODE == 1 ? old_i[u] - vi : vi;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+
   __device__ static void load_stage(double* st, const Seg& sg, int kofs, int m0, int n0, int M, int N,
                                     int64_t aim, int64_t bim) {
     double* As = st;

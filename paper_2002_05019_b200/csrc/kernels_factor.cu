@@ -1099,14 +1099,7 @@ __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_upd
   const unsigned mask = G::tile_mask(mlim, nlim, tg.diag ? T.tn * BN - T.tm * BM : G::NO_DIAG);
   G::run(segfn, tg.c1 - tg.c0, T.tm * BM, T.tn * BN, tg.M, tg.N, a.wim, a.aim, smem, acc, mask);
   double* Cb = a.arena + nj.panel + tg.ro + (int64_t)T.tm * BM + (int64_t)T.tn * BN * nj.ld;
-  const int64_t ldc = nj.ld, aim = a.aim;
-  G::for_each(acc, [&](int r, int c, double vr, double vi) {
-    if (r < mlim && c < nlim) {
-      int64_t e = (int64_t)r + (int64_t)c * ldc;
-      Cb[e] -= vr;
-      if (C) Cb[e + aim] -= vi;
-    }
-  });
+  G::template store_tile<1>(acc, smem, Cb, nj.ld, a.aim, mlim, nlim);
 }
 
 // ============================================================================ K2 panel TRSM
@@ -1136,14 +1129,7 @@ __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k2_gem
   G::run([&](int) { return sg; }, 1, m0, n0, nd.rp, s, a.aim, a.aim, smem, acc,
          G::tile_mask(mlim, nlim, G::NO_DIAG));
   double* W = a.work + nd.w + m0 + (int64_t)n0 * nd.ldw;
-  const int64_t ldw = nd.ldw, wim = a.wim;
-  G::for_each(acc, [&](int r, int c, double vr, double vi) {
-    if (r < mlim && c < nlim) {
-      const int64_t e = (int64_t)r + (int64_t)c * ldw;
-      W[e] = vr;
-      if (C) W[e + wim] = vi;
-    }
-  });
+  G::template store_tile<0>(acc, smem, W, nd.ldw, a.wim, mlim, nlim);
 }
 
 constexpr int NT2 = 128;

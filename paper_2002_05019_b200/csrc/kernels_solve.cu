@@ -116,14 +116,7 @@ __global__ void __launch_bounds__(128) k_diag_g(SolveArgs a) {
   G::zero(acc);
   G::run([&](int) { return sg; }, 1, 0, n0, s - m0, a.nrhs, a.aim, a.yim, smem, acc,
          G::tile_mask(s - m0, a.nrhs - n0, G::NO_DIAG));
-  double* T = a.T + D.toff + m0;
-  G::for_each(acc, [&](int r, int c, double vr, double vi) {
-    if (m0 + r < s && n0 + c < a.nrhs) {
-      const int64_t e = (int64_t)r + (int64_t)(n0 + c) * a.ldT;
-      T[e] = vr;
-      if (C) T[e + a.Tim] = vi;
-    }
-  });
+  G::template store_tile<0>(acc, smem, a.T + D.toff + m0 + (int64_t)n0 * a.ldT, a.ldT, a.Tim, s - m0, a.nrhs - n0);
 }
 
 template <bool C>
@@ -163,14 +156,8 @@ __global__ void __launch_bounds__(128) k_fupd(SolveArgs a) {
   };
   G::run(segfn, T.c1 - T.c0, m0, n0, ni.s, a.nrhs, a.aim, a.yim, smem, acc,
          G::tile_mask(ni.s - m0, a.nrhs - n0, G::NO_DIAG));
-  double* y = a.y + ni.ydof;
-  G::for_each(acc, [&](int r, int c, double vr, double vi) {
-    if (m0 + r < ni.s && n0 + c < a.nrhs) {
-      int64_t e = (int64_t)(m0 + r) + (int64_t)(n0 + c) * a.ldy;
-      y[e] -= vr;
-      if (C) y[e + a.yim] -= vi;
-    }
-  });
+  G::template store_tile<1>(acc, smem, a.y + ni.ydof + m0 + (int64_t)n0 * a.ldy, a.ldy, a.yim, ni.s - m0,
+                            a.nrhs - n0);
 }
 
 // Backward pull update y_t -= sum_{i in struct(t)} L_it^T y_i.  With split-K (G > 1) CTA
@@ -200,14 +187,8 @@ __global__ void __launch_bounds__(128) k_bupd(SolveArgs a, int G, double* part, 
   G_::run(segfn, q1 - q0, m0, n0, nt.s, a.nrhs, a.aim, a.yim, smem, acc,
           G_::tile_mask(nt.s - m0, a.nrhs - n0, G_::NO_DIAG));
   if (G == 1) {
-    double* y = a.y + nt.ydof;
-    G_::for_each(acc, [&](int r, int c, double vr, double vi) {
-      if (m0 + r < nt.s && n0 + c < a.nrhs) {
-        int64_t e = (int64_t)(m0 + r) + (int64_t)(n0 + c) * a.ldy;
-        y[e] -= vr;
-        if (C) y[e + a.yim] -= vi;
-      }
-    });
+    G_::template store_tile<1>(acc, smem, a.y + nt.ydof + m0 + (int64_t)n0 * a.ldy, a.ldy, a.yim, nt.s - m0,
+                               a.nrhs - n0);
   } else {
     double* P = part + (int64_t)blockIdx.x * SUBM * a.nrhs;  // SUBM x nrhs, ld SUBM
     G_::for_each(acc, [&](int r, int c, double vr, double vi) {
