@@ -74,6 +74,15 @@ def fp64_peak(cplx):
     return (d["zgemm_tflops_burst"] if cplx else d["dgemm_tflops_burst"]), os.path.relpath(path, ROOT)
 
 
+def hbm_peak():
+    """Measured HBM copy bandwidth (GB/s) of this pool's B200s (driver-written MEASURED_PEAKS.json)."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(path))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (b.copy_(a), read+write bytes)"
+    except Exception:
+        return 7700.0, "fallback: nominal HBM3e 7.7 TB/s (MEASURED_PEAKS.json absent)"
+
+
 class Clocks:
     """nvidia-smi sampler (B200_PROFILING.md clocks line) running during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -183,6 +192,13 @@ def reduce_max(values, dist, device="cpu"):
     return [float(x) for x in t.tolist()]
 
 
+def rhs_shard(batches, world, rank):
+    """f4: the multi-RHS solve shards by right-hand-side columns with zero
+    communication -- every rank holds its own factor replica and solves batches
+    rank, rank + world, ... of the job's RHS batches (round robin)."""
+    return list(range(rank, batches, world))
+
+
 def reference_arm(args, rank, world):
     """The oracle on the box's host cores; rank 0 only (others exit 0 without work)."""
     if rank != 0:
@@ -227,7 +243,8 @@ def gpu_arm(args, rank, world, local, dist):
     c = dd_inputs.CONFIGS[cfg]
     nrhs = args.nrhs or c["nrhs"]
     t0 = time.time()
-    prob = dd_inputs.config(cfg, seed=args.seed + rank, backend="torch", device=str(dev))
+    # clique form of the workload (one dense S_p per subdomain, drawn on the device)
+    prob, Scl, Soff = dd_inputs.config_cliques(cfg, seed=args.seed + rank, device=str(dev))
     torch.cuda.synchronize()
     gen_s = time.time() - t0
     cplx = prob.is_complex
@@ -238,13 +255,30 @@ def gpu_arm(args, rank, world, local, dist):
                           complex_3m=not args.complex_4m)
     analyze_s = time.time() - t0
     info = solver.info
-    vals = prob.values
+    # f1: the auxiliary matrix is assembled on the device from the cliques by the library
+    # (HBM-bound; measured here, outside the factor+solve step), then the cliques are freed
+    cl = [c for _, c in prob.cliques]
+    vals = solver.assemble(cl, Scl, Soff, prob.val_offset)
+    dd.dd_aux_set_trace(solver.h, True)
+    dd.dd_aux_get_trace(solver.h, reset=True)
+    solver.assemble(cl, Scl, Soff, prob.val_offset, d_vals=vals)
+    asm_ms = dd.dd_aux_get_trace(solver.h, reset=True)["assemble"]["ms"]
+    dd.dd_aux_set_trace(solver.h, False)
+    asm_bytes = dd.dd_aux_last_assemble_bytes(solver.h)
+    del Scl
+    solver._asm_work = None
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    prob.values = vals
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + args.seed + rank)
     tdt = torch.complex128 if cplx else torch.float64
     Bsrc = torch.randn((nrhs, prob.n), dtype=tdt, device=dev, generator=gen).t()  # column-major n x nrhs
     Bw = torch.empty((nrhs, prob.n), dtype=tdt, device=dev).t()
     batches = c.get("batches", 1)  # configs[4]: many-excitation stress test, batches of nrhs per step
+    # f4: with several batches per step and N > 1 ranks, the RHS batches are sharded across the
+    # ranks' factor replicas (strong scaling of the solve); a single batch is replicated (weak)
+    my_batches = rhs_shard(batches, world, rank) if batches > 1 else [0]
     solver.factor(vals, prob.val_offset)  # allocates factor/work buffers
     solver._work(max(info["work_bytes"], dd.dd_aux_solve_work_bytes(solver.h, nrhs)))
     stream = torch.cuda.current_stream()
@@ -256,7 +290,7 @@ def gpu_arm(args, rank, world, local, dist):
             raise RuntimeError(f"factor rc={rc}")
         ev[1].record(stream)
         ev[2].record(stream)
-        for _ in range(batches):
+        for _ in my_batches:
             Bw.copy_(Bsrc)
             solver.solve_(Bw)
         ev[3].record(stream)
@@ -369,11 +403,16 @@ def gpu_arm(args, rank, world, local, dist):
                    "l2": "inputs larger than L2 (no flush needed)",
                    "parallelism": "replicas" if world > 1 else "single GPU"},
         "factor_ms": fac_ms / K, "factor_frac_of_fp64_peak": value / world / 1e3 / peak_tf,
-        "solve_ms_per_1000_rhs": sol_ms / K * 1000.0 / (nrhs * batches), "solve_ms_per_batch": sol_ms / K / batches,
+        "solve_ms_per_1000_rhs": (sol_ms / K * 1000.0 / (nrhs * batches)) if batches > 1
+        else (sol_ms / K * 1000.0 / nrhs),
+        "solve_ms_per_batch": sol_ms / K / max(1, len(my_batches)),
         "solve_batches_per_step": batches,
+        "solve_sharding": ({"by": "rhs batches (round robin over the ranks' factor replicas)", "scaling": "strong",
+                            "batches_per_rank": [len(rhs_shard(batches, world, r)) for r in range(world)]}
+                           if batches > 1 and world > 1 else None),
         # HBM evidence for the solve: each sweep streams the whole factor once (L panels + inverse
         # diagonal blocks); (1 + refine_steps) sweeps per batch; achieved = those bytes / solve time
-        "solve_hbm_gbs": (1 + args.refine) * info["factor_value_bytes"] * batches * K / (sol_ms * 1e-3) / 1e9,
+        "solve_hbm_gbs": (1 + args.refine) * info["factor_value_bytes"] * len(my_batches) * K / (sol_ms * 1e-3) / 1e9,
         "flops_factor": flops, "flops_solve_per_rhs": info["flops_solve_per_rhs"],
         "accuracy": {"berr_max": berr, "berr_unrefined_max": berr0, "columns_checked": len(cols),
                      "tolerance": 1e-12, "refine_steps": args.refine, "refine_tol": args.refine_tol,
@@ -386,6 +425,11 @@ def gpu_arm(args, rank, world, local, dist):
         "phases": {p: {"ms_per_step": v["ms"] / K, "launches_per_step": v["launches"] / K,
                        "tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["ms"] > 0 and v["flops"] > 0 else None}
                    for p, v in trace.items() if v["launches"]},
+        "assemble": {"kernel": "k_assemble", "bound": "hbm", "ms": asm_ms, "bytes": asm_bytes,
+                     "achieved_gbs": asm_bytes / (asm_ms * 1e-3) / 1e9 if asm_ms > 0 else None,
+                     "peak_gbs": hbm_peak()[0], "frac": (asm_bytes / (asm_ms * 1e-3) / 1e9 / hbm_peak()[0])
+                     if asm_ms > 0 else None, "peak_src": hbm_peak()[1],
+                     "what": "f1: A = sum_p sym(S_p) over the cliques, read S_p blocks + write A (algorithmic bytes)"},
         "gpu_launches": launches,
         "clocks": clk, "cpu_baseline": cpu, "e2e": e2e,
         "setup_s": {"generate": gen_s, "analyze": analyze_s},

@@ -16,12 +16,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 HERE = os.path.join(ROOT, "paper_2002_05019_b200")
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdd_aux.so")
-SOURCES = ["api.cu", "kernels_factor.cu", "kernels_solve.cu", "analyze.cpp"]
+SOURCES = ["api.cu", "kernels_factor.cu", "kernels_solve.cu", "kernels_assemble.cu", "analyze.cpp"]
 HEADERS = ["analyze.hpp", "layout.hpp", "launch.hpp", "common.cuh", "gemm_core.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
+# A/B switches (e.g. DD_AUX_DEFS="DDK_SEGC=0 DDK_EPI_BATCH=16"): compile-time kernel variants
+FLAGS += ["-D" + d for d in os.environ.get("DD_AUX_DEFS", "").split()]
 
 
 def _digest() -> str:

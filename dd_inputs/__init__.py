@@ -39,7 +39,8 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-__all__ = ["Problem", "grid_interfaces", "build_problem", "config", "CONFIGS", "random_rhs",
+__all__ = ["Problem", "grid_interfaces", "build_problem", "build_clique_buffer", "config", "config_cliques",
+           "CONFIGS", "random_rhs",
            "dense_expand", "block_pattern_from_cliques"]
 
 
@@ -204,15 +205,8 @@ def _layout(blk_size, colptr, rowidx):
     return off, tot
 
 
-def build_problem(nx, ny, nz, sizes_fn, *, complex_=False, seed=0, topology="faces",
-                  backend="numpy", device="cpu", name="") -> Problem:
-    """Build the auxiliary matrix of a grid DD model (recipe in the module doc).
-
-    sizes_fn(n_interfaces, rng) -> int array of interface sizes.
-    backend "numpy" draws with default_rng(seed); "torch" with a torch.Generator
-    on `device` (values then produced on that device and copied to host numpy).
-    """
-    rng = np.random.default_rng(seed)
+def _topology(nx, ny, nz, sizes_fn, rng, topology):
+    """Interfaces, sizes, cliques, lower block pattern and value layout (no values)."""
     if topology == "faces":
         pairs = grid_interfaces(nx, ny, nz)
     else:
@@ -227,49 +221,74 @@ def build_problem(nx, ny, nz, sizes_fn, *, complex_=False, seed=0, topology="fac
     cliques = [(p, sorted(touch[p])) for p in range(nsub) if touch[p]]
     colptr, rowidx = block_pattern_from_cliques(nblk, [c for _, c in cliques])
     val_offset, total = _layout(blk_size, colptr, rowidx)
+    return pairs, blk_size, cliques, colptr, rowidx, val_offset, total
+
+
+def _clique_draw(m, complex_, rng=None, gen=None, device="cpu"):
+    """One subdomain's raw dense contribution S_p = G^T diag(d) G + sigma*I (before the
+    symmetrisation of ledger L12); numpy (rng) or torch (gen) draws, recipe in the module doc."""
+    sigma = (0.1 + 0.05j) if complex_ else 0.1
+    if rng is not None:
+        G = rng.standard_normal((m, m))
+        if complex_:
+            G = G + 1j * rng.standard_normal((m, m))
+        sign = 2.0 * rng.integers(0, 2, m) - 1.0
+        mag = rng.uniform(0.5, 2.0, m)
+        d = sign * mag
+        if complex_:
+            d = d + 1j * rng.uniform(0.0, 0.1, m)
+        S = G.T @ (d[:, None] * G)
+        return S + sigma * np.eye(m)
+    import torch
+    tdt = torch.complex128 if complex_ else torch.float64
+    G = torch.randn(m, m, generator=gen, device=device, dtype=torch.float64)
+    if complex_:
+        G = torch.complex(G, torch.randn(m, m, generator=gen, device=device, dtype=torch.float64))
+    sign = 2.0 * torch.randint(0, 2, (m,), generator=gen, device=device).double() - 1.0
+    mag = 0.5 + 1.5 * torch.rand(m, generator=gen, device=device, dtype=torch.float64)
+    d = (sign * mag).to(tdt)
+    if complex_:
+        d = d + 1j * (0.1 * torch.rand(m, generator=gen, device=device, dtype=torch.float64))
+    S = G.transpose(0, 1) @ (d[:, None] * G)
+    return S + sigma * torch.eye(m, dtype=tdt, device=device)
+
+
+def build_problem(nx, ny, nz, sizes_fn, *, complex_=False, seed=0, topology="faces",
+                  backend="numpy", device="cpu", name="", keep_cliques=False) -> Problem:
+    """Build the auxiliary matrix of a grid DD model (recipe in the module doc).
+
+    sizes_fn(n_interfaces, rng) -> int array of interface sizes.
+    backend "numpy" draws with default_rng(seed); "torch" with a torch.Generator
+    on `device` (values then stay on that device as a torch tensor).
+    keep_cliques (numpy only): also keep the raw per-clique matrices S_p in
+    prob.clique_S (list, clique order), the input of the f1 assembly.
+    """
+    rng = np.random.default_rng(seed)
+    pairs, blk_size, cliques, colptr, rowidx, val_offset, total = _topology(nx, ny, nz, sizes_fn, rng, topology)
+    nblk = len(pairs)
     dtype = np.complex128 if complex_ else np.float64
     if backend == "torch":
         import torch
         values = torch.zeros(total, dtype=torch.complex128 if complex_ else torch.float64, device=device)
+        gen = torch.Generator(device=device)
+        gen.manual_seed(seed)
     else:
         values = np.zeros(total, dtype=dtype)
     pos = {}
     for j in range(nblk):
         for p in range(int(colptr[j]), int(colptr[j + 1])):
             pos[(int(rowidx[p]), j)] = p
-
-    sigma = (0.1 + 0.05j) if complex_ else 0.1
-    if backend == "torch":
-        import torch
-        gen = torch.Generator(device=device)
-        gen.manual_seed(seed)
-        tdt = torch.complex128 if complex_ else torch.float64
+    kept = []
     for p_sub, members in cliques:
         m = int(sum(blk_size[I] for I in members))
         if backend == "numpy":
-            G = rng.standard_normal((m, m))
-            if complex_:
-                G = G + 1j * rng.standard_normal((m, m))
-            sign = 2.0 * rng.integers(0, 2, m) - 1.0
-            mag = rng.uniform(0.5, 2.0, m)
-            d = sign * mag
-            if complex_:
-                d = d + 1j * rng.uniform(0.0, 0.1, m)
-            S = G.T @ (d[:, None] * G)
-            S = S + sigma * np.eye(m)
+            S = _clique_draw(m, complex_, rng=rng)
+            if keep_cliques:
+                kept.append(S)
             S = 0.5 * (S + S.T)
         else:
             import torch
-            G = torch.randn(m, m, generator=gen, device=device, dtype=torch.float64)
-            if complex_:
-                G = torch.complex(G, torch.randn(m, m, generator=gen, device=device, dtype=torch.float64))
-            sign = 2.0 * torch.randint(0, 2, (m,), generator=gen, device=device).double() - 1.0
-            mag = 0.5 + 1.5 * torch.rand(m, generator=gen, device=device, dtype=torch.float64)
-            d = (sign * mag).to(tdt)
-            if complex_:
-                d = d + 1j * (0.1 * torch.rand(m, generator=gen, device=device, dtype=torch.float64))
-            S = G.transpose(0, 1) @ (d[:, None] * G)
-            S = S + sigma * torch.eye(m, dtype=tdt, device=device)
+            S = _clique_draw(m, complex_, gen=gen, device=device)
             S = 0.5 * (S + S.transpose(0, 1))
         offs = np.concatenate([[0], np.cumsum([blk_size[I] for I in members])])
         if backend == "torch":
@@ -307,7 +326,39 @@ def build_problem(nx, ny, nz, sizes_fn, *, complex_=False, seed=0, topology="fac
     prob = Problem(blk_size, colptr, rowidx, values, val_offset, cliques, name)
     prob.pairs = pairs
     prob.grid = (nx, ny, nz)
+    if keep_cliques:
+        prob.clique_S = kept
     return prob
+
+
+def build_clique_buffer(nx, ny, nz, sizes_fn, *, complex_=False, seed=0, topology="faces", device="cuda",
+                        name=""):
+    """Clique form of the same workload for the f1 assembly bench (torch draws on `device`).
+
+    Returns (prob, S, S_offset): prob carries the pattern and value layout (values=None);
+    S is one 1-D device tensor holding every raw S_p column-major (ld = m_p) at element
+    offset S_offset[p], clique order.  The draws are those of build_problem(backend="torch"),
+    so assembling with symmetrisation reproduces its values.
+    """
+    import torch
+    rng = np.random.default_rng(seed)
+    pairs, blk_size, cliques, colptr, rowidx, val_offset, total = _topology(nx, ny, nz, sizes_fn, rng, topology)
+    ms = [int(sum(blk_size[I] for I in members)) for _, members in cliques]
+    S_offset = np.concatenate([[0], np.cumsum([m * m for m in ms])]).astype(np.int64)
+    tdt = torch.complex128 if complex_ else torch.float64
+    S = torch.empty(int(S_offset[-1]), dtype=tdt, device=device)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    for q, m in enumerate(ms):
+        Sp = _clique_draw(m, complex_, gen=gen, device=device)
+        # column-major m x m == row-major transpose
+        S[int(S_offset[q]):int(S_offset[q]) + m * m].copy_(Sp.transpose(0, 1).reshape(-1))
+        del Sp
+    prob = Problem(blk_size, colptr, rowidx, None, val_offset, cliques, name)
+    prob.pairs = pairs
+    prob.grid = (nx, ny, nz)
+    prob.total = total
+    return prob, S, S_offset[:-1]
 
 
 def corner_interfaces(prob: Problem, sub_grid) -> List[int]:
@@ -407,10 +458,17 @@ CONFIGS = {
 
 
 def config(name: str, *, seed: int = 0, backend: str = "numpy", device: str = "cpu",
-           grid: Optional[Tuple[int, int, int]] = None, sizes=None) -> Problem:
+           grid: Optional[Tuple[int, int, int]] = None, sizes=None, keep_cliques=False) -> Problem:
     """Problem for a named BASELINE config; `grid`/`sizes` override for scaled-down variants."""
     c = CONFIGS[name]
     g = grid or c["grid"]
     sz = c["sizes"] if sizes is None else (sizes if callable(sizes) else _const(int(sizes)))
     return build_problem(*g, sz, complex_=c["complex_"], seed=seed, topology=c["topology"],
-                         backend=backend, device=device, name=name)
+                         backend=backend, device=device, name=name, keep_cliques=keep_cliques)
+
+
+def config_cliques(name: str, *, seed: int = 0, device: str = "cuda"):
+    """Clique form (prob without values, S buffer, S offsets) of a named config (torch draws)."""
+    c = CONFIGS[name]
+    return build_clique_buffer(*c["grid"], c["sizes"], complex_=c["complex_"], seed=seed, topology=c["topology"],
+                               device=device, name=name)

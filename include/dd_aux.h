@@ -63,7 +63,9 @@ typedef struct {
   int32_t order;              /* DD_ORDER_*                                               */
   const int32_t* user_order;  /* [nblk] block elimination order for DD_ORDER_USER (copied) */
   int32_t refine_steps;       /* iterative-refinement steps in dd_aux_solve (default 1, L7) */
-  int32_t use_graphs;         /* reserved (CUDA-graph capture of the level loop), default 0 */
+  int32_t use_graphs;         /* 1: dd_aux_factor's level loop and the whole dd_aux_solve are captured
+                                 once into CUDA graphs (per buffer-pointer set) and replayed; default 0.
+                                 Ignored while tracing is enabled (the trace brackets every launch). */
   double refine_tol;          /* a refinement step is skipped (on the device, no host sync) when
                                  every column already has berr <= refine_tol; 0 = always refine */
   int32_t complex_3m;         /* complex Schur update with 3 real products (Gauss/3M, default 1) or
@@ -153,8 +155,42 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
  * Entries are grouped by elimination position (block order[0] first).  Any pointer may be NULL. */
 int dd_aux_get_pivots(dd_aux_handle_t h, const void* d_factor, int32_t* ipiv, int32_t* perm, void* d, void* e);
 
+/* f1: on-device assembly of the auxiliary matrix from its cliques.
+ * PAPER.md:27 (§II): eliminating a subdomain's primal unknowns leaves a dense contribution
+ * over the dual DoFs of the interfaces it touches; the auxiliary matrix is the
+ * resulting "sparse collection of dense blocks" (one dense clique per subdomain).  This call
+ * writes every lower block of the handle's pattern:
+ *     A_IJ = sum over cliques p containing I and J (ascending p) of  S_p[I rows, J cols]
+ * or, with symmetrize != 0, of (S_p + S_p^T)/2 restricted to those rows/cols (reading L12;
+ * complex: plain transpose, never conjugated).  Blocks no clique covers are written as zero.
+ *  nclq        number of cliques (>= 0)
+ *  clq_ptr     host [nclq+1]: clique p's members are clq_blk[clq_ptr[p] .. clq_ptr[p+1])
+ *  clq_blk     host: interface (block) ids, strictly ascending within a clique; every pair of
+ *              members must be in the handle's block pattern (else DD_ERR_PATTERN)
+ *  d_S         device: clique p's dense m_p x m_p matrix (m_p = sum of its members' sizes,
+ *              DoFs = members concatenated in the listed order), column-major, ld = m_p, at
+ *              element offset S_offset[p]; complex interleaved (re, im).  Read only.
+ *  S_offset    host [nclq] element offsets
+ *  val_offset  host [nnzb_in] element offsets of the output blocks in d_vals (the layout
+ *              dd_aux_factor reads: block at CSC position q is s_row x s_col, ld = s_row)
+ *  d_vals      device out; every element of every block is written
+ *  d_work      device, dd_aux_assemble_work_bytes() bytes, 256-byte aligned (descriptor tables)
+ *  stream      enqueued asynchronously; the host tables are copied before the call returns
+ * The sum is evaluated in a fixed order with correctly rounded additions, so it is bitwise
+ * reproducible and equals the plain loop of oracle/assemble.py exactly. */
+int dd_aux_assemble_work_bytes(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, const int32_t* clq_blk,
+                               size_t* bytes);
+int dd_aux_assemble(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, const int32_t* clq_blk,
+                    const void* d_S, const int64_t* S_offset, int32_t symmetrize, const int64_t* val_offset,
+                    void* d_vals, void* d_work, void* stream);
+/* Algorithmic HBM bytes of the last dd_aux_assemble (contributions read + output written). */
+double dd_aux_last_assemble_bytes(dd_aux_handle_t h);
+
 /* Change the refinement policy of an analyzed handle (same meaning as the options fields). */
 int dd_aux_set_refine(dd_aux_handle_t h, int32_t refine_steps, double refine_tol);
+
+/* Enable / disable CUDA-graph replay (options.use_graphs) on an analyzed handle. */
+int dd_aux_set_graphs(dd_aux_handle_t h, int32_t enable);
 
 /* Tracing (SURVEY.md §5 "CUDA events per phase").  Launch counts and algorithmic flops per
  * kernel class are always accumulated; with tracing enabled every kernel launch is also
@@ -164,7 +200,7 @@ int dd_aux_set_refine(dd_aux_handle_t h, int32_t refine_steps, double refine_tol
 enum {
   DD_PH_LOAD = 0, DD_PH_K1, DD_PH_ROWPERM, DD_PH_K2, DD_PH_K3, DD_PH_STATS,
   DD_PH_PERM, DD_PH_FDIAG, DD_PH_FUPD, DD_PH_DSOLVE, DD_PH_BUPD, DD_PH_BDIAG, DD_PH_SPMV,
-  DD_PH_LINV, DD_NPHASE
+  DD_PH_LINV, DD_PH_ASSEMBLE, DD_NPHASE
 };
 typedef struct {
   double ms[16];        /* device milliseconds per kernel class (tracing enabled only) */

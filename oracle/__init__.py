@@ -22,5 +22,6 @@ symbolic step, SPEC worked examples, metamorphic scaling/negation.  Every oracle
 function is pinned; none is "parity unpinned".
 """
 from .bk import bk_factor, ALPHA, cabs1  # noqa: F401
+from .assemble import assemble  # noqa: F401
 from .block_ldlt import (symbolic, block_factor, block_solve, refine_solve, inertia,  # noqa: F401
                          flops_factor, flops_solve_per_rhs, residual_berr, OracleFactor)

@@ -20,7 +20,8 @@ __all__ = ["DD_REAL64", "DD_COMPLEX128", "DD_ORDER_AUTO", "DD_ORDER_ND", "DD_ORD
            "DD_ORDER_USER", "DD_OK", "DD_ZERO_PIVOT", "DDAuxError", "dd_aux_default_options", "dd_aux_analyze",
            "dd_aux_get_info", "dd_aux_get_order", "dd_aux_get_etree", "dd_aux_solve_work_bytes", "dd_aux_factor",
            "dd_aux_solve", "dd_aux_get_pivots", "dd_aux_destroy", "dd_aux_last_error", "dd_aux_version",
-           "dd_aux_set_refine", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_get_level_trace", "AuxSolver", "LIB_PATH", "EXPORTED_SYMBOLS", "PHASES"]
+           "dd_aux_set_refine", "dd_aux_set_graphs", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_get_level_trace", "dd_aux_assemble_work_bytes", "dd_aux_assemble",
+           "dd_aux_last_assemble_bytes", "cliques_to_csr", "AuxSolver", "LIB_PATH", "EXPORTED_SYMBOLS", "PHASES"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdd_aux.so")
 
@@ -31,10 +32,11 @@ DD_ERR_CUDA, DD_ERR_WORKSPACE, DD_ERR_NOT_FACTORED, DD_ERR_SINGULAR, DD_ERR_PATT
 
 EXPORTED_SYMBOLS = ["dd_aux_default_options", "dd_aux_analyze", "dd_aux_get_info", "dd_aux_get_order",
                     "dd_aux_get_etree", "dd_aux_solve_work_bytes", "dd_aux_factor", "dd_aux_solve",
-                    "dd_aux_get_pivots", "dd_aux_set_refine", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_get_level_trace", "dd_aux_destroy",
-                    "dd_aux_last_error", "dd_aux_version"]
+                    "dd_aux_get_pivots", "dd_aux_set_refine", "dd_aux_set_graphs", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_get_level_trace", "dd_aux_destroy",
+                    "dd_aux_last_error", "dd_aux_version", "dd_aux_assemble_work_bytes", "dd_aux_assemble",
+                    "dd_aux_last_assemble_bytes"]
 PHASES = ["load", "k1_diag_bk", "rowperm", "k2_panel", "k3_update", "stats", "perm", "fdiag", "fupd", "dsolve",
-          "bupd", "bdiag", "spmv", "linv"]
+          "bupd", "bdiag", "spmv", "linv", "assemble"]
 
 
 class DDAuxError(RuntimeError):
@@ -88,8 +90,12 @@ def _load():
         "dd_aux_get_pivots": (ctypes.c_int, [P, P, pi32, pi32, P, P]),
         "dd_aux_set_refine": (ctypes.c_int, [P, i32, ctypes.c_double]),
         "dd_aux_set_trace": (ctypes.c_int, [P, i32]),
+        "dd_aux_set_graphs": (ctypes.c_int, [P, i32]),
         "dd_aux_get_trace": (ctypes.c_int, [P, ctypes.POINTER(dd_aux_trace), i32]),
         "dd_aux_get_level_trace": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+        "dd_aux_assemble_work_bytes": (ctypes.c_int, [P, i64, pi64, pi32, ctypes.POINTER(ctypes.c_size_t)]),
+        "dd_aux_assemble": (ctypes.c_int, [P, i64, pi64, pi32, P, pi64, i32, pi64, P, P, P]),
+        "dd_aux_last_assemble_bytes": (ctypes.c_double, [P]),
         "dd_aux_destroy": (ctypes.c_int, [P]),
         "dd_aux_last_error": (ctypes.c_char_p, []),
         "dd_aux_version": (ctypes.c_char_p, []),
@@ -138,9 +144,10 @@ def dd_aux_version() -> str:
 
 
 def dd_aux_default_options(order=DD_ORDER_AUTO, refine_steps=1, user_order=None, refine_tol=None,
-                           complex_3m=True) -> dd_aux_options:
+                           complex_3m=True, use_graphs=False) -> dd_aux_options:
     o = dd_aux_options()
     _lib.dd_aux_default_options(ctypes.byref(o))
+    o.use_graphs = int(bool(use_graphs))
     o.order = int(order)
     o.complex_3m = int(bool(complex_3m))
     o.refine_steps = int(refine_steps)
@@ -234,6 +241,10 @@ def dd_aux_set_refine(h, refine_steps, refine_tol=0.0):
     _check(_lib.dd_aux_set_refine(h, int(refine_steps), float(refine_tol)))
 
 
+def dd_aux_set_graphs(h, enable=True):
+    _check(_lib.dd_aux_set_graphs(h, int(bool(enable))))
+
+
 def dd_aux_set_trace(h, enable=True):
     _check(_lib.dd_aux_set_trace(h, int(bool(enable))))
 
@@ -254,6 +265,40 @@ def dd_aux_get_level_trace(h) -> dict:
     return {"ms": ms.reshape(nl, 16)[:, :len(PHASES)], "flops": fl.reshape(nl, 16)[:, :len(PHASES)]}
 
 
+def cliques_to_csr(cliques):
+    """[[block ids], ...] -> (clq_ptr int64[nclq+1], clq_blk int32[...]) (marshalling only)."""
+    ptr = np.zeros(len(cliques) + 1, dtype=np.int64)
+    for p, members in enumerate(cliques):
+        ptr[p + 1] = ptr[p] + len(members)
+    blk = np.asarray([int(b) for members in cliques for b in members], dtype=np.int32)
+    return ptr, blk
+
+
+def dd_aux_assemble_work_bytes(h, clq_ptr, clq_blk) -> int:
+    cp = np.ascontiguousarray(clq_ptr, dtype=np.int64)
+    cb = np.ascontiguousarray(clq_blk, dtype=np.int32)
+    b = ctypes.c_size_t()
+    _check(_lib.dd_aux_assemble_work_bytes(h, len(cp) - 1, _np_ptr(cp, ctypes.c_int64), _np_ptr(cb, ctypes.c_int32),
+                                           ctypes.byref(b)))
+    return int(b.value)
+
+
+def dd_aux_assemble(h, clq_ptr, clq_blk, d_S, S_offset, val_offset, d_vals, d_work, symmetrize=True, stream=None):
+    """f1: d_vals <- sum of the cliques' dense contributions (see include/dd_aux.h)."""
+    cp = np.ascontiguousarray(clq_ptr, dtype=np.int64)
+    cb = np.ascontiguousarray(clq_blk, dtype=np.int32)
+    so = np.ascontiguousarray(S_offset, dtype=np.int64)
+    vo = np.ascontiguousarray(val_offset, dtype=np.int64)
+    rc = _lib.dd_aux_assemble(h, len(cp) - 1, _np_ptr(cp, ctypes.c_int64), _np_ptr(cb, ctypes.c_int32), _dev_ptr(d_S),
+                              _np_ptr(so, ctypes.c_int64), int(bool(symmetrize)), _np_ptr(vo, ctypes.c_int64),
+                              _dev_ptr(d_vals), _dev_ptr(d_work), _stream_ptr(stream))
+    return _check(rc)
+
+
+def dd_aux_last_assemble_bytes(h) -> float:
+    return float(_lib.dd_aux_last_assemble_bytes(h))
+
+
 def dd_aux_destroy(h):
     if h:
         _lib.dd_aux_destroy(h)
@@ -267,12 +312,15 @@ class AuxSolver:
     """
 
     def __init__(self, blk_size, colptr, rowidx, complex_=False, order=DD_ORDER_AUTO, refine_steps=1,
-                 user_order=None, device="cuda", refine_tol=None, complex_3m=True):
+                 user_order=None, device="cuda", refine_tol=None, complex_3m=True, use_graphs=False):
         import torch
         self.torch = torch
         self.cplx = bool(complex_)
-        self.opt = dd_aux_default_options(order, refine_steps, user_order, refine_tol, complex_3m)
+        self.opt = dd_aux_default_options(order, refine_steps, user_order, refine_tol, complex_3m, use_graphs)
         self.h = dd_aux_analyze(blk_size, colptr, rowidx, DD_COMPLEX128 if self.cplx else DD_REAL64, self.opt)
+        self._bs = np.asarray(blk_size, dtype=np.int64)
+        self._rows = np.asarray(rowidx, dtype=np.int64)
+        self._col = np.repeat(np.arange(len(self._bs)), np.diff(np.asarray(colptr, dtype=np.int64)))
         self.info = dd_aux_get_info(self.h)
         self.device = device
         self.factor_buf = None
@@ -307,6 +355,23 @@ class AuxSolver:
         w = self._work(dd_aux_solve_work_bytes(self.h, nrhs))
         dd_aux_solve(self.h, self.factor_buf, self.vals, d_B, w, stream)
         return d_B
+
+    def assemble(self, cliques, d_S, S_offset, val_offset, d_vals=None, symmetrize=True, stream=None):
+        """f1: assemble the auxiliary matrix on the device from per-clique dense contributions.
+
+        cliques: list of ascending block-id lists; d_S: CUDA tensor holding every S_p (column-major,
+        ld = m_p) at element offsets S_offset; returns d_vals (allocated if None) in the layout
+        val_offset describes."""
+        torch = self.torch
+        ptr, blk = cliques_to_csr(cliques)
+        if d_vals is None:
+            nvals = int(max((int(val_offset[q]) + int(self._bs[self._rows[q]]) * int(self._bs[self._col[q]])
+                             for q in range(len(val_offset))), default=0))
+            d_vals = torch.empty(nvals, dtype=torch.complex128 if self.cplx else torch.float64, device=self.device)
+        w = torch.empty(max(256, dd_aux_assemble_work_bytes(self.h, ptr, blk)), dtype=torch.uint8, device=self.device)
+        dd_aux_assemble(self.h, ptr, blk, d_S, S_offset, val_offset, d_vals, w, symmetrize, stream)
+        self._asm_work = w  # kept alive until the next assembly (the launch is asynchronous)
+        return d_vals
 
     def pivots(self):
         return dd_aux_get_pivots(self.h, self.factor_buf, self.cplx)

@@ -79,6 +79,13 @@ struct LevelRanges {
 
 }  // namespace
 
+struct GraphCache {           // one instantiated CUDA graph + the pointer key it was captured for
+  cudaGraphExec_t exec = nullptr;
+  std::vector<uintptr_t> key;
+  int64_t dl[16] = {0};       // launches / flops the captured sequence accounts for per replay
+  double df[16] = {0};
+};
+
 struct dd_aux_handle_s {
   int dtype = DD_REAL64;
   bool cplx = false;
@@ -124,6 +131,13 @@ struct dd_aux_handle_s {
   bool lookahead = true;   // env DD_AUX_LOOKAHEAD=0 disables the side-stream overlap
   std::vector<cudaEvent_t> evA, evB;
   cudaEvent_t evLoad = nullptr;
+  // f1 assembly tables (host images kept alive for the async upload)
+  std::vector<AsmItem> asm_items;
+  std::vector<AsmContrib> asm_cons;
+  double asm_bytes = 0;
+  // CUDA graphs (options.use_graphs): factor level loop and whole solve, captured on `cap`
+  GraphCache gfactor, gsolve;
+  cudaStream_t cap = nullptr;
   // tracing
   bool trace = false;
   std::vector<cudaEvent_t> pool;
@@ -149,6 +163,9 @@ struct dd_aux_handle_s {
     for (auto e : evB) cudaEventDestroy(e);
     if (evLoad) cudaEventDestroy(evLoad);
     if (side) cudaStreamDestroy(side);
+    if (gfactor.exec) cudaGraphExecDestroy(gfactor.exec);
+    if (gsolve.exec) cudaGraphExecDestroy(gsolve.exec);
+    if (cap) cudaStreamDestroy(cap);
   }
 };
 
@@ -181,6 +198,56 @@ struct TraceScope {
     }
   }
 };
+
+// Enqueue fn(stream) directly, or (options.use_graphs, tracing off) replay a CUDA graph of it
+// captured once per pointer key on the handle's capture stream.  Launch
+// and flop counters advance by the captured sequence's counts on every replay.
+template <class Fn>
+int run_graph(dd_aux_handle_s* h, GraphCache& gc, const std::vector<uintptr_t>& key, Fn&& fn, cudaStream_t st) {
+  if (!h->opt.use_graphs || h->trace) return fn(st);
+  if (!gc.exec || gc.key != key) {
+    if (gc.exec) {
+      cudaGraphExecDestroy(gc.exec);
+      gc.exec = nullptr;
+    }
+    if (!h->cap) CUDA_TRY(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+    int64_t l0[16];
+    double f0[16];
+    for (int q = 0; q < 16; ++q) {
+      l0[q] = h->launches[q];
+      f0[q] = h->flops[q];
+    }
+    CUDA_TRY(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+    const int rc = fn(h->cap);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(h->cap, &g);
+    for (int q = 0; q < 16; ++q) {
+      gc.dl[q] = h->launches[q] - l0[q];
+      gc.df[q] = h->flops[q] - f0[q];
+      h->launches[q] = l0[q];
+      h->flops[q] = f0[q];
+    }
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      return rc;
+    }
+    if (e != cudaSuccess) return fail(DD_ERR_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e));
+    const cudaError_t ei = cudaGraphInstantiate(&gc.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) {
+      gc.exec = nullptr;
+      return fail(DD_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ei));
+    }
+    gc.key = key;
+  }
+  CUDA_TRY(cudaGraphLaunch(gc.exec, st));
+  for (int q = 0; q < 16; ++q) {
+    h->launches[q] += gc.dl[q];
+    h->flops[q] += gc.df[q];
+  }
+  return DD_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -769,119 +836,130 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   k1.e_off = h->e_off;
   k1.stats = (int64_t*)(F + h->off_stats);
   k1.nb = getenv("DD_AUX_K1NB") ? atoi(getenv("DD_AUX_K1NB")) : 0;
-  CUDA_TRY(cudaMemsetAsync(k1.ipiv, 0, (size_t)h->n_pad * 4, st));
-  RowpermArgs rp{(const RowPerm*)(F + h->off_rowperm), dnodes, arena, aim, k1.perm};
-  K2Args k2{(const Tile*)(F + h->off_k2items), (const Strip*)(F + h->off_strips), dnodes, arena, aim, work, wim,
-            k1.perm, k1.ipiv, h->d_off, h->e_off};
-  K3Args k3{(const UpdTarget*)(F + h->off_targets), (const int64_t*)(F + h->off_tiles), 0, 0,
-            (const UpdContrib*)(F + h->off_contribs), dnodes, arena, aim, work, wim};
-  const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
-  // ---- a2-a5: level-scheduled factorization with a one-level lookahead.
-  // Main stream st: K3a(l) [targets in panels of level l+1] -> K3b(l) [the rest].
-  // Side stream (high priority): K1 / rowperm / K2 of level l+1 as soon as K3a(l) is done, so
-  // the sequential diagonal factorizations overlap the bulk Schur update of level l.
-  // W is double-buffered by level parity (K2(l+1) writes while K3b(l) still reads W(l)).
-  const int nL = (int)h->lv.size();
+  int64_t* totals_d = (int64_t*)(F + h->off_totals);
+  const int nLv = (int)h->lv.size();
   if (!h->side) {
     int lo, hi;
     CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CUDA_TRY(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi));
     CUDA_TRY(cudaEventCreateWithFlags(&h->evLoad, cudaEventDisableTiming));
   }
-  while ((int)h->evA.size() < nL) {
+  while ((int)h->evA.size() < nLv) {
     cudaEvent_t a, b;
     CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
     h->evA.push_back(a);
     h->evB.push_back(b);
   }
-  cudaStream_t sd = h->lookahead ? h->side : st;
-  const size_t wpar = (size_t)h->nW * (C ? 2 : 1);  // elements per parity buffer
-  auto diag_phase = [&](int l) -> int {              // K1 + rowperm + K2 of level l on the side stream
-    const LevelRanges& R = h->lv[l];
-    h->cur_level = l;
-    k1.nodes = lvlnodes + R.n0;
-    {
-      TraceScope ts(h, DD_PH_K1, R.fl_k1, sd);
-      launch_k1(C, k1, R.n1 - R.n0, R.max_s, sd);
-    }
-    LAUNCH_CHECK("k1_diag_bk");
-    {
-      LinvArgs li{(const DTile*)(F + h->off_litems) + R.i0, dnodes, arena, aim};
-      double fl = 0;
-      for (int q = R.n0; q < R.n1; ++q) {
-        const double sv = h->nodes[((const int*)(h->blob.data.data() + h->off_lvlnodes))[q]].s;
-        fl += (C ? 4.0 : 1.0) * sv * sv * sv / 3.0;
+  // a2-a6 as one enqueue function of the stream, so it can be captured once into a CUDA graph
+  // (options.use_graphs; SURVEY.md §8(a) a5 "graph-capture the whole level sequence")
+  auto levels = [&](cudaStream_t st) -> int {
+    CUDA_TRY(cudaMemsetAsync(k1.ipiv, 0, (size_t)h->n_pad * 4, st));
+    RowpermArgs rp{(const RowPerm*)(F + h->off_rowperm), dnodes, arena, aim, k1.perm};
+    K2Args k2{(const Tile*)(F + h->off_k2items), (const Strip*)(F + h->off_strips), dnodes, arena, aim, work, wim,
+              k1.perm, k1.ipiv, h->d_off, h->e_off};
+    K3Args k3{(const UpdTarget*)(F + h->off_targets), (const int64_t*)(F + h->off_tiles), 0, 0,
+              (const UpdContrib*)(F + h->off_contribs), dnodes, arena, aim, work, wim};
+    const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
+    // ---- a2-a5: level-scheduled factorization with a one-level lookahead.
+    // Main stream st: K3a(l) [targets in panels of level l+1] -> K3b(l) [the rest].
+    // Side stream (high priority): K1 / rowperm / K2 of level l+1 as soon as K3a(l) is done, so
+    // the sequential diagonal factorizations overlap the bulk Schur update of level l.
+    // W is double-buffered by level parity (K2(l+1) writes while K3b(l) still reads W(l)).
+    const int nL = (int)h->lv.size();
+    cudaStream_t sd = h->lookahead ? h->side : st;
+    const size_t wpar = (size_t)h->nW * (C ? 2 : 1);  // elements per parity buffer
+    auto diag_phase = [&](int l) -> int {              // K1 + rowperm + K2 of level l on the side stream
+      const LevelRanges& R = h->lv[l];
+      h->cur_level = l;
+      k1.nodes = lvlnodes + R.n0;
+      {
+        TraceScope ts(h, DD_PH_K1, R.fl_k1, sd);
+        launch_k1(C, k1, R.n1 - R.n0, R.max_s, sd);
       }
-      TraceScope ts(h, DD_PH_LINV, fl, sd);
-      launch_linv(C, li, R.i1 - R.i0, sd);
-    }
-    LAUNCH_CHECK("k_linv");
-    RowpermArgs r = rp;
-    r.list = rp.list + R.r0;
-    if (R.r1 > R.r0) {
-      TraceScope ts(h, DD_PH_ROWPERM, 0.0, sd);
-      launch_rowperm(C, r, R.r1 - R.r0, h->max_s, sd);
-    }
-    LAUNCH_CHECK("k_rowperm");
-    K2Args a2 = k2;
-    a2.strips = k2.strips + R.s0;
-    a2.items = k2.items + R.k0;
-    a2.work = work + (l & 1) * wpar;
-    if (R.s1 > R.s0) {
-      TraceScope ts(h, DD_PH_K2, R.fl_k2, sd);
-      launch_k2(C, h->k3cfg, a2, R.k1 - R.k0, R.s1 - R.s0, sd);
-    }
-    LAUNCH_CHECK("k2_panel");
-    CUDA_TRY(cudaEventRecord(h->evB[l], sd));
-    return DD_OK;
-  };
-  CUDA_TRY(cudaEventRecord(h->evLoad, st));
-  CUDA_TRY(cudaStreamWaitEvent(sd, h->evLoad, 0));
-  if (nL > 0) {
-    int rc = diag_phase(0);
-    if (rc) return rc;
-  }
-  for (int l = 0; l < nL; ++l) {
-    const LevelRanges& R = h->lv[l];
-    h->cur_level = l;
-    CUDA_TRY(cudaStreamWaitEvent(st, h->evB[l], 0));
-    K3Args a3 = k3;
-    a3.work = work + (l & 1) * wpar;
-    a3.targets = k3.targets + R.t0;
-    a3.tprefix = k3.tprefix + R.t0;
-    a3.ntargets = R.ta - R.t0;
-    a3.tile0 = 0;
-    if (R.tiles_a > 0) {
-      TraceScope ts(h, DD_PH_K3, R.tiles_b > 0 ? 0.0 : R.fl_k3, st);
-      launch_k3(C, h->k3cfg, a3, (int)R.tiles_a, st);
-    }
-    LAUNCH_CHECK("k3_update");
-    CUDA_TRY(cudaEventRecord(h->evA[l], st));
-    if (l + 1 < nL) {
-      CUDA_TRY(cudaStreamWaitEvent(sd, h->evA[l], 0));
-      int rc = diag_phase(l + 1);
+      LAUNCH_CHECK("k1_diag_bk");
+      {
+        LinvArgs li{(const DTile*)(F + h->off_litems) + R.i0, dnodes, arena, aim};
+        double fl = 0;
+        for (int q = R.n0; q < R.n1; ++q) {
+          const double sv = h->nodes[((const int*)(h->blob.data.data() + h->off_lvlnodes))[q]].s;
+          fl += (C ? 4.0 : 1.0) * sv * sv * sv / 3.0;
+        }
+        TraceScope ts(h, DD_PH_LINV, fl, sd);
+        launch_linv(C, li, R.i1 - R.i0, sd);
+      }
+      LAUNCH_CHECK("k_linv");
+      RowpermArgs r = rp;
+      r.list = rp.list + R.r0;
+      if (R.r1 > R.r0) {
+        TraceScope ts(h, DD_PH_ROWPERM, 0.0, sd);
+        launch_rowperm(C, r, R.r1 - R.r0, h->max_s, sd);
+      }
+      LAUNCH_CHECK("k_rowperm");
+      K2Args a2 = k2;
+      a2.strips = k2.strips + R.s0;
+      a2.items = k2.items + R.k0;
+      a2.work = work + (l & 1) * wpar;
+      if (R.s1 > R.s0) {
+        TraceScope ts(h, DD_PH_K2, R.fl_k2, sd);
+        launch_k2(C, h->k3cfg, a2, R.k1 - R.k0, R.s1 - R.s0, sd);
+      }
+      LAUNCH_CHECK("k2_panel");
+      CUDA_TRY(cudaEventRecord(h->evB[l], sd));
+      return DD_OK;
+    };
+    CUDA_TRY(cudaEventRecord(h->evLoad, st));
+    CUDA_TRY(cudaStreamWaitEvent(sd, h->evLoad, 0));
+    if (nL > 0) {
+      int rc = diag_phase(0);
       if (rc) return rc;
     }
-    a3.targets = k3.targets + R.ta;
-    a3.tprefix = k3.tprefix + R.ta;
-    a3.ntargets = R.t1 - R.ta;
-    a3.tile0 = R.tiles_a;
-    h->cur_level = l;
-    if (R.tiles_b > 0) {
-      TraceScope ts(h, DD_PH_K3, R.fl_k3, st);
-      launch_k3(C, h->k3cfg, a3, (int)R.tiles_b, st);
+    for (int l = 0; l < nL; ++l) {
+      const LevelRanges& R = h->lv[l];
+      h->cur_level = l;
+      CUDA_TRY(cudaStreamWaitEvent(st, h->evB[l], 0));
+      K3Args a3 = k3;
+      a3.work = work + (l & 1) * wpar;
+      a3.targets = k3.targets + R.t0;
+      a3.tprefix = k3.tprefix + R.t0;
+      a3.ntargets = R.ta - R.t0;
+      a3.tile0 = 0;
+      if (R.tiles_a > 0) {
+        TraceScope ts(h, DD_PH_K3, R.tiles_b > 0 ? 0.0 : R.fl_k3, st);
+        launch_k3(C, h->k3cfg, a3, (int)R.tiles_a, st);
+      }
+      LAUNCH_CHECK("k3_update");
+      CUDA_TRY(cudaEventRecord(h->evA[l], st));
+      if (l + 1 < nL) {
+        CUDA_TRY(cudaStreamWaitEvent(sd, h->evA[l], 0));
+        int rc = diag_phase(l + 1);
+        if (rc) return rc;
+      }
+      a3.targets = k3.targets + R.ta;
+      a3.tprefix = k3.tprefix + R.ta;
+      a3.ntargets = R.t1 - R.ta;
+      a3.tile0 = R.tiles_a;
+      h->cur_level = l;
+      if (R.tiles_b > 0) {
+        TraceScope ts(h, DD_PH_K3, R.fl_k3, st);
+        launch_k3(C, h->k3cfg, a3, (int)R.tiles_b, st);
+      }
+      LAUNCH_CHECK("k3_update");
     }
-    LAUNCH_CHECK("k3_update");
-  }
-  h->cur_level = -1;
-  // ---- a6: statistics
-  int64_t* totals_d = (int64_t*)(F + h->off_totals);
+    h->cur_level = -1;
+    // ---- a6: statistics
+      {
+      TraceScope ts(h, DD_PH_STATS, 0.0, st);
+      launch_k4((const int64_t*)(F + h->off_stats), N, totals_d, st);
+    }
+    LAUNCH_CHECK("k4_stats");
+    return DD_OK;
+  };
   {
-    TraceScope ts(h, DD_PH_STATS, 0.0, st);
-    launch_k4((const int64_t*)(F + h->off_stats), N, totals_d, st);
+    const std::vector<uintptr_t> key = {(uintptr_t)d_factor, (uintptr_t)d_work};
+    int rc = run_graph(h, h->gfactor, key, levels, st);
+    if (rc) return rc;
   }
-  LAUNCH_CHECK("k4_stats");
   cudaEventRecord(e2, st);
   int64_t totals[16] = {0};
   CUDA_TRY(cudaMemcpyAsync(totals, totals_d, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -996,97 +1074,226 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
   const int refine = h->opt.refine_steps;
   if (refine > 0 && !d_vals) return fail(-3, "d_vals is NULL but refine_steps > 0");
   if (nrhs > (1 << 30)) return fail(-4, "nrhs too large");
-  cudaStream_t st = (cudaStream_t)stream;
-  const bool C = h->cplx;
-  const int planes = C ? 2 : 1;
-  const uint8_t* F = (const uint8_t*)d_factor;
-  uint8_t* Wb = (uint8_t*)d_work;
-  const int64_t ldy = pad8(h->n_pad);
-  double* y = (double*)Wb;
-  const int64_t yim = C ? ldy * nrhs : 0;
-  double* Bsave = (double*)(Wb + align256((size_t)ldy * nrhs * planes * sizeof(double)));
+  cudaStream_t st0 = (cudaStream_t)stream;
+  const bool in_graph = h->opt.use_graphs && !h->trace;
+  auto body = [&](cudaStream_t st) -> int {
+    const bool C = h->cplx;
+    const int planes = C ? 2 : 1;
+    const uint8_t* F = (const uint8_t*)d_factor;
+    uint8_t* Wb = (uint8_t*)d_work;
+    const int64_t ldy = pad8(h->n_pad);
+    double* y = (double*)Wb;
+    const int64_t yim = C ? ldy * nrhs : 0;
+    double* Bsave = (double*)(Wb + align256((size_t)ldy * nrhs * planes * sizeof(double)));
 
-  PermArgs pa{};
-  pa.gperm = (const int*)(F + h->off_gperm);
-  pa.nrows = h->n_pad;
-  pa.nrhs = (int)nrhs;
-  pa.y = y;
-  pa.yim = yim;
-  pa.ldy = ldy;
-  if (refine > 0) {
-    TraceScope ts(h, DD_PH_PERM, 0.0, st);
-    launch_copy(C, (const double*)d_B, ldb, Bsave, h->n, h->n, (int)nrhs, st);
-    LAUNCH_CHECK("k_copy");
-  }
-  pa.src = (const double*)d_B;
-  pa.lds = ldb;
-  {
-    TraceScope ts(h, DD_PH_PERM, 0.0, st);
-    launch_perm_in(C, pa, st);
-  }
-  LAUNCH_CHECK("k_perm_in");
-  double* berr_d = (double*)((uint8_t*)Bsave + align256((size_t)h->n * nrhs * planes * sizeof(double)));
-  int* flag_d = (int*)((uint8_t*)berr_d + align256((size_t)nrhs * sizeof(double)));
-  double* part = (double*)((uint8_t*)flag_d + 256);
-  double* Tbuf = (double*)((uint8_t*)part + align256(bupd_part_bytes(C, (int)nrhs)));
-  int rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf);
-  if (rc) return rc;
-  pa.dst = (double*)d_B;
-  pa.ldd = ldb;
-  pa.accumulate = 0;
-  {
-    TraceScope ts(h, DD_PH_PERM, 0.0, st);
-    launch_perm_out(C, pa, st);
-  }
-  LAUNCH_CHECK("k_perm_out");
-  const double tol = h->opt.refine_tol;
-  unsigned long long* norm_d = (unsigned long long*)(F + h->off_norm);
-  for (int r = 0; r < refine; ++r) {
-    SpmvArgs sa{};
-    sa.rows = (const SpRow*)(F + h->off_sprows);
-    sa.segs = (const SpSeg*)(F + h->off_spsegs);
-    sa.blk_size = (const int64_t*)(F + h->off_blksize);
-    sa.odof = (const int64_t*)(F + h->off_odof);
-    sa.vals = (const double*)d_vals;
-    sa.X = (const double*)d_B;
-    sa.ldx = ldb;
-    sa.Bsave = Bsave;
-    sa.ldb = h->n;
-    sa.ginv = (const int*)(F + h->off_ginv);
-    sa.y = y;
-    sa.yim = yim;
-    sa.ldy = ldy;
-    sa.nrhs = (int)nrhs;
+    PermArgs pa{};
+    pa.gperm = (const int*)(F + h->off_gperm);
+    pa.nrows = h->n_pad;
+    pa.nrhs = (int)nrhs;
+    pa.y = y;
+    pa.yim = yim;
+    pa.ldy = ldy;
+    if (refine > 0) {
+      TraceScope ts(h, DD_PH_PERM, 0.0, st);
+      launch_copy(C, (const double*)d_B, ldb, Bsave, h->n, h->n, (int)nrhs, st);
+      LAUNCH_CHECK("k_copy");
+    }
+    pa.src = (const double*)d_B;
+    pa.lds = ldb;
     {
-      TraceScope ts(h, DD_PH_SPMV, (C ? 8.0 : 2.0) * h->nnz_full * (double)nrhs, st);
-      launch_spmv(C, sa, h->n_sprows, st);
+      TraceScope ts(h, DD_PH_PERM, 0.0, st);
+      launch_perm_in(C, pa, st);
     }
-    LAUNCH_CHECK("k_spmv");
-    const int* flag = nullptr;
-    if (tol > 0) {  // adaptive: skip the correction on the device when every column is converged
-      if (!h->norm_valid) {
-        CUDA_TRY(cudaMemsetAsync(norm_d, 0, sizeof(unsigned long long), st));
-        launch_norm_a(C, sa, h->n_sprows, norm_d, st);
-        LAUNCH_CHECK("k_norm_a");
-        h->norm_valid = true;
-      }
-      CUDA_TRY(cudaMemsetAsync(flag_d, 0, sizeof(int), st));
-      launch_berr(C, y, yim, ldy, h->n_pad, (const double*)d_B, ldb, h->n, (int)nrhs, norm_d, tol, berr_d, flag_d, st);
-      LAUNCH_CHECK("k_berr");
-      flag = flag_d;
-    }
-    rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf, flag);
+    LAUNCH_CHECK("k_perm_in");
+    double* berr_d = (double*)((uint8_t*)Bsave + align256((size_t)h->n * nrhs * planes * sizeof(double)));
+    int* flag_d = (int*)((uint8_t*)berr_d + align256((size_t)nrhs * sizeof(double)));
+    double* part = (double*)((uint8_t*)flag_d + 256);
+    double* Tbuf = (double*)((uint8_t*)part + align256(bupd_part_bytes(C, (int)nrhs)));
+    int rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf);
     if (rc) return rc;
-    pa.accumulate = 1;
-    pa.flag = flag;
+    pa.dst = (double*)d_B;
+    pa.ldd = ldb;
+    pa.accumulate = 0;
     {
       TraceScope ts(h, DD_PH_PERM, 0.0, st);
       launch_perm_out(C, pa, st);
     }
     LAUNCH_CHECK("k_perm_out");
+    const double tol = h->opt.refine_tol;
+    unsigned long long* norm_d = (unsigned long long*)(F + h->off_norm);
+    for (int r = 0; r < refine; ++r) {
+      SpmvArgs sa{};
+      sa.rows = (const SpRow*)(F + h->off_sprows);
+      sa.segs = (const SpSeg*)(F + h->off_spsegs);
+      sa.blk_size = (const int64_t*)(F + h->off_blksize);
+      sa.odof = (const int64_t*)(F + h->off_odof);
+      sa.vals = (const double*)d_vals;
+      sa.X = (const double*)d_B;
+      sa.ldx = ldb;
+      sa.Bsave = Bsave;
+      sa.ldb = h->n;
+      sa.ginv = (const int*)(F + h->off_ginv);
+      sa.y = y;
+      sa.yim = yim;
+      sa.ldy = ldy;
+      sa.nrhs = (int)nrhs;
+      {
+        TraceScope ts(h, DD_PH_SPMV, (C ? 8.0 : 2.0) * h->nnz_full * (double)nrhs, st);
+        launch_spmv(C, sa, h->n_sprows, st);
+      }
+      LAUNCH_CHECK("k_spmv");
+      const int* flag = nullptr;
+      if (tol > 0) {  // adaptive: skip the correction on the device when every column is converged
+        if (!h->norm_valid || in_graph) {  // a replayed graph recomputes ||A|| (values may change)
+          CUDA_TRY(cudaMemsetAsync(norm_d, 0, sizeof(unsigned long long), st));
+          launch_norm_a(C, sa, h->n_sprows, norm_d, st);
+          LAUNCH_CHECK("k_norm_a");
+          h->norm_valid = !in_graph;
+        }
+        CUDA_TRY(cudaMemsetAsync(flag_d, 0, sizeof(int), st));
+        launch_berr(C, y, yim, ldy, h->n_pad, (const double*)d_B, ldb, h->n, (int)nrhs, norm_d, tol, berr_d, flag_d, st);
+        LAUNCH_CHECK("k_berr");
+        flag = flag_d;
+      }
+      rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf, flag);
+      if (rc) return rc;
+      pa.accumulate = 1;
+      pa.flag = flag;
+      {
+        TraceScope ts(h, DD_PH_PERM, 0.0, st);
+        launch_perm_out(C, pa, st);
+      }
+      LAUNCH_CHECK("k_perm_out");
+    }
+    return DD_OK;
+  };
+  double tolv = h->opt.refine_tol;
+  uint64_t tolbits;
+  std::memcpy(&tolbits, &tolv, 8);
+  const std::vector<uintptr_t> key = {(uintptr_t)d_factor, (uintptr_t)d_vals, (uintptr_t)nrhs, (uintptr_t)d_B,
+                                      (uintptr_t)ldb, (uintptr_t)d_work, (uintptr_t)refine, (uintptr_t)tolbits};
+  return run_graph(h, h->gsolve, key, body, st0);
+}
+
+}  // extern "C"
+
+// f1 tables: per output block (CSC order) its 32-column chunks, each with the contributor list
+// (cliques containing both interfaces, ascending clique index).  S_offset / val_offset may be
+// NULL for the size query (the offsets are then left zero).
+static int build_assembly(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, const int32_t* clq_blk,
+                          const int64_t* S_offset, const int64_t* val_offset, std::vector<AsmItem>& items,
+                          std::vector<AsmContrib>& cons) {
+  const int N = h->S.nblk;
+  if (nclq < 0) return fail(-2, "nclq must be >= 0");
+  if (nclq > 0 && (!clq_ptr || !clq_blk)) return fail(!clq_ptr ? -3 : -4, "clique arrays are NULL");
+  std::vector<std::vector<AsmContrib>> per(h->nnzb_in);
+  for (int64_t p = 0; p < nclq; ++p) {
+    const int64_t b0 = clq_ptr[p], b1 = clq_ptr[p + 1];
+    if (b1 < b0 || b0 < 0) return fail(-3, "clq_ptr is not non-decreasing");
+    std::vector<int64_t> off(b1 - b0 + 1, 0);
+    for (int64_t a = b0; a < b1; ++a) {
+      const int I = clq_blk[a];
+      if (I < 0 || I >= N) return fail(DD_ERR_PATTERN, "clique " + std::to_string(p) + ": block id out of range");
+      if (a > b0 && I <= clq_blk[a - 1])
+        return fail(DD_ERR_PATTERN, "clique " + std::to_string(p) + ": members not strictly ascending");
+      off[a - b0 + 1] = off[a - b0] + h->blk_size[I];
+    }
+    const int64_t m = off.back();
+    for (int64_t a = b0; a < b1; ++a)
+      for (int64_t b = b0; b <= a; ++b) {
+        const int I = clq_blk[a], J = clq_blk[b];  // I >= J
+        auto rb = h->rowidx.begin() + h->colptr[J], re = h->rowidx.begin() + h->colptr[J + 1];
+        auto itp = std::lower_bound(rb, re, I);
+        if (itp == re || *itp != I)
+          return fail(DD_ERR_PATTERN, "clique " + std::to_string(p) + ": block (" + std::to_string(I) + "," +
+                                          std::to_string(J) + ") is not in the pattern");
+        AsmContrib c{};
+        c.soff = S_offset ? S_offset[p] : 0;
+        c.ld = m;
+        c.ra = (int32_t)off[a - b0];
+        c.cb = (int32_t)off[b - b0];
+        per[itp - h->rowidx.begin()].push_back(c);
+      }
   }
+  const int CH = asm_chunk();
+  items.clear();
+  cons.clear();
+  for (int j = 0; j < N; ++j)
+    for (int64_t q = h->colptr[j]; q < h->colptr[j + 1]; ++q) {
+      const int i = h->rowidx[q];
+      const int k0 = (int)cons.size();
+      for (auto& c : per[q]) cons.push_back(c);
+      const int k1 = (int)cons.size();
+      for (int c0 = 0; c0 < h->blk_size[j]; c0 += CH) {
+        AsmItem it{};
+        it.dst = val_offset ? val_offset[q] : 0;
+        it.rows = (int32_t)h->blk_size[i];
+        it.cols = (int32_t)h->blk_size[j];
+        it.c0 = c0;
+        it.k0 = k0;
+        it.k1 = k1;
+        items.push_back(it);
+      }
+    }
   return DD_OK;
 }
+
+extern "C" {
+
+int dd_aux_assemble_work_bytes(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, const int32_t* clq_blk,
+                               size_t* bytes) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (!bytes) return fail(-5, "bytes is NULL");
+  std::vector<AsmItem> items;
+  std::vector<AsmContrib> cons;
+  int rc = build_assembly(h, nclq, clq_ptr, clq_blk, nullptr, nullptr, items, cons);
+  if (rc) return rc;
+  *bytes = align256(items.size() * sizeof(AsmItem)) + align256(cons.size() * sizeof(AsmContrib));
+  return DD_OK;
+}
+
+int dd_aux_assemble(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, const int32_t* clq_blk,
+                    const void* d_S, const int64_t* S_offset, int32_t symmetrize, const int64_t* val_offset,
+                    void* d_vals, void* d_work, void* stream) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (nclq > 0 && !d_S) return fail(-5, "d_S is NULL");
+  if (nclq > 0 && !S_offset) return fail(-6, "S_offset is NULL");
+  if (!val_offset) return fail(-8, "val_offset is NULL");
+  if (!d_vals) return fail(-9, "d_vals is NULL");
+  if (!d_work || ((uintptr_t)d_work & 255)) return fail(-10, "d_work is NULL or not 256-byte aligned");
+  std::vector<AsmItem> items;
+  std::vector<AsmContrib> cons;
+  int rc = build_assembly(h, nclq, clq_ptr, clq_blk, S_offset, val_offset, items, cons);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  // the host images live in the handle until the next call, so the async copies never race a free
+  h->asm_items.swap(items);
+  h->asm_cons.swap(cons);
+  uint8_t* W = (uint8_t*)d_work;
+  const size_t off_c = align256(h->asm_items.size() * sizeof(AsmItem));
+  if (!h->asm_items.empty())
+    CUDA_TRY(cudaMemcpyAsync(W, h->asm_items.data(), h->asm_items.size() * sizeof(AsmItem), cudaMemcpyHostToDevice, st));
+  if (!h->asm_cons.empty())
+    CUDA_TRY(cudaMemcpyAsync(W + off_c, h->asm_cons.data(), h->asm_cons.size() * sizeof(AsmContrib),
+                             cudaMemcpyHostToDevice, st));
+  AsmArgs a{(const AsmItem*)W, (const AsmContrib*)(W + off_c), (const double*)d_S, (double*)d_vals};
+  {
+    double bytes = 0;  // algorithmic traffic: contributions read (x2 with the symmetric part) + output written
+    const double es = h->cplx ? 16.0 : 8.0;
+    for (size_t q = 0; q < h->asm_items.size(); ++q) {
+      const AsmItem& it = h->asm_items[q];
+      const double cells = (double)it.rows * std::min(asm_chunk(), it.cols - it.c0);
+      bytes += cells * es * (1.0 + (symmetrize ? 2.0 : 1.0) * (it.k1 - it.k0));
+    }
+    h->asm_bytes = bytes;
+    TraceScope ts(h, DD_PH_ASSEMBLE, 0.0, st);
+    launch_assemble(h->cplx, symmetrize != 0, a, (int)h->asm_items.size(), st);
+  }
+  LAUNCH_CHECK("k_assemble");
+  return DD_OK;
+}
+
+double dd_aux_last_assemble_bytes(dd_aux_handle_t h) { return h ? h->asm_bytes : 0.0; }
 
 int dd_aux_set_refine(dd_aux_handle_t h, int32_t refine_steps, double refine_tol) {
   if (!h) return fail(-1, "handle is NULL");
@@ -1140,6 +1347,12 @@ int dd_aux_get_pivots(dd_aux_handle_t h, const void* d_factor, int32_t* ipiv, in
       }
     }
   }
+  return DD_OK;
+}
+
+int dd_aux_set_graphs(dd_aux_handle_t h, int32_t enable) {
+  if (!h) return fail(-1, "handle is NULL");
+  h->opt.use_graphs = enable != 0;
   return DD_OK;
 }
 

@@ -58,8 +58,13 @@ __device__ __forceinline__ double dneg(double x) {  // sign flip on the integer 
 // Cr = T1 - T2, Ci = T3 - T1 - T2: three real DMMA products instead of four.
 // FINE: per-16x8-sub-tile DMMA masking (one predicate per mma) vs coarse per-warp masking (a warp
 // whose whole warp tile is outside the valid region skips the stage; otherwise branch-free).
+// VEC (MK x NK only): vectorised fragment loads.  The mma's row slots g / g+8 of a 16-row sub-tile
+// map to tile rows 2g / 2g+1 and its column slot g of sub-tile b to tile column
+// 16*(b/2) + 2g + (b%2), so a thread's two A values and the B values of a sub-tile pair are
+// adjacent in shared memory: one 16-byte LDS each instead of two 8-byte ones (bank-conflict free
+// with the ld = 4 (mod 16) padding).  The accumulator mapping (for_each, masks) follows.
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool CPLX, bool A_KM, bool B_KN,
-          bool C3M = false, bool FINE = true>
+          bool C3M = false, bool FINE = true, bool VEC = false>
 struct Gemm {
   static constexpr int NTHR = WARPS_M * WARPS_N * 32;
   static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
@@ -73,6 +78,7 @@ struct Gemm {
   static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE * sizeof(double);
   static_assert(WTM % 16 == 0 && WTN % 8 == 0 && BK % 4 == 0, "tile shape");
   static_assert((A_LD % 16) == 4 && (B_LD % 16) == 4, "bank-conflict-free padding");
+  static_assert(!VEC || (!A_KM && !B_KN && NI % 2 == 0), "VEC needs MK x NK and an even NI");
 
   static_assert(!C3M || CPLX, "3M needs complex operands");
   struct Acc {
@@ -106,8 +112,8 @@ struct Gemm {
       for (int b = 0; b < NI; ++b)
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-          int row = wm * WTM + a * 16 + g + ((v >> 1) << 3);
-          int col = wn * WTN + b * 8 + 2 * tg + (v & 1);
+          int row = VEC ? wm * WTM + a * 16 + 2 * g + (v >> 1) : wm * WTM + a * 16 + g + ((v >> 1) << 3);
+          int col = VEC ? wn * WTN + (b >> 1) * 16 + 4 * tg + 2 * (v & 1) + (b & 1) : wn * WTN + b * 8 + 2 * tg + (v & 1);
           if constexpr (C3M) {
             const double t1 = acc.r[a][b][v], t2 = acc.i[a][b][v], t3 = acc.t[a][b][v];
             f(row, col, t1 - t2, t3 - t1 - t2);
@@ -134,7 +140,11 @@ struct Gemm {
     });
     __syncthreads();
     constexpr int PER = (BM * BN + NTHR - 1) / NTHR;
-    constexpr int BATCH = PER < 8 ? PER : 8;
+    // the accumulator registers are dead once staged, so a whole tile's loads fit in flight
+#ifndef DDK_EPI_BATCH
+#define DDK_EPI_BATCH 16
+#endif
+    constexpr int BATCH = PER < DDK_EPI_BATCH ? PER : DDK_EPI_BATCH;
 #pragma unroll 1
     for (int q0 = 0; q0 < PER; q0 += BATCH) {
       double old_r[BATCH], old_i[CPLX ? BATCH : 1];
@@ -162,6 +172,29 @@ struct Gemm {
       }
     }
     __syncthreads();
+  }
+
+  // Pull the C tile (valid region) into L2 ahead of the epilogue's read-modify-write: one
+  // prefetch per 128-byte line, issued at tile start so the epilogue's loads hit L2.
+  __device__ static void prefetch_tile_l2(const double* C, int64_t ldc, int64_t cim, int mlim, int nlim) {
+#ifndef DDK_PREFETCH_C
+#define DDK_PREFETCH_C 1
+#endif
+    if (!DDK_PREFETCH_C) return;
+    const int rows = mlim < BM ? mlim : BM, cols = nlim < BN ? nlim : BN;
+    if (rows <= 0 || cols <= 0) return;
+    const int lpc = (rows + 15) / 16;  // 128-byte lines per column (lines may straddle: +1 below)
+    const int nl = (lpc + 1) * cols * (CPLX ? 2 : 1);
+    for (int q = threadIdx.x; q < nl; q += NTHR) {
+      int x = q;
+      const int pl = CPLX ? (x % 2) : 0;
+      if (CPLX) x /= 2;
+      const int c = x / (lpc + 1), l = x % (lpc + 1);
+      const double* col = C + (int64_t)c * ldc + pl * cim;
+      const uintptr_t a0 = (uintptr_t)col & ~uintptr_t(127);
+      const uintptr_t a = a0 + (uintptr_t)l * 128;
+      if (a <= (uintptr_t)(col + rows - 1)) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
   }
 
   __device__ static void load_stage(double* st, const Seg& sg, int kofs, int m0, int n0, int M, int N,
@@ -233,7 +266,7 @@ struct Gemm {
     for (int a = 0; a < MI; ++a)
 #pragma unroll
       for (int b = 0; b < NI; ++b) {
-        const int r0 = wm * WTM + a * 16, c0 = wn * WTN + b * 8;
+        const int r0 = wm * WTM + a * 16, c0 = VEC ? wn * WTN + (b >> 1) * 16 + (b & 1) : wn * WTN + b * 8;
         bool on = r0 < mlim && c0 < nlim;
         if (diag_off != NO_DIAG && r0 + 15 < c0 + diag_off) on = false;
         if (on) m |= 1u << (a * NI + b);
@@ -256,24 +289,51 @@ struct Gemm {
       const int k = ks * 4 + tg;
       double ar[MI][2], br[NI];
       double ai[CPLX ? MI : 1][2], bi[CPLX ? NI : 1];
+      if constexpr (VEC) {
 #pragma unroll
-      for (int a = 0; a < MI; ++a) {
-        int m = wm * WTM + a * 16 + g;
-        int o0 = A_KM ? (m * A_LD + k) : (k * A_LD + m);
-        int o1 = A_KM ? ((m + 8) * A_LD + k) : (k * A_LD + m + 8);
-        ar[a][0] = As[o0];
-        ar[a][1] = As[o1];
-        if constexpr (CPLX) {
-          ai[a][0] = As[A_TILE + o0];
-          ai[a][1] = As[A_TILE + o1];
+        for (int a = 0; a < MI; ++a) {
+          const int o = k * A_LD + wm * WTM + a * 16 + 2 * g;
+          const double2 v = *reinterpret_cast<const double2*>(As + o);
+          ar[a][0] = v.x;
+          ar[a][1] = v.y;
+          if constexpr (CPLX) {
+            const double2 w = *reinterpret_cast<const double2*>(As + A_TILE + o);
+            ai[a][0] = w.x;
+            ai[a][1] = w.y;
+          }
         }
-      }
 #pragma unroll
-      for (int b = 0; b < NI; ++b) {
-        int n = wn * WTN + b * 8 + g;
-        int o = B_KN ? (n * B_LD + k) : (k * B_LD + n);
-        br[b] = Bs[o];
-        if constexpr (CPLX) bi[b] = Bs[B_TILE + o];
+        for (int p = 0; p < NI / 2; ++p) {
+          const int o = k * B_LD + wn * WTN + p * 16 + 2 * g;
+          const double2 v = *reinterpret_cast<const double2*>(Bs + o);
+          br[2 * p] = v.x;
+          br[2 * p + 1] = v.y;
+          if constexpr (CPLX) {
+            const double2 w = *reinterpret_cast<const double2*>(Bs + B_TILE + o);
+            bi[2 * p] = w.x;
+            bi[2 * p + 1] = w.y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int a = 0; a < MI; ++a) {
+          int m = wm * WTM + a * 16 + g;
+          int o0 = A_KM ? (m * A_LD + k) : (k * A_LD + m);
+          int o1 = A_KM ? ((m + 8) * A_LD + k) : (k * A_LD + m + 8);
+          ar[a][0] = As[o0];
+          ar[a][1] = As[o1];
+          if constexpr (CPLX) {
+            ai[a][0] = As[A_TILE + o0];
+            ai[a][1] = As[A_TILE + o1];
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < NI; ++b) {
+          int n = wn * WTN + b * 8 + g;
+          int o = B_KN ? (n * B_LD + k) : (k * B_LD + n);
+          br[b] = Bs[o];
+          if constexpr (CPLX) bi[b] = Bs[B_TILE + o];
+        }
       }
       // Issue order: every product class over all (a, b) before the next class, so two
       // DMMAs into the same accumulator are MI*NI instructions apart (no dependency stall).

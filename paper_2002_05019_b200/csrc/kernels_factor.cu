@@ -1046,6 +1046,27 @@ struct K3Cfg<true, 8> {  // complex 64x32 3M, coarse masking
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
 
+template <>
+struct K3Cfg<false, 9> {  // real 64x64, coarse masking, vectorised (16-byte) fragment loads
+  using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false, true>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
+};
+template <>
+struct K3Cfg<true, 9> {  // complex 64x32 3M, vectorised fragment loads
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, true, true>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
+};
+template <>
+struct K3Cfg<false, 10> {  // real 64x64, per-sub-tile masking, vectorised fragment loads
+  using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, true, true>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
+};
+template <>
+struct K3Cfg<true, 10> {  // complex 64x32 4M, coarse masking, vectorised fragment loads
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, false, false, true>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
+};
+
 template <bool C, int CFG>
 __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_update(K3Args a) {
   using Cf = K3Cfg<C, CFG>;
@@ -1083,7 +1104,7 @@ __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_upd
   typename G::Acc acc;
   G::zero(acc);
   const UpdContrib* cl = a.contribs + tg.c0;
-  auto segfn = [&](int q) {
+  auto gseg = [&](int q) {
     const UpdContrib u = cl[q];
     const NodeDev nk = a.nd[u.k];
     Seg sg;
@@ -1095,10 +1116,24 @@ __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_upd
     sg.K = nk.s;
     return sg;
   };
+  // the first K3_SEGC contributor descriptors are fetched once, in parallel, into shared memory
+  // (a segment switch inside the pipeline then costs no dependent global round trips)
+#ifndef DDK_SEGC
+#define DDK_SEGC 0
+#endif
+  constexpr int K3_SEGC = DDK_SEGC > 0 ? DDK_SEGC : 1;
+  __shared__ Seg segc[K3_SEGC];
+  const int ncon = tg.c1 - tg.c0;
+  if (DDK_SEGC > 0) {
+    if ((int)threadIdx.x < min(ncon, K3_SEGC)) segc[threadIdx.x] = gseg(threadIdx.x);
+    __syncthreads();
+  }
+  auto segfn = [&](int q) { return (DDK_SEGC > 0 && q < K3_SEGC) ? segc[q] : gseg(q); };
   const int mlim = tg.M - T.tm * BM, nlim = tg.N - T.tn * BN;
   const unsigned mask = G::tile_mask(mlim, nlim, tg.diag ? T.tn * BN - T.tm * BM : G::NO_DIAG);
-  G::run(segfn, tg.c1 - tg.c0, T.tm * BM, T.tn * BN, tg.M, tg.N, a.wim, a.aim, smem, acc, mask);
   double* Cb = a.arena + nj.panel + tg.ro + (int64_t)T.tm * BM + (int64_t)T.tn * BN * nj.ld;
+  G::prefetch_tile_l2(Cb, nj.ld, a.aim, mlim, nlim);
+  G::run(segfn, tg.c1 - tg.c0, T.tm * BM, T.tn * BN, tg.M, tg.N, a.wim, a.aim, smem, acc, mask);
   G::template store_tile<1>(acc, smem, Cb, nj.ld, a.aim, mlim, nlim);
 }
 
@@ -1291,6 +1326,8 @@ int k3_bm(bool cplx, int cfg) {
     case 6: return bm_of<6>(cplx);
     case 7: return bm_of<7>(cplx);
     case 8: return bm_of<8>(cplx);
+    case 9: return bm_of<9>(cplx);
+    case 10: return bm_of<10>(cplx);
     default: return bm_of<1>(cplx);
   }
 }
@@ -1304,6 +1341,8 @@ int k3_bn(bool cplx, int cfg) {
     case 6: return bn_of<6>(cplx);
     case 7: return bn_of<7>(cplx);
     case 8: return bn_of<8>(cplx);
+    case 9: return bn_of<9>(cplx);
+    case 10: return bn_of<10>(cplx);
     default: return bn_of<1>(cplx);
   }
 }
@@ -1332,6 +1371,8 @@ void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st)
     case 6: launch_k3_c<6>(cplx, a, ntiles, st); break;
     case 7: launch_k3_c<7>(cplx, a, ntiles, st); break;
     case 8: launch_k3_c<8>(cplx, a, ntiles, st); break;
+    case 9: launch_k3_c<9>(cplx, a, ntiles, st); break;
+    case 10: launch_k3_c<10>(cplx, a, ntiles, st); break;
     default: launch_k3_c<1>(cplx, a, ntiles, st); break;
   }
 }

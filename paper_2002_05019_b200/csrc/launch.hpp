@@ -126,6 +126,30 @@ struct SpmvArgs {
   int nrhs;
 };
 
+struct AsmItem {       // f1: one 32-column chunk of one output block (lower pattern, caller layout)
+  int64_t dst;         // element offset of the block in d_vals (column-major rows x cols, ld = rows)
+  int32_t rows, cols;  // s_I, s_J
+  int32_t c0;          // first column of the chunk
+  int32_t k0, k1;      // contributor range (ascending clique index)
+  int32_t pad;
+};
+
+struct AsmContrib {    // clique p's sub-block: S_p[ra + r, cb + c], S_p column-major with ld = m_p
+  int64_t soff;        // element offset of S_p in d_S
+  int64_t ld;
+  int32_t ra, cb;
+};
+
+struct AsmArgs {
+  const AsmItem* items;
+  const AsmContrib* con;
+  const double* S;     // interleaved complex or real
+  double* vals;
+};
+
+void launch_assemble(bool cplx, bool sym, const AsmArgs& a, int nitems, cudaStream_t st);
+int asm_chunk();
+
 void launch_load(bool cplx, const double* vals, const LoadBlock* lb, int nblocks, int64_t max_elems, double* arena,
                  int64_t aim, cudaStream_t st);
 size_t k1_smem(bool cplx, int max_s, int nb_req);

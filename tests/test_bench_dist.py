@@ -58,3 +58,49 @@ def test_reduce_max_gloo(tmp_path):
                        env=dict(os.environ, CUDA_VISIBLE_DEVICES=""))
     assert r.returncode == 0, r.stderr[-3000:]
     assert json.loads([l for l in r.stdout.splitlines() if l.startswith("[")][0]) == [2.0, 5.0, 2.0]
+
+
+_SHARD_WORKER = r"""
+import os, sys, json
+sys.path.insert(0, {root!r})
+import numpy as np
+import torch.distributed as dist
+import bench, dd_inputs, oracle
+dist.init_process_group("gloo")
+r, w = dist.get_rank(), dist.get_world_size()
+p = dd_inputs.config("cfg0")
+nb, per = 5, 3                                   # 5 RHS batches of 3 columns
+B = dd_inputs.random_rhs(p.n, nb * per, False, 4)
+F = oracle.block_factor(p, list(range(p.nblk)))  # every rank: its own factor replica
+mine = bench.rhs_shard(nb, w, r)
+part = {{b: oracle.refine_solve(p, F, np.asfortranarray(B[:, b * per:(b + 1) * per]), 1)[0] for b in mine}}
+got = [None] * w
+dist.all_gather_object(got, part)
+if r == 0:
+    X = np.zeros_like(B)
+    seen = []
+    for d in got:
+        for b, xb in d.items():
+            X[:, b * per:(b + 1) * per] = xb
+            seen.append(b)
+    Xref = oracle.refine_solve(p, F, B, 1)[0]
+    rel = float((np.abs(X - Xref).max(0) / np.abs(Xref).max(0)).max())
+    print(json.dumps({{"seen": sorted(seen), "rel": rel, "shards": [bench.rhs_shard(nb, w, q) for q in range(w)]}}))
+dist.barrier()
+dist.destroy_process_group()
+"""
+
+
+def test_rhs_sharded_solve_gloo(tmp_path):
+    """f4 host logic: the RHS-batch shards of the ranks partition the job exactly, and the
+    per-rank solves on factor replicas reassemble to the unsharded solution (columns independent)."""
+    w = tmp_path / "s.py"
+    w.write_text(_SHARD_WORKER.format(root=ROOT))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", str(w)]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, CUDA_VISIBLE_DEVICES=""))
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert d["seen"] == [0, 1, 2, 3, 4] and d["shards"] == [[0, 2, 4], [1, 3]]
+    assert d["rel"] <= 1e-12

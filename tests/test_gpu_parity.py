@@ -230,3 +230,42 @@ def test_complex_3m_parity():
     Xo, _, _ = oracle.refine_solve(p, F, B, 1)
     assert residual_berr(p, X, B).max() <= TOL_BERR
     assert rel_diff(X, Xo) <= TOL_REL
+
+
+@pytest.mark.parametrize("name,grid,sizes,tol", [("cfg1", (3, 3, 2), 40, 0.0), ("cfg3", (2, 2, 2), 24, 1e-14)])
+def test_cuda_graphs_bitwise_equal_direct(name, grid, sizes, tol):
+    """options.use_graphs (a5): the captured-and-replayed factor level loop and solve give the
+    bitwise result of direct launches, on first capture, on replay with new right-hand sides and
+    after a re-capture for a different buffer; refine_tol > 0 exercises the in-graph ||A||."""
+    import torch
+    import paper_2002_05019_b200 as dd
+    from tests._gpu import to_dev_colmajor
+    p = dd_inputs.config(name, grid=grid, sizes=sizes)
+    vals = torch.from_numpy(p.values).cuda()
+    outs = {}
+    for graphs in (False, True):
+        s = dd.AuxSolver(p.blk_size, p.colptr, p.rowidx, complex_=p.is_complex, use_graphs=graphs, refine_tol=tol)
+        res = []
+        for rep in range(2):
+            rc, fi = s.factor(vals, p.val_offset)
+            assert rc == dd.DD_OK
+            for seed in (0, 1):
+                B = random_rhs(p.n, 5, p.is_complex, seed)
+                Bd = to_dev_colmajor(B, torch)
+                s.solve_(Bd)
+                torch.cuda.synchronize()
+                res.append(Bd.cpu().numpy())
+        # a different right-hand-side buffer forces a re-capture of the solve graph
+        B = random_rhs(p.n, 3, p.is_complex, 2)
+        Bd = to_dev_colmajor(B, torch)
+        s.solve_(Bd)
+        torch.cuda.synchronize()
+        res.append(Bd.cpu().numpy())
+        tr = dd.dd_aux_get_trace(s.h, reset=True)
+        outs[graphs] = (res, sum(v["launches"] for v in tr.values()))
+        s.close()
+    for a, b in zip(outs[False][0], outs[True][0]):
+        assert np.array_equal(a, b)
+    assert outs[False][1] == outs[True][1]  # replayed graphs account for the same kernel launches
+    X = outs[True][0][-1]
+    assert residual_berr(p, X, random_rhs(p.n, 3, p.is_complex, 2)).max() <= TOL_BERR

@@ -24,7 +24,7 @@ def _lib():
 def test_header_symbols_exported():
     dd = _lib()
     hdr = open(os.path.join(ROOT, "include", "dd_aux.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|void|const char\*)\s+(dd_aux_\w+)\s*\(", hdr, re.M))
+    declared = set(re.findall(r"^\s*(?:int|void|double|const char\*)\s+(dd_aux_\w+)\s*\(", hdr, re.M))
     assert declared == set(dd.EXPORTED_SYMBOLS)
     so = ctypes.CDLL(dd.LIB_PATH)
     for name in declared:
@@ -123,3 +123,29 @@ def test_argument_errors():
     with pytest.raises(dd.DDAuxError):
         dd.dd_aux_default_options(user_order=[0, 0])  # not a permutation -> rejected at analyze
         dd.dd_aux_analyze([3, 3], [0, 1, 2], [0, 1], opt=dd.dd_aux_default_options(user_order=[0, 0]))
+
+
+def test_assemble_tables_host():
+    """f1 host logic: the assembly's descriptor tables are sized without a GPU and invalid
+    clique lists are rejected (DD_ERR_PATTERN) before anything is enqueued."""
+    dd = _lib()
+    p = dd_inputs.config("cfg0")
+    h = dd.dd_aux_analyze(p.blk_size, p.colptr, p.rowidx)
+    try:
+        cl = [c for _, c in p.cliques]
+        ptr, blk = dd.cliques_to_csr(cl)
+        nb = dd.dd_aux_assemble_work_bytes(h, ptr, blk)
+        # one 32-column chunk per block (s = 32) and one contributor per (clique, lower pair)
+        ncon = sum(len(c) * (len(c) + 1) // 2 for c in cl)
+        assert nb == (-(-p.nnzb * 32 // 256) * 256) + (-(-ncon * 24 // 256) * 256)
+        assert dd.dd_aux_assemble_work_bytes(h, *dd.cliques_to_csr([])) >= 0
+        for bad, rule in [([[1, 0]], "ascending"), ([[0, 9]], "range"), ([[0, 0]], "ascending")]:
+            with pytest.raises(dd.DDAuxError) as ei:
+                dd.dd_aux_assemble_work_bytes(h, *dd.cliques_to_csr(bad))
+            assert ei.value.code == dd.DD_ERR_PATTERN and rule in str(ei.value)
+        # cfg0 is a 4-cycle: interfaces 0 and 3 never share a subdomain, (3, 0) is not in the pattern
+        with pytest.raises(dd.DDAuxError) as ei:
+            dd.dd_aux_assemble_work_bytes(h, *dd.cliques_to_csr([[0, 3]]))
+        assert ei.value.code == dd.DD_ERR_PATTERN and "not in the pattern" in str(ei.value)
+    finally:
+        dd.dd_aux_destroy(h)
