@@ -78,6 +78,8 @@ class Problem:
 
     @property
     def is_complex(self) -> bool:
+        if self.values is None:  # clique form before assembly (build_clique_buffer)
+            return bool(getattr(self, "complex_", False))
         if isinstance(self.values, np.ndarray):
             return np.iscomplexobj(self.values)
         return bool(self.values.is_complex())  # torch tensor (device-resident values)
@@ -358,6 +360,7 @@ def build_clique_buffer(nx, ny, nz, sizes_fn, *, complex_=False, seed=0, topolog
     prob.pairs = pairs
     prob.grid = (nx, ny, nz)
     prob.total = total
+    prob.complex_ = bool(complex_)
     return prob, S, S_offset[:-1]
 
 

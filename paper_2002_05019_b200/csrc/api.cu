@@ -74,6 +74,7 @@ struct LevelRanges {
   int i0, i1;     // inverse work items (node, TB column tile)
   double fl_k1, fl_k2, fl_k3;      // algorithmic flops of the level's factor kernels
   int max_s;                       // largest diagonal block of the level
+  int max_rp;                      // largest padded struct-row count of the level's nodes
   double fl_diag, fl_upd;          // solve flops per rhs: one diagonal sweep / one update sweep
 };
 
@@ -449,8 +450,8 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
     const char* ev = getenv("DD_AUX_K3CFG");
     // default tile config per scalar type (measured on B200): real 64x64 at
     // 4 CTAs/SM with per-warp masking; complex 64x32, 2 stages, 4 CTAs/SM: 3M (Gauss) by default,
-    // 4M with per-warp masking when complex_3m = 0
-    h->k3cfg = ev ? atoi(ev) : (h->cplx ? (opt.complex_3m ? 6 : 7) : 7);
+    // 4M with per-warp masking when complex_3m = 0; all with 16-byte fragment loads (VEC)
+    h->k3cfg = ev ? atoi(ev) : (h->cplx ? (opt.complex_3m ? 9 : 10) : 12);
     h->m3 = h->cplx && opt.complex_3m;
     const char* la = getenv("DD_AUX_LOOKAHEAD");
     h->lookahead = la ? atoi(la) != 0 : true;
@@ -589,8 +590,10 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
       const double mu = h->cplx ? 4.0 : 1.0;
       R.fl_k1 = R.fl_k2 = R.fl_k3 = R.fl_diag = R.fl_upd = 0;
       R.max_s = 0;
+      R.max_rp = 0;
       for (int t : L) {
         R.max_s = std::max(R.max_s, (int)h->nodes[t].s);
+        R.max_rp = std::max(R.max_rp, (int)h->nodes[t].rp);
         double sv = h->nodes[t].s, rv = 0;
         for (int q = 0; q < h->nodes[t].nst; ++q) rv += h->nodes[st_pos[h->nodes[t].st0 + q]].s;
         R.fl_k1 += mu * sv * sv * sv / 3.0;
@@ -1045,7 +1048,7 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
     b.btiles = a.btiles + R.b0;
     if (R.b1 > R.b0) {
       TraceScope ts(h, DD_PH_BUPD, R.fl_upd * nrhs * fs, st);
-      launch_bupd(C, h->m3, b, R.b1 - R.b0, part, st);
+      launch_bupd(C, h->m3, b, R.b1 - R.b0, R.max_rp, part, st);
     }
     LAUNCH_CHECK("k_bupd");
     b.nodes = lvlnodes + R.n0;

@@ -64,7 +64,7 @@ __device__ __forceinline__ double dneg(double x) {  // sign flip on the integer 
 // adjacent in shared memory: one 16-byte LDS each instead of two 8-byte ones (bank-conflict free
 // with the ld = 4 (mod 16) padding).  The accumulator mapping (for_each, masks) follows.
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool CPLX, bool A_KM, bool B_KN,
-          bool C3M = false, bool FINE = true, bool VEC = false>
+          bool C3M = false, bool FINE = true, bool VEC = false, bool RECT = false>
 struct Gemm {
   static constexpr int NTHR = WARPS_M * WARPS_N * 32;
   static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
@@ -144,7 +144,8 @@ struct Gemm {
 #ifndef DDK_EPI_BATCH
 #define DDK_EPI_BATCH 16
 #endif
-    constexpr int BATCH = PER < DDK_EPI_BATCH ? PER : DDK_EPI_BATCH;
+    constexpr int EB = CPLX ? 8 : DDK_EPI_BATCH;  // complex: two planes in flight per element
+    constexpr int BATCH = PER < EB ? PER : EB;
 #pragma unroll 1
     for (int q0 = 0; q0 < PER; q0 += BATCH) {
       double old_r[BATCH], old_i[CPLX ? BATCH : 1];
@@ -258,9 +259,21 @@ struct Gemm {
   // col - row == diag_off (diagonal target blocks store only their lower triangle).  Masked
   // sub-tiles issue no DMMA, which the co-resident CTA's warps pick up.
   static constexpr int NO_DIAG = -(1 << 30);
+  // RECT: the valid part of a warp tile is a rectangle of whole 16-row groups x whole column
+  // groups (8 columns; 16 with VEC) -- code = 1 | na << 4 | ncg << 8, 0 = skip the warp tile
+  // (entirely outside, or strictly above a diagonal target's diagonal).
+  static constexpr int CG = VEC ? 16 : 8;    // columns per column group
+  static constexpr int NCG = WTN / CG;       // column groups per warp tile
   __device__ static unsigned tile_mask(int mlim, int nlim, int diag_off) {
     const int warp = threadIdx.x >> 5;
     const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+    if constexpr (RECT) {
+      const int r0 = wm * WTM, c0 = wn * WTN;
+      if (r0 >= mlim || c0 >= nlim) return 0u;
+      if (diag_off != NO_DIAG && r0 + WTM - 1 < c0 + diag_off) return 0u;
+      const int na = min(MI, (mlim - r0 + 15) / 16), ncg = min(NCG, (nlim - c0 + CG - 1) / CG);
+      return 1u | ((unsigned)na << 4) | ((unsigned)ncg << 8);
+    }
     unsigned m = 0;
 #pragma unroll
     for (int a = 0; a < MI; ++a)
@@ -274,11 +287,10 @@ struct Gemm {
     return m;
   }
 
-  __device__ static void compute_stage(const double* st, Acc& acc, unsigned mask = ~0u) {
-    if constexpr (!FINE) {
-      if (mask == 0u) return;  // warp-uniform
-      mask = ~0u;              // constant from here on: the per-mma predicates fold away
-    }
+  // Sub-tiles a < NA, b < NB of the warp tile; PRED: per-mma predicate from mask (FINE mode).
+  template <int NA, int NB, bool PRED>
+  __device__ static void compute_body(const double* st, Acc& acc, unsigned mask) {
+    if constexpr (!PRED) mask = ~0u;  // constant: the per-mma predicates fold away
     const double* As = st;
     const double* Bs = st + NPL * A_TILE;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -291,7 +303,7 @@ struct Gemm {
       double ai[CPLX ? MI : 1][2], bi[CPLX ? NI : 1];
       if constexpr (VEC) {
 #pragma unroll
-        for (int a = 0; a < MI; ++a) {
+        for (int a = 0; a < NA; ++a) {
           const int o = k * A_LD + wm * WTM + a * 16 + 2 * g;
           const double2 v = *reinterpret_cast<const double2*>(As + o);
           ar[a][0] = v.x;
@@ -303,7 +315,7 @@ struct Gemm {
           }
         }
 #pragma unroll
-        for (int p = 0; p < NI / 2; ++p) {
+        for (int p = 0; p < NB / 2; ++p) {
           const int o = k * B_LD + wn * WTN + p * 16 + 2 * g;
           const double2 v = *reinterpret_cast<const double2*>(Bs + o);
           br[2 * p] = v.x;
@@ -316,7 +328,7 @@ struct Gemm {
         }
       } else {
 #pragma unroll
-        for (int a = 0; a < MI; ++a) {
+        for (int a = 0; a < NA; ++a) {
           int m = wm * WTM + a * 16 + g;
           int o0 = A_KM ? (m * A_LD + k) : (k * A_LD + m);
           int o1 = A_KM ? ((m + 8) * A_LD + k) : (k * A_LD + m + 8);
@@ -328,7 +340,7 @@ struct Gemm {
           }
         }
 #pragma unroll
-        for (int b = 0; b < NI; ++b) {
+        for (int b = 0; b < NB; ++b) {
           int n = wn * WTN + b * 8 + g;
           int o = B_KN ? (n * B_LD + k) : (k * B_LD + n);
           br[b] = Bs[o];
@@ -340,57 +352,79 @@ struct Gemm {
       if constexpr (C3M) {
         double sa[MI][2], sb[NI];
 #pragma unroll
-        for (int a = 0; a < MI; ++a) {
+        for (int a = 0; a < NA; ++a) {
           sa[a][0] = ar[a][0] + ai[a][0];
           sa[a][1] = ar[a][1] + ai[a][1];
         }
 #pragma unroll
-        for (int b = 0; b < NI; ++b) sb[b] = br[b] + bi[b];
+        for (int b = 0; b < NB; ++b) sb[b] = br[b] + bi[b];
 #pragma unroll
-        for (int a = 0; a < MI; ++a)
+        for (int a = 0; a < NA; ++a)
 #pragma unroll
-          for (int b = 0; b < NI; ++b)
+          for (int b = 0; b < NB; ++b)
             if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.r[a][b], ar[a][0], ar[a][1], br[b]);
 #pragma unroll
-        for (int a = 0; a < MI; ++a)
+        for (int a = 0; a < NA; ++a)
 #pragma unroll
-          for (int b = 0; b < NI; ++b)
+          for (int b = 0; b < NB; ++b)
             if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.i[a][b], ai[a][0], ai[a][1], bi[b]);
 #pragma unroll
-        for (int a = 0; a < MI; ++a)
+        for (int a = 0; a < NA; ++a)
 #pragma unroll
-          for (int b = 0; b < NI; ++b)
+          for (int b = 0; b < NB; ++b)
             if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.t[a][b], sa[a][0], sa[a][1], sb[b]);
         continue;
       }
 #pragma unroll
-      for (int a = 0; a < MI; ++a)
+      for (int a = 0; a < NA; ++a)
 #pragma unroll
-        for (int b = 0; b < NI; ++b)
+        for (int b = 0; b < NB; ++b)
           if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.r[a][b], ar[a][0], ar[a][1], br[b]);
       if constexpr (CPLX) {
 #pragma unroll
-        for (int a = 0; a < MI; ++a)
+        for (int a = 0; a < NA; ++a)
 #pragma unroll
-          for (int b = 0; b < NI; ++b)
+          for (int b = 0; b < NB; ++b)
             if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.i[a][b], ar[a][0], ar[a][1], bi[b]);
         double nai[MI][2];
 #pragma unroll
-        for (int a = 0; a < MI; ++a) {
+        for (int a = 0; a < NA; ++a) {
           nai[a][0] = dneg(ai[a][0]);
           nai[a][1] = dneg(ai[a][1]);
         }
 #pragma unroll
-        for (int a = 0; a < MI; ++a)
+        for (int a = 0; a < NA; ++a)
 #pragma unroll
-          for (int b = 0; b < NI; ++b)
+          for (int b = 0; b < NB; ++b)
             if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.r[a][b], nai[a][0], nai[a][1], bi[b]);
 #pragma unroll
-        for (int a = 0; a < MI; ++a)
+        for (int a = 0; a < NA; ++a)
 #pragma unroll
-          for (int b = 0; b < NI; ++b)
+          for (int b = 0; b < NB; ++b)
             if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.i[a][b], ai[a][0], ai[a][1], br[b]);
       }
+    }
+  }
+
+  __device__ static void compute_stage(const double* st, Acc& acc, unsigned mask = ~0u) {
+    if constexpr (RECT) {
+      if (mask == 0u) return;  // warp-uniform
+      const int na = (mask >> 4) & 15, ncg = (mask >> 8) & 15;
+      constexpr int BPG = VEC ? 2 : 1;  // sub-tiles per column group
+      if (na == MI && ncg == NCG) return compute_body<MI, NI, false>(st, acc, ~0u);
+      if constexpr (MI >= 2) {
+        if (na == 1 && ncg == NCG) return compute_body<1, NI, false>(st, acc, ~0u);
+      }
+      if constexpr (NCG >= 2) {
+        if (na == MI && ncg == 1) return compute_body<MI, BPG, false>(st, acc, ~0u);
+        if (na == 1 && ncg == 1) return compute_body<1, BPG, false>(st, acc, ~0u);
+      }
+      return compute_body<MI, NI, false>(st, acc, ~0u);  // other shapes: full warp tile
+    } else if constexpr (!FINE) {
+      if (mask == 0u) return;  // warp-uniform
+      compute_body<MI, NI, false>(st, acc, ~0u);
+    } else {
+      compute_body<MI, NI, true>(st, acc, mask);
     }
   }
 

@@ -269,6 +269,21 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
     while (k < s) {
       const int kk = k - c0;
       if (!last_panel && kk >= NB - 1) break;
+      // prefetch column k+1 of A now (its latency hides behind this column's work); it is kept
+      // only if this step is a 1x1 pivot without interchange (which leaves column k+1 untouched)
+      constexpr bool PF = K1_MAXQ <= 4;
+      cz An[PF ? K1_MAXQ : 1];
+      const bool pf = PF && k + 1 < s && !(kk + 1 >= NB - 1 && !last_panel);
+      if constexpr (PF) {
+        if (pf) {
+#pragma unroll
+          for (int q = 0; q < K1_MAXQ; ++q) {
+            const int i = tid + q * NT1;
+            if (i >= k + 1 && i < s) An[q] = ld<C>(A, Ael(i, k + 1), aim);
+          }
+        }
+      }
+      bool swapped = false;
       // updated column k:  W(k:s, kk) = A(k:s, k) - Lp(k:s, 0:kk) W(k, 0:kk)^T  (W row k: window)
       double bv = -1.0;
       int bi = INT_MAX;
@@ -367,6 +382,7 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
       }
       const int kkk = k + kstep - 1;
       if (kp != kkk) {
+        swapped = true;
         __syncthreads();
         // move the non-updated column kkk of the trailing block to position kp (dlasyf)
         if (tid == 0) st<C>(A, Ael(kp, kp), aim, ld<C>(A, Ael(kkk, kkk), aim));
@@ -470,10 +486,15 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
       }
       k += kstep;
       if (k < s && !(kk + kstep >= NB - 1 && !last_panel)) {
+        if (PF && pf && kstep == 1 && !swapped) {
 #pragma unroll
-        for (int q = 0; q < K1_MAXQ; ++q) {
-          const int i = tid + q * NT1;
-          if (i >= k && i < s) Ak[q] = ld<C>(A, Ael(i, k), aim);
+          for (int q = 0; q < K1_MAXQ; ++q) Ak[q] = An[PF ? q : 0];
+        } else {
+#pragma unroll
+          for (int q = 0; q < K1_MAXQ; ++q) {
+            const int i = tid + q * NT1;
+            if (i >= k && i < s) Ak[q] = ld<C>(A, Ael(i, k), aim);
+          }
         }
       }
     }
@@ -1067,6 +1088,27 @@ struct K3Cfg<true, 10> {  // complex 64x32 4M, coarse masking, vectorised fragme
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
 
+template <>
+struct K3Cfg<false, 11> {  // real 64x64, VEC, rectangular 16x16-granular edge masking (RECT)
+  using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false, true, true>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
+};
+template <>
+struct K3Cfg<true, 11> {  // complex 64x32 3M, VEC, RECT
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, false, true, true>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
+};
+template <>
+struct K3Cfg<false, 12> {  // real 64x64, scalar fragments, RECT (16x8-granular)
+  using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false, false, true>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
+};
+template <>
+struct K3Cfg<true, 12> {  // complex 64x32 4M, VEC, RECT
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, false, false, true, true>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
+};
+
 template <bool C, int CFG>
 __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_update(K3Args a) {
   using Cf = K3Cfg<C, CFG>;
@@ -1328,6 +1370,8 @@ int k3_bm(bool cplx, int cfg) {
     case 8: return bm_of<8>(cplx);
     case 9: return bm_of<9>(cplx);
     case 10: return bm_of<10>(cplx);
+    case 11: return bm_of<11>(cplx);
+    case 12: return bm_of<12>(cplx);
     default: return bm_of<1>(cplx);
   }
 }
@@ -1343,6 +1387,8 @@ int k3_bn(bool cplx, int cfg) {
     case 8: return bn_of<8>(cplx);
     case 9: return bn_of<9>(cplx);
     case 10: return bn_of<10>(cplx);
+    case 11: return bn_of<11>(cplx);
+    case 12: return bn_of<12>(cplx);
     default: return bn_of<1>(cplx);
   }
 }
@@ -1373,6 +1419,8 @@ void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st)
     case 8: launch_k3_c<8>(cplx, a, ntiles, st); break;
     case 9: launch_k3_c<9>(cplx, a, ntiles, st); break;
     case 10: launch_k3_c<10>(cplx, a, ntiles, st); break;
+    case 11: launch_k3_c<11>(cplx, a, ntiles, st); break;
+    case 12: launch_k3_c<12>(cplx, a, ntiles, st); break;
     default: launch_k3_c<1>(cplx, a, ntiles, st); break;
   }
 }
@@ -1387,6 +1435,10 @@ static void launch_k2_t(const K2Args& a, int nitems, cudaStream_t st) {
 void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, cudaStream_t st) {
   if (nitems > 0) {
     switch (cfg) {  // same tile shapes as the Schur update
+      case 9: cplx ? launch_k2_t<true, 9>(a, nitems, st) : launch_k2_t<false, 9>(a, nitems, st); break;
+      case 10: cplx ? launch_k2_t<true, 10>(a, nitems, st) : launch_k2_t<false, 10>(a, nitems, st); break;
+      case 11: cplx ? launch_k2_t<true, 11>(a, nitems, st) : launch_k2_t<false, 11>(a, nitems, st); break;
+      case 12: cplx ? launch_k2_t<true, 12>(a, nitems, st) : launch_k2_t<false, 12>(a, nitems, st); break;
       case 6: cplx ? launch_k2_t<true, 6>(a, nitems, st) : launch_k2_t<false, 6>(a, nitems, st); break;
       case 5: cplx ? launch_k2_t<true, 5>(a, nitems, st) : launch_k2_t<false, 5>(a, nitems, st); break;
       case 4: cplx ? launch_k2_t<true, 4>(a, nitems, st) : launch_k2_t<false, 4>(a, nitems, st); break;

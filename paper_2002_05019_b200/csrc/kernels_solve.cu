@@ -26,7 +26,7 @@ namespace ddk {
 // Solve GEMM configurations: 64-row tiles; rhs tile 64 (real) / 32 (complex, so the 3M form's
 // three accumulator sets fit at 4 CTAs per SM).  Real: per-warp masking; complex: per-sub-tile.
 constexpr int SUBM = 64;
-constexpr int BUPD_MAX_PARTS = 320;  // split-K partial tiles of the backward update (workspace bound)
+constexpr int BUPD_MAX_PARTS = 1024;  // split-K partial tiles of the backward update (workspace bound)
 template <bool C>
 struct SolveN {
   static constexpr int value = C ? 32 : 64;
@@ -173,18 +173,33 @@ __global__ void __launch_bounds__(128) k_bupd(SolveArgs a, int G, double* part, 
   const int2 T = a.btiles[tile];  // (t, tm)
   const NodeDev nt = a.nd[T.x];
   const int n0 = blockIdx.y * SBN, m0 = T.y * SUBM;
-  const int q0 = (int)((int64_t)nt.nst * g / G), q1 = (int)((int64_t)nt.nst * (g + 1) / G);
+  // chunk g = padded struct rows [R0, R1) (even bounds: 16-byte cp.async chunks), split inside
+  // members so every chunk carries the same K; members qa..qb intersect it
+  const int R0 = (int)((int64_t)nt.rp * g / G) & ~1;
+  const int R1 = g == G - 1 ? nt.rp : ((int)((int64_t)nt.rp * (g + 1) / G) & ~1);
+  auto member_of = [&](int r) {  // last member q with (st_row[q] - sp) <= r
+    int lo = 0, hi = nt.nst - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.st_row[nt.st0 + mid] - nt.sp <= r) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  };
+  const int qa = R1 > R0 ? member_of(R0) : 0, qb = R1 > R0 ? member_of(R1 - 1) : -1;
   typename G_::Acc acc;
   G_::zero(acc);
   auto segfn = [&](int q) {
-    const int ipos = a.st_pos[nt.st0 + q0 + q];
-    const int ro = a.st_row[nt.st0 + q0 + q];
+    const int ipos = a.st_pos[nt.st0 + qa + q];
+    const int ro = a.st_row[nt.st0 + qa + q];
     const NodeDev ni = a.nd[ipos];
-    // A(m, k) = L_it(k, m) = panel_t[(ro + k) + m*ld]  (KM)
-    Seg sg{a.arena + nt.panel + ro, a.y + ni.ydof, nullptr, (int64_t)nt.ld, a.ldy, ni.s};
+    const int o = ro - nt.sp;
+    const int lo = max(0, R0 - o), hi = min(ni.s, R1 - o);
+    // A(m, k) = L_it(lo + k, m) = panel_t[(ro + lo + k) + m*ld]  (KM)
+    Seg sg{a.arena + nt.panel + ro + lo, a.y + ni.ydof + lo, nullptr, (int64_t)nt.ld, a.ldy, max(0, hi - lo)};
     return sg;
   };
-  G_::run(segfn, q1 - q0, m0, n0, nt.s, a.nrhs, a.aim, a.yim, smem, acc,
+  G_::run(segfn, qb - qa + 1, m0, n0, nt.s, a.nrhs, a.aim, a.yim, smem, acc,
           G_::tile_mask(nt.s - m0, a.nrhs - n0, G_::NO_DIAG));
   if (G == 1) {
     G_::template store_tile<1>(acc, smem, a.y + nt.ydof + m0 + (int64_t)n0 * a.ldy, a.ldy, a.yim, nt.s - m0,
@@ -624,13 +639,20 @@ void launch_fupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, cudaStream_
   else launch_g(k_fupd<true, false>, SolveG<true, false>::FU::SMEM_BYTES, grid, st, a);
 }
 
-int bupd_split(bool cplx, int ntiles, int nrhs) {
-  // enough CTAs for two per SM; partial buffer bounded by BUPD_MAX_PARTS tiles
-  const int ctas = ntiles * ntn(cplx, nrhs);
-  if (ctas >= 2 * 148) return 1;
-  int G = (2 * 148 + ctas - 1) / ctas;
+int bupd_split(bool cplx, int ntiles, int nrhs, int max_rp) {
+  // enough CTAs to fill every SM at the backward-update kernel's occupancy (3 CTAs/SM) counting
+  // one right-hand-side tile column, each chunk >= 128 rows of K; partial buffer bounded by
+  // BUPD_MAX_PARTS tiles.  Independent of nrhs, so a column's result does not depend on how many
+  // columns are solved together (bitwise).
+  (void)cplx;
+  (void)nrhs;
+  const int want = 3 * 148;
+  const int ctas = ntiles;
+  if (ctas >= want) return 1;
+  int G = (want + ctas - 1) / ctas;
+  G = std::min(G, std::max(1, max_rp / 128));
   G = std::min(G, std::max(1, BUPD_MAX_PARTS / std::max(ntiles, 1)));
-  return std::max(1, std::min(G, 16));
+  return std::max(1, std::min(G, 32));
 }
 
 template <bool C, bool M3>
@@ -641,9 +663,9 @@ static void bupd_t(const SolveArgs& a, int ntiles, int G, double* part, int64_t 
   k_bupd<C, M3><<<grid, 128, GB::SMEM_BYTES, st>>>(a, G, part, pim);
 }
 
-void launch_bupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, double* part, cudaStream_t st) {
+void launch_bupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, int max_rp, double* part, cudaStream_t st) {
   if (ntiles == 0 || a.nrhs == 0) return;
-  const int G = part ? bupd_split(cplx, ntiles, a.nrhs) : 1;
+  const int G = part ? bupd_split(cplx, ntiles, a.nrhs, max_rp) : 1;
   const int64_t pim = (int64_t)BUPD_MAX_PARTS * SUBM * a.nrhs;
   if (!cplx) bupd_t<false, false>(a, ntiles, G, part, pim, st);
   else if (m3) bupd_t<true, true>(a, ntiles, G, part, pim, st);

@@ -172,7 +172,8 @@ void launch_linv(bool cplx, const LinvArgs& a, int nitems, cudaStream_t st);
 void launch_diag_gemm(bool cplx, bool m3, bool backward, const SolveArgs& a, int ntiles, cudaStream_t st);
 void launch_fupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, cudaStream_t st);
 void launch_dsolve(bool cplx, const SolveArgs& a, cudaStream_t st);
-void launch_bupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, double* part, cudaStream_t st);
+// max_rp: largest padded struct-row count of the level's nodes (bounds the split-K factor)
+void launch_bupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, int max_rp, double* part, cudaStream_t st);
 size_t bupd_part_bytes(bool cplx, int nrhs);
 int spmv_bm();
 // ||A||_inf of the caller's original blocks (max row sum of moduli) -> *out (bits of a double)

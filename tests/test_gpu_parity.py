@@ -133,9 +133,9 @@ def test_multi_rhs_columns_bitwise_equal_single():
     import torch
     from tests._gpu import to_dev_colmajor
     p = dd_inputs.config("cfg1", grid=(2, 2, 2), sizes=70)
-    B = random_rhs(p.n, 9, False, 3)
+    B = random_rhs(p.n, 130, False, 3)   # three right-hand-side tiles of 64
     X, _, s = run_gpu(p, B, keep=True)
-    for j in (0, 4, 8):
+    for j in (0, 4, 8, 129):
         b = to_dev_colmajor(B[:, j:j + 1], torch)
         s.solve_(b)
         torch.cuda.synchronize()
