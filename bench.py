@@ -383,6 +383,25 @@ def gpu_arm(args, rank, world, local, dist):
                "solve_ms_per_1000_rhs": s_ms * 1000.0 / nrhs, "factor_ms": f_ms}
         del vh, bh, xh
 
+    # ---- a5 evidence: the same step replayed from CUDA graphs (options.use_graphs; tracing off, so
+    # outside the traced timed region above); reported for the small, launch-bound configs
+    graphs = None
+    if prob.n <= 100000:
+        dd.dd_aux_set_graphs(solver.h, True)
+        for _ in range(2):  # capture + one replay
+            step(mk())
+        torch.cuda.synchronize()
+        gev = [mk() for _ in range(K)]
+        for k in range(K):
+            step(gev[k])
+        torch.cuda.synchronize()
+        dd.dd_aux_set_graphs(solver.h, False)
+        g_fac = sum(e[0].elapsed_time(e[1]) for e in gev) / K
+        g_sol = sum(e[2].elapsed_time(e[3]) for e in gev) / K
+        graphs = {"factor_ms": g_fac, "solve_ms_per_batch": g_sol / max(1, len(my_batches)),
+                  "solve_ms_per_1000_rhs": g_sol * 1000.0 / (nrhs * max(1, len(my_batches))),
+                  "what": "same step with use_graphs=1 (factor level loop + solve replayed from CUDA graphs), "
+                          "untraced, after the timed region"}
     if rank != 0:
         return
     cpu = None
@@ -431,7 +450,7 @@ def gpu_arm(args, rank, world, local, dist):
                      if asm_ms > 0 else None, "peak_src": hbm_peak()[1],
                      "what": "f1: A = sum_p sym(S_p) over the cliques, read S_p blocks + write A (algorithmic bytes)"},
         "gpu_launches": launches,
-        "clocks": clk, "cpu_baseline": cpu, "e2e": e2e,
+        "clocks": clk, "cpu_baseline": cpu, "e2e": e2e, "graphs": graphs,
         "setup_s": {"generate": gen_s, "analyze": analyze_s},
     }
     if args.trace_out:

@@ -451,7 +451,7 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
     // default tile config per scalar type (measured on B200): real 64x64 at
     // 4 CTAs/SM with per-warp masking; complex 64x32, 2 stages, 4 CTAs/SM: 3M (Gauss) by default,
     // 4M with per-warp masking when complex_3m = 0; all with 16-byte fragment loads (VEC)
-    h->k3cfg = ev ? atoi(ev) : (h->cplx ? (opt.complex_3m ? 9 : 10) : 12);
+    h->k3cfg = ev ? atoi(ev) : (h->cplx ? (opt.complex_3m ? 9 : 10) : 13);
     h->m3 = h->cplx && opt.complex_3m;
     const char* la = getenv("DD_AUX_LOOKAHEAD");
     h->lookahead = la ? atoi(la) != 0 : true;

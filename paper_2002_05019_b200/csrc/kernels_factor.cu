@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
   __shared__ int s_swa[K1NB_MAX], s_swb[K1NB_MAX], s_nswp;
   __shared__ int s_kp, s_kstep, s_zero, s_imax;
   __shared__ double s_absakk2[2];  // parity-buffered: no barrier between a read and the next write
+  __shared__ double s_xw[2][4];    // register copies (wv, wv2) of the two interchanged rows
 
   const int t = a.nodes[blockIdx.x];
   const NodeDev nd = a.nd[t];
@@ -420,15 +421,27 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           s_swb[s_nswp] = kp;
           ++s_nswp;
         }
-        __threadfence_block();
-        __syncthreads();
-        // register copies of the two exchanged rows
+        // the owners of rows kkk and kp trade their register copies through shared memory (the
+        // barrier orders this CTA's shared and global accesses; no fence or global reload needed)
 #pragma unroll
         for (int q = 0; q < K1_MAXQ; ++q) {
           const int i = tid + q * NT1;
           if (i == kkk || i == kp) {
-            wv[q] = ld<C>(W, Wel(i, kk), wim);
-            if (kstep == 2) wv2[q] = ld<C>(W, Wel(i, kk + 1), wim);
+            double* x = s_xw[i == kkk ? 0 : 1];
+            x[0] = wv[q].r;
+            x[1] = wv[q].i;
+            x[2] = wv2[q].r;
+            x[3] = wv2[q].i;
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < K1_MAXQ; ++q) {
+          const int i = tid + q * NT1;
+          if (i == kkk || i == kp) {
+            const double* x = s_xw[i == kkk ? 1 : 0];
+            wv[q] = mk(x[0], x[1]);
+            if (kstep == 2) wv2[q] = mk(x[2], x[3]);
           }
         }
       }
@@ -1109,6 +1122,17 @@ struct K3Cfg<true, 12> {  // complex 64x32 4M, VEC, RECT
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
 
+template <>
+struct K3Cfg<false, 13> {  // real 64x64, RECT, 2 stages (34 KB smem; dense microbench +1.5% at K=576)
+  using G = Gemm<64, 64, 16, 2, 2, 2, false, false, false, false, false, false, true>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
+};
+template <>
+struct K3Cfg<true, 13> {  // complex 64x32 3M, 2 stages, coarse masking (no per-mma predicates)
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, false, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
+};
+
 template <bool C, int CFG>
 __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_update(K3Args a) {
   using Cf = K3Cfg<C, CFG>;
@@ -1320,7 +1344,16 @@ void launch_k1(bool cplx, const K1Args& a, int nnodes, int max_s, cudaStream_t s
     }
     return;
   }
-  if (max_s <= NT1 * 4) {
+  // rows per thread sized to the level's largest block: the per-row loops are unrolled over
+  // K1_MAXQ, so a tighter bound removes dead per-column work for small interfaces
+  static const int maxq_env = getenv("DD_AUX_K1MAXQ") ? atoi(getenv("DD_AUX_K1MAXQ")) : 0;
+  if (max_s <= NT1 && maxq_env != 4) {
+    if (cplx) launch_k1_t<true, 1>(a, nnodes, max_s, st);
+    else launch_k1_t<false, 1>(a, nnodes, max_s, st);
+  } else if (max_s <= NT1 * 2 && maxq_env != 4) {
+    if (cplx) launch_k1_t<true, 2>(a, nnodes, max_s, st);
+    else launch_k1_t<false, 2>(a, nnodes, max_s, st);
+  } else if (max_s <= NT1 * 4) {
     if (cplx) launch_k1_t<true, 4>(a, nnodes, max_s, st);
     else launch_k1_t<false, 4>(a, nnodes, max_s, st);
   } else {
@@ -1372,6 +1405,7 @@ int k3_bm(bool cplx, int cfg) {
     case 10: return bm_of<10>(cplx);
     case 11: return bm_of<11>(cplx);
     case 12: return bm_of<12>(cplx);
+    case 13: return bm_of<13>(cplx);
     default: return bm_of<1>(cplx);
   }
 }
@@ -1389,6 +1423,7 @@ int k3_bn(bool cplx, int cfg) {
     case 10: return bn_of<10>(cplx);
     case 11: return bn_of<11>(cplx);
     case 12: return bn_of<12>(cplx);
+    case 13: return bn_of<13>(cplx);
     default: return bn_of<1>(cplx);
   }
 }
@@ -1421,6 +1456,7 @@ void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st)
     case 10: launch_k3_c<10>(cplx, a, ntiles, st); break;
     case 11: launch_k3_c<11>(cplx, a, ntiles, st); break;
     case 12: launch_k3_c<12>(cplx, a, ntiles, st); break;
+    case 13: launch_k3_c<13>(cplx, a, ntiles, st); break;
     default: launch_k3_c<1>(cplx, a, ntiles, st); break;
   }
 }
@@ -1439,6 +1475,7 @@ void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, cud
       case 10: cplx ? launch_k2_t<true, 10>(a, nitems, st) : launch_k2_t<false, 10>(a, nitems, st); break;
       case 11: cplx ? launch_k2_t<true, 11>(a, nitems, st) : launch_k2_t<false, 11>(a, nitems, st); break;
       case 12: cplx ? launch_k2_t<true, 12>(a, nitems, st) : launch_k2_t<false, 12>(a, nitems, st); break;
+      case 13: cplx ? launch_k2_t<true, 13>(a, nitems, st) : launch_k2_t<false, 13>(a, nitems, st); break;
       case 6: cplx ? launch_k2_t<true, 6>(a, nitems, st) : launch_k2_t<false, 6>(a, nitems, st); break;
       case 5: cplx ? launch_k2_t<true, 5>(a, nitems, st) : launch_k2_t<false, 5>(a, nitems, st); break;
       case 4: cplx ? launch_k2_t<true, 4>(a, nitems, st) : launch_k2_t<false, 4>(a, nitems, st); break;
