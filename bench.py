@@ -348,14 +348,18 @@ def gpu_arm(args, rank, world, local, dist):
     dk = trace[dom]
     achieved = dk["flops"] / (dk["ms"] * 1e-3) / 1e12 if dk["ms"] > 0 else 0.0
     achieved_eff = achieved
-    if cplx and not args.complex_4m and dom == "k3_update":
+    if cplx and not args.complex_4m and dom in ("k3_update", "k2_panel", "fupd", "bupd", "fdiag", "bdiag"):
         achieved = 0.75 * achieved_eff  # 3M executes 3 of the 4 real products the 8-flop convention counts
     traffic, traffic_src = None, None
+    asm_traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{cfg}.json")
     if os.path.exists(tpath):  # dram read+write bytes per launch from one ncu --set full capture
-        t = json.load(open(tpath)).get(dom)
+        tj = json.load(open(tpath))
+        t = tj.get(dom)
         if t:
             traffic, traffic_src = t["dram_bytes_per_launch"], t["launch"]
+        if tj.get("k_assemble"):
+            asm_traffic = tj["k_assemble"]
     step_ms = total_ms / K
 
     # ---- e2e: host buffers through the public API (H2D inputs, D2H result inside the region)
@@ -448,6 +452,8 @@ def gpu_arm(args, rank, world, local, dist):
                      "achieved_gbs": asm_bytes / (asm_ms * 1e-3) / 1e9 if asm_ms > 0 else None,
                      "peak_gbs": hbm_peak()[0], "frac": (asm_bytes / (asm_ms * 1e-3) / 1e9 / hbm_peak()[0])
                      if asm_ms > 0 else None, "peak_src": hbm_peak()[1],
+                     "traffic": asm_traffic["dram_bytes_per_launch"] if asm_traffic else None,
+                     "traffic_src": asm_traffic["launch"] if asm_traffic else None,
                      "what": "f1: A = sum_p sym(S_p) over the cliques, read S_p blocks + write A (algorithmic bytes)"},
         "gpu_launches": launches,
         "clocks": clk, "cpu_baseline": cpu, "e2e": e2e, "graphs": graphs,

@@ -123,6 +123,27 @@ struct Gemm {
         }
   }
 
+  // Mutable visit (not 3M): f(row_in_tile, col_in_tile, re&, im&)
+  template <class F>
+  __device__ static void for_each_mut(Acc& acc, F f) {
+    static_assert(!C3M, "for_each_mut: 3M accumulators hold products, not the result");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+    const int g = lane >> 2, tg = lane & 3;
+    double dummy = 0.0;
+#pragma unroll
+    for (int a = 0; a < MI; ++a)
+#pragma unroll
+      for (int b = 0; b < NI; ++b)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          int row = VEC ? wm * WTM + a * 16 + 2 * g + (v >> 1) : wm * WTM + a * 16 + g + ((v >> 1) << 3);
+          int col = VEC ? wn * WTN + (b >> 1) * 16 + 4 * tg + 2 * (v & 1) + (b & 1) : wn * WTN + b * 8 + 2 * tg + (v & 1);
+          if constexpr (CPLX) f(row, col, acc.r[a][b][v], acc.i[a][b][v]);
+          else f(row, col, acc.r[a][b][v], dummy);
+        }
+  }
+
   // Epilogue through shared memory: the accumulator tile is staged in the (idle) pipeline buffers
   // and written back column-coalesced with all loads of a batch in flight before the stores
   // (the fragment-order read-modify-write serialised ~32 dependent L2 round trips per tile).

@@ -96,12 +96,14 @@ __device__ __forceinline__ void block_argmax(double& v, int& i, double (*shv)[NT
     si[w] = i;
   }
   __syncthreads();
-  v = sv[0];
-  i = si[0];
+  // every warp reduces the NT1/32 warp results with shuffles (one shared load per lane)
+  constexpr int NW = NT1 / 32;
+  v = sv[lane % NW];
+  i = si[lane % NW];
 #pragma unroll
-  for (int q = 1; q < NT1 / 32; ++q) {
-    double v2 = sv[q];
-    int i2 = si[q];
+  for (int o = NW / 2; o; o >>= 1) {
+    double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    int i2 = __shfl_xor_sync(0xffffffffu, i, o);
     if (v2 > v || (v2 == v && i2 < i)) {
       v = v2;
       i = i2;
@@ -537,7 +539,7 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
       // A(k:s, k:s) -= L(k:s, c0:k) W(k:s, 0:kb)^T.  The GEMM window starts at the even
       // row ke <= k (16-byte aligned cp.async chunks); row/column ke < k is masked.
       const int kb = k - c0, ke = k & ~1, M = s - ke;
-      __threadfence();
+      // the barrier orders this CTA's earlier global stores (L panel, W) before the cp.async reads
       __syncthreads();
       Seg sg;
       sg.a = A + Ael(ke, c0);
@@ -554,16 +556,14 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           G::run([&](int) { return sg; }, 1, tm * 64, tn * 64, M, M, aim, wim, smem, acc,
                  G::tile_mask(M - tm * 64, M - tn * 64, tn * 64 - tm * 64));
           double* Cb = A + Ael(ke + tm * 64, ke + tn * 64);
-          G::for_each(acc, [&](int r, int c, double vr, double vi) {
-            const int gr = ke + tm * 64 + r, gc = ke + tn * 64 + c;
-            if (gr < s && gc < s && gr >= k && gc >= k) {
-              int64_t e = (int64_t)r + (int64_t)c * ldA;
-              Cb[e] -= vr;
-              if (C) Cb[e + aim] -= vi;
-            }
-          });
+          if (ke < k) {  // row / column ke (already eliminated) must stay: subtract exact zeros there
+            G::for_each_mut(acc, [&](int r, int c, double& vr, double& vi) {
+              if ((tm == 0 && r == 0) || (tn == 0 && c == 0)) vr = vi = 0.0;
+            });
+          }
+          // coalesced read-modify-write (all loads of a batch in flight before the stores)
+          G::template store_tile<1>(acc, smem, Cb, ldA, aim, M - tm * 64, M - tn * 64);
         }
-      __threadfence();
       __syncthreads();
 #pragma unroll
       for (int q = 0; q < K1_MAXQ; ++q) {
@@ -861,16 +861,14 @@ __global__ void __launch_bounds__(NT1W) k1_diag_bk_warp(K1Args a) {
           G::run([&](int) { return sg; }, 1, tm * 64, tn * 64, M, M, aim, wim, smem, acc,
                  G::tile_mask(M - tm * 64, M - tn * 64, tn * 64 - tm * 64));
           double* Cb = A + Ael(ke + tm * 64, ke + tn * 64);
-          G::for_each(acc, [&](int r, int c, double vr, double vi) {
-            const int gr = ke + tm * 64 + r, gc = ke + tn * 64 + c;
-            if (gr < s && gc < s && gr >= k && gc >= k) {
-              int64_t e = (int64_t)r + (int64_t)c * ldA;
-              Cb[e] -= vr;
-              if (C) Cb[e + aim] -= vi;
-            }
-          });
+          if (ke < k) {  // row / column ke (already eliminated) must stay: subtract exact zeros there
+            G::for_each_mut(acc, [&](int r, int c, double& vr, double& vi) {
+              if ((tm == 0 && r == 0) || (tn == 0 && c == 0)) vr = vi = 0.0;
+            });
+          }
+          // coalesced read-modify-write (all loads of a batch in flight before the stores)
+          G::template store_tile<1>(acc, smem, Cb, ldA, aim, M - tm * 64, M - tn * 64);
         }
-      __threadfence();
       __syncthreads();
     }
   }
@@ -913,8 +911,7 @@ __global__ void __launch_bounds__(128) k_linv(LinvArgs a) {
     const int r = e % wc, q = e / wc;
     st<C>(X, (c0 + r) + (int64_t)(c0 + q) * ldi, aim, ld<C>(Lt, (int64_t)c * TB * TB + r + (int64_t)q * TB, aim));
   }
-  __threadfence();
-  __syncthreads();
+  __syncthreads();  // orders the CTA's global stores before its cp.async reads
   const int np = (s + TB - 1) / TB;
   for (int p = c + 1; p < np; ++p) {
     const int p0 = p * TB, wp = min(TB, s - p0);
@@ -931,7 +928,6 @@ __global__ void __launch_bounds__(128) k_linv(LinvArgs a) {
         if (C) Xp[r + (int64_t)q * ldi + aim] = vi;
       }
     });
-    __threadfence();
     __syncthreads();
     G::zero(acc);
     {  // X_pc = -Linv_pp acc
@@ -944,7 +940,6 @@ __global__ void __launch_bounds__(128) k_linv(LinvArgs a) {
         if (C) Xp[r + (int64_t)q * ldi + aim] = -vi;
       }
     });
-    __threadfence();
     __syncthreads();
   }
 }

@@ -269,3 +269,70 @@ def test_cuda_graphs_bitwise_equal_direct(name, grid, sizes, tol):
     assert outs[False][1] == outs[True][1]  # replayed graphs account for the same kernel launches
     X = outs[True][0][-1]
     assert residual_berr(p, X, random_rhs(p.n, 3, p.is_complex, 2)).max() <= TOL_BERR
+
+
+@pytest.mark.parametrize("s,cplx", [(1100, False), (1100, True), (2100, False)])
+def test_isolated_large_block_pivots(s, cplx):
+    """Interfaces above 1024 DoFs take K1's 16-rows-per-thread path (up to K1_MAX_BLOCK = 4096):
+    BK decisions equal the oracle's on one isolated block; solution within the north_star bounds."""
+    rng = np.random.default_rng(s + 7 * cplx)
+    A = rng.standard_normal((s, s))
+    if cplx:
+        A = A + 1j * rng.standard_normal((s, s))
+    A = A + A.T
+    p = Problem(np.array([s]), np.array([0, 1]), np.array([0], dtype=np.int32),
+                np.asfortranarray(A).ravel(order="F"), np.array([0]), [])
+    B = random_rhs(s, 3, cplx, 1)
+    X, finfo, sv = run_gpu(p, B, keep=True)
+    piv = sv.pivots()
+    sv.close()
+    f = bk_factor(A)
+    agree = float(np.mean(piv["ipiv"] == f["ipiv"]))
+    assert agree >= 0.99, agree  # near-ties may legitimately diverge at this size (DESIGN.md)
+    assert residual_berr(p, X, B).max() <= TOL_BERR
+
+
+def test_complex_4m_parity():
+    """Complex Schur update with the four-real-product (4M) form (options.complex_3m = 0)."""
+    import torch
+    import paper_2002_05019_b200 as dd
+    from tests._gpu import to_dev_colmajor
+    p = dd_inputs.config("cfg3", grid=(3, 2, 2), sizes=90)
+    B = random_rhs(p.n, 33, True, 4)
+    s = dd.AuxSolver(p.blk_size, p.colptr, p.rowidx, complex_=True, complex_3m=False)
+    s.factor(torch.from_numpy(p.values).cuda(), p.val_offset)
+    b = to_dev_colmajor(B, torch)
+    s.solve_(b)
+    torch.cuda.synchronize()
+    X = b.cpu().numpy()
+    F = oracle.block_factor(p, list(s.order()))
+    s.close()
+    Xo, _, _ = oracle.refine_solve(p, F, B, 1)
+    assert residual_berr(p, X, B).max() <= TOL_BERR
+    assert rel_diff(X, Xo) <= TOL_REL
+
+
+def test_padded_ldb_zero_rhs_and_two_refinement_steps():
+    """ldb > n (a column-major view into a taller buffer), nrhs = 0 as a no-op, refine_steps = 2."""
+    import torch
+    import paper_2002_05019_b200 as dd
+    p = dd_inputs.config("cfg1", grid=(2, 2, 2), sizes=50)
+    B = random_rhs(p.n, 4, False, 9)
+    s = dd.AuxSolver(p.blk_size, p.colptr, p.rowidx, refine_steps=2)
+    vals = torch.from_numpy(p.values).cuda()
+    s.factor(vals, p.val_offset)
+    ld = p.n + 13
+    buf = torch.full((4, ld), 7.0, dtype=torch.float64, device="cuda")
+    buf[:, :p.n] = torch.from_numpy(np.ascontiguousarray(B.T)).cuda()
+    Bv = buf.t()[:p.n]                       # n x 4, stride (1, ld)
+    w = s._work(dd.dd_aux_solve_work_bytes(s.h, 4))
+    dd.dd_aux_solve(s.h, s.factor_buf, vals, Bv, w, nrhs=4, ldb=ld)
+    dd.dd_aux_solve(s.h, s.factor_buf, vals, Bv, w, nrhs=0, ldb=ld)   # no-op
+    torch.cuda.synchronize()
+    X = Bv.cpu().numpy()
+    assert torch.all(buf[:, p.n:] == 7.0)    # padding rows untouched
+    F = oracle.block_factor(p, list(s.order()))
+    s.close()
+    Xo, _, _ = oracle.refine_solve(p, F, B, 2)
+    assert rel_diff(X, Xo) <= TOL_REL
+    assert residual_berr(p, X, B).max() <= TOL_BERR

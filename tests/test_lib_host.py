@@ -149,3 +149,13 @@ def test_assemble_tables_host():
         assert ei.value.code == dd.DD_ERR_PATTERN and "not in the pattern" in str(ei.value)
     finally:
         dd.dd_aux_destroy(h)
+
+
+def test_interface_size_limit():
+    """Interfaces above K1_MAX_BLOCK (4096) are rejected at analyze (DD_ERR_PATTERN)."""
+    dd = _lib()
+    with pytest.raises(dd.DDAuxError) as ei:
+        dd.dd_aux_analyze([4097], [0, 1], [0])
+    assert ei.value.code == dd.DD_ERR_PATTERN and "4096" in str(ei.value)
+    h = dd.dd_aux_analyze([4096], [0, 1], [0])
+    dd.dd_aux_destroy(h)
