@@ -66,8 +66,10 @@ struct LevelRanges {
   int k0, k1;     // K2 GEMM tiles
   int r0, r1;     // rowperm entries
   int t0, t1;     // K3 targets: [t0, ta) update the next level's panels, [ta, t1) the rest
-  int ta;
+  int ta, ta1;               // [t0, ta1): diagonal blocks of the next level's nodes (K3a1), [ta1, ta): the
+                             // rest of their panels (K3a2)
   int64_t tiles_a, tiles_b;  // implicit tile counts of the two parts
+  int64_t tiles_a1;          // tiles of K3a1
   int f0, f1;     // forward-solve tiles
   int b0, b1;     // backward-solve tiles
   int d0, d1;     // diagonal-solve tiles (node, 64-row tile)
@@ -130,7 +132,7 @@ struct dd_aux_handle_s {
   bool m3 = false;         // complex products in the 3M form (options.complex_3m)
   int k3cfg = 1;           // K3 tile configuration (env DD_AUX_K3CFG, read at analyze)
   bool lookahead = true;   // env DD_AUX_LOOKAHEAD=0 disables the side-stream overlap
-  std::vector<cudaEvent_t> evA, evB;
+  std::vector<cudaEvent_t> evA, evA2, evB;
   cudaEvent_t evLoad = nullptr;
   // f1 assembly tables (host images kept alive for the async upload)
   std::vector<AsmItem> asm_items;
@@ -162,6 +164,7 @@ struct dd_aux_handle_s {
     for (auto e : pool) cudaEventDestroy(e);
     for (auto e : evA) cudaEventDestroy(e);
     for (auto e : evB) cudaEventDestroy(e);
+    for (auto e : evA2) cudaEventDestroy(e);
     if (evLoad) cudaEventDestroy(evLoad);
     if (side) cudaStreamDestroy(side);
     if (gfactor.exec) cudaGraphExecDestroy(gfactor.exec);
@@ -510,15 +513,18 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
     std::vector<char> next(N, 0);
     if (l + 1 < S.nlevels)
       for (int t : S.level_nodes[l + 1]) next[t] = 1;
-    std::vector<std::pair<int64_t, int>> cost_a, cost_b;
+    // (K1 of level l+1 waits for K3a1 only: every update of a diagonal block is a (t, t) target)
+    std::vector<std::pair<int64_t, int>> cost_a1, cost_a, cost_b;
     for (size_t id = 0; id < tij.size(); ++id) {
       int64_t kcost = 0;
       for (auto& c : tcon[id]) kcost += h->nodes[c.k].s;
-      (next[tij[id].second] ? cost_a : cost_b).push_back({kcost, (int)id});
+      if (next[tij[id].second] && tij[id].first == tij[id].second) cost_a1.push_back({kcost, (int)id});
+      else (next[tij[id].second] ? cost_a : cost_b).push_back({kcost, (int)id});
     }
     auto bycost = [](const std::pair<int64_t, int>& x, const std::pair<int64_t, int>& y) {
       return x.first != y.first ? x.first > y.first : x.second < y.second;
     };
+    std::sort(cost_a1.begin(), cost_a1.end(), bycost);
     std::sort(cost_a.begin(), cost_a.end(), bycost);
     std::sort(cost_b.begin(), cost_b.end(), bycost);
     R.t0 = (int)targets.size();
@@ -542,6 +548,9 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
       tiles_lvl += nt;
       targets.push_back(tg);
     };
+    for (auto& cp : cost_a1) emit(cp);
+    R.ta1 = (int)targets.size();
+    R.tiles_a1 = tiles_lvl;
     for (auto& cp : cost_a) emit(cp);
     R.ta = (int)targets.size();
     R.tiles_a = tiles_lvl;
@@ -848,10 +857,12 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     CUDA_TRY(cudaEventCreateWithFlags(&h->evLoad, cudaEventDisableTiming));
   }
   while ((int)h->evA.size() < nLv) {
-    cudaEvent_t a, b;
+    cudaEvent_t a, a2, b;
     CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&a2, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
     h->evA.push_back(a);
+    h->evA2.push_back(a2);
     h->evB.push_back(b);
   }
   // a2-a6 as one enqueue function of the stream, so it can be captured once into a CUDA graph
@@ -892,6 +903,13 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
         launch_linv(C, li, R.i1 - R.i0, sd);
       }
       LAUNCH_CHECK("k_linv");
+      return DD_OK;
+    };
+    // rowperm + K2 of level l: need every K3 update of level l-1 into level l's panels (K3a2:
+    // it reads the rows of block t in earlier panels, which rowperm permutes)
+    auto panel_phase = [&](int l) -> int {
+      const LevelRanges& R = h->lv[l];
+      h->cur_level = l;
       RowpermArgs r = rp;
       r.list = rp.list + R.r0;
       if (R.r1 > R.r0) {
@@ -915,6 +933,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     CUDA_TRY(cudaStreamWaitEvent(sd, h->evLoad, 0));
     if (nL > 0) {
       int rc = diag_phase(0);
+      if (!rc) rc = panel_phase(0);
       if (rc) return rc;
     }
     for (int l = 0; l < nL; ++l) {
@@ -925,17 +944,36 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
       a3.work = work + (l & 1) * wpar;
       a3.targets = k3.targets + R.t0;
       a3.tprefix = k3.tprefix + R.t0;
-      a3.ntargets = R.ta - R.t0;
+      // K3a1: the next level's diagonal blocks first, so its K1 starts while K3a2 / K3b run
+      a3.ntargets = R.ta1 - R.t0;
       a3.tile0 = 0;
-      if (R.tiles_a > 0) {
-        TraceScope ts(h, DD_PH_K3, R.tiles_b > 0 ? 0.0 : R.fl_k3, st);
-        launch_k3(C, h->k3cfg, a3, (int)R.tiles_a, st);
+      const int64_t tiles_a2 = R.tiles_a - R.tiles_a1;
+      if (R.tiles_a1 > 0) {
+        TraceScope ts(h, DD_PH_K3, (tiles_a2 > 0 || R.tiles_b > 0) ? 0.0 : R.fl_k3, st);
+        launch_k3(C, h->k3cfg, a3, (int)R.tiles_a1, st);
       }
       LAUNCH_CHECK("k3_update");
       CUDA_TRY(cudaEventRecord(h->evA[l], st));
       if (l + 1 < nL) {
         CUDA_TRY(cudaStreamWaitEvent(sd, h->evA[l], 0));
         int rc = diag_phase(l + 1);
+        if (rc) return rc;
+      }
+      // K3a2: the rest of the next level's panels
+      a3.targets = k3.targets + R.ta1;
+      a3.tprefix = k3.tprefix + R.ta1;
+      a3.ntargets = R.ta - R.ta1;
+      a3.tile0 = R.tiles_a1;
+      h->cur_level = l;
+      if (tiles_a2 > 0) {
+        TraceScope ts(h, DD_PH_K3, R.tiles_b > 0 ? 0.0 : R.fl_k3, st);
+        launch_k3(C, h->k3cfg, a3, (int)tiles_a2, st);
+      }
+      LAUNCH_CHECK("k3_update");
+      CUDA_TRY(cudaEventRecord(h->evA2[l], st));
+      if (l + 1 < nL) {
+        CUDA_TRY(cudaStreamWaitEvent(sd, h->evA2[l], 0));
+        int rc = panel_phase(l + 1);
         if (rc) return rc;
       }
       a3.targets = k3.targets + R.ta;

@@ -294,9 +294,21 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
       for (int q = 0; q < K1_MAXQ; ++q) {
         const int i = tid + q * NT1;
         if (i < k || i >= s) continue;
-        cz v = Ak[q];
-        for (int m = 0; m < kk; ++m)
+        // one FMA chain (DDK_K1_CHAINS=2 splits it in two: measured slower on cfg1, 35.1 vs 32.4 ms)
+#ifndef DDK_K1_CHAINS
+#define DDK_K1_CHAINS 1
+#endif
+        cz v = Ak[q], v1 = mk(0.0, 0.0);
+        int m = 0;
+        if (DDK_K1_CHAINS == 2)
+        for (; m + 1 < kk; m += 2) {
           v = fms<C>(v, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0), mk(wtr[(kk) * WLD + (m)], C ? wti[(kk) * WLD + (m)] : 0.0));
+          v1 = fms<C>(v1, mk(Lpr[LP(i, m + 1)], C ? Lpi[LP(i, m + 1)] : 0.0),
+                      mk(wtr[(kk) * WLD + (m + 1)], C ? wti[(kk) * WLD + (m + 1)] : 0.0));
+        }
+        for (; m < kk; ++m)
+          v = fms<C>(v, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0), mk(wtr[(kk) * WLD + (m)], C ? wti[(kk) * WLD + (m)] : 0.0));
+        if (DDK_K1_CHAINS == 2) v = v + v1;
         wv[q] = v;
         st<C>(W, Wel(i, kk), wim, v);
         if (i - c0 < NB) {
@@ -340,10 +352,17 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           const int i = tid + q * NT1;
           if (i < k || i >= s) continue;
           cz v = (i < imax) ? ld<C>(A, Ael(imax, i), aim) : ld<C>(A, Ael(i, imax), aim);
-          for (int m = 0; m < kk; ++m) {
-            const cz w = inwin ? mk(wtr[(imax - c0) * WLD + (m)], C ? wti[(imax - c0) * WLD + (m)] : 0.0) : mk(wrow_r[m], wrow_i[m]);
-            v = fms<C>(v, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0), w);
+          cz v1 = mk(0.0, 0.0);
+          const double* wr = inwin ? wtr + (imax - c0) * WLD : wrow_r;
+          const double* wi = inwin ? wti + (imax - c0) * WLD : wrow_i;
+          int m = 0;
+          if (DDK_K1_CHAINS == 2)
+          for (; m + 1 < kk; m += 2) {
+            v = fms<C>(v, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0), mk(wr[m], C ? wi[m] : 0.0));
+            v1 = fms<C>(v1, mk(Lpr[LP(i, m + 1)], C ? Lpi[LP(i, m + 1)] : 0.0), mk(wr[m + 1], C ? wi[m + 1] : 0.0));
           }
+          for (; m < kk; ++m) v = fms<C>(v, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0), mk(wr[m], C ? wi[m] : 0.0));
+          if (DDK_K1_CHAINS == 2) v = v + v1;
           wv2[q] = v;
           st<C>(W, Wel(i, kk + 1), wim, v);
           if (i - c0 < NB) {
