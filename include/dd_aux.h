@@ -183,7 +183,9 @@ int dd_aux_assemble_work_bytes(dd_aux_handle_t h, int64_t nclq, const int64_t* c
 int dd_aux_assemble(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, const int32_t* clq_blk,
                     const void* d_S, const int64_t* S_offset, int32_t symmetrize, const int64_t* val_offset,
                     void* d_vals, void* d_work, void* stream);
-/* Algorithmic HBM bytes of the last dd_aux_assemble (contributions read + output written). */
+/* Algorithmic (unique) HBM bytes of the last dd_aux_assemble: every output element written once,
+ * every contributing S_p element read once (the mirrored S_p[J, I] too for the symmetric part of
+ * an off-diagonal block). */
 double dd_aux_last_assemble_bytes(dd_aux_handle_t h);
 
 /* Change the refinement policy of an analyzed handle (same meaning as the options fields). */

@@ -134,6 +134,7 @@ struct dd_aux_handle_s {
   bool lookahead = true;   // env DD_AUX_LOOKAHEAD=0 disables the side-stream overlap
   std::vector<cudaEvent_t> evA, evA2, evB;
   cudaEvent_t evLoad = nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr;  // factor timing (finfo.ms_load / ms_factor)
   // f1 assembly tables (host images kept alive for the async upload)
   std::vector<AsmItem> asm_items;
   std::vector<AsmContrib> asm_cons;
@@ -166,6 +167,8 @@ struct dd_aux_handle_s {
     for (auto e : evB) cudaEventDestroy(e);
     for (auto e : evA2) cudaEventDestroy(e);
     if (evLoad) cudaEventDestroy(evLoad);
+    for (auto e : {t0, t1, t2})
+      if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
     if (gfactor.exec) cudaGraphExecDestroy(gfactor.exec);
     if (gsolve.exec) cudaGraphExecDestroy(gsolve.exec);
@@ -819,10 +822,10 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   const int64_t k1im = C ? h->nK1 : 0;
   const NodeDev* dnodes = (const NodeDev*)(F + h->off_nodes);
 
-  cudaEvent_t e0, e1, e2;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  cudaEventCreate(&e2);
+  // timing events owned by the handle (no leak on an early error return)
+  for (auto* e : {&h->t0, &h->t1, &h->t2})
+    if (!*e) CUDA_TRY(cudaEventCreate(e));
+  cudaEvent_t e0 = h->t0, e1 = h->t1, e2 = h->t2;
   cudaEventRecord(e0, st);
   // ---- a1: zero the arena, load the caller's blocks
   CUDA_TRY(cudaMemsetAsync(arena, 0, (size_t)h->nA * (C ? 2 : 1) * sizeof(double), st));
@@ -1008,9 +1011,6 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   float ms_load = 0, ms_fac = 0;
   cudaEventElapsedTime(&ms_load, e0, e1);
   cudaEventElapsedTime(&ms_fac, e1, e2);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaEventDestroy(e2);
   if (finfo) {
     finfo->npos = C ? 0 : totals[0];
     finfo->nneg = C ? 0 : totals[1];
@@ -1273,6 +1273,7 @@ static int build_assembly(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_pt
         it.c0 = c0;
         it.k0 = k0;
         it.k1 = k1;
+        it.pad = (i == j);  // diagonal block (byte accounting only)
         items.push_back(it);
       }
     }
@@ -1319,12 +1320,15 @@ int dd_aux_assemble(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, con
                              cudaMemcpyHostToDevice, st));
   AsmArgs a{(const AsmItem*)W, (const AsmContrib*)(W + off_c), (const double*)d_S, (double*)d_vals};
   {
-    double bytes = 0;  // algorithmic traffic: contributions read (x2 with the symmetric part) + output written
+    // algorithmic (unique) traffic: output written once + each contribution read once, plus the
+    // mirrored block S_p[J, I] for the symmetric part of an off-diagonal block (a diagonal
+    // block's transpose is the same memory)
+    double bytes = 0;
     const double es = h->cplx ? 16.0 : 8.0;
     for (size_t q = 0; q < h->asm_items.size(); ++q) {
       const AsmItem& it = h->asm_items[q];
       const double cells = (double)it.rows * std::min(asm_chunk(), it.cols - it.c0);
-      bytes += cells * es * (1.0 + (symmetrize ? 2.0 : 1.0) * (it.k1 - it.k0));
+      bytes += cells * es * (1.0 + ((symmetrize && !it.pad) ? 2.0 : 1.0) * (it.k1 - it.k0));
     }
     h->asm_bytes = bytes;
     TraceScope ts(h, DD_PH_ASSEMBLE, 0.0, st);

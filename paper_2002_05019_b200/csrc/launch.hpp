@@ -131,7 +131,7 @@ struct AsmItem {       // f1: one 32-column chunk of one output block (lower pat
   int32_t rows, cols;  // s_I, s_J
   int32_t c0;          // first column of the chunk
   int32_t k0, k1;      // contributor range (ascending clique index)
-  int32_t pad;
+  int32_t pad;         // 1 = diagonal block (byte accounting only)
 };
 
 struct AsmContrib {    // clique p's sub-block: S_p[ra + r, cb + c], S_p column-major with ld = m_p
