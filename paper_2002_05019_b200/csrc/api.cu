@@ -926,7 +926,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
       a2.work = work + (l & 1) * wpar;
       if (R.s1 > R.s0) {
         TraceScope ts(h, DD_PH_K2, R.fl_k2, sd);
-        launch_k2(C, h->k3cfg, a2, R.k1 - R.k0, R.s1 - R.s0, sd);
+        launch_k2(C, h->k3cfg, a2, R.k1 - R.k0, R.s1 - R.s0, R.max_s, sd);
       }
       LAUNCH_CHECK("k2_panel");
       CUDA_TRY(cudaEventRecord(h->evB[l], sd));

@@ -1231,10 +1231,16 @@ __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k2_gem
   const Tile T = a.items[blockIdx.x];
   const NodeDev nd = a.nd[T.target];
   const int s = nd.s, m0 = T.tm * BM, n0 = T.tn * BN;
+  // the column gather map (P_t) of the K range goes to shared memory first: the loader then
+  // never waits on a dependent global load before its cp.async
+  int* pcol = reinterpret_cast<int*>(smem + G::SMEM_BYTES / sizeof(double));
+  const int kmax = min(s, n0 + BN);
+  for (int q = threadIdx.x; q < kmax; q += blockDim.x) pcol[q] = a.perm[nd.ydof + q];
+  __syncthreads();
   Seg sg;
   sg.a = a.arena + nd.panel + nd.sp;   // Ahat rows (struct part), columns gathered by perm
   sg.lda = nd.ld;
-  sg.acol = a.perm + nd.ydof;
+  sg.acol = pcol;
   sg.b = a.arena + nd.inv;             // B(k, n) = X(n, k)
   sg.ldb = nd.ldi;
   sg.K = min(s, n0 + BN);
@@ -1476,25 +1482,28 @@ void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st)
 }
 
 template <bool C, int CFG>
-static void launch_k2_t(const K2Args& a, int nitems, cudaStream_t st) {
+static void launch_k2_t(const K2Args& a, int nitems, int max_s, cudaStream_t st) {
   using Cf = K3Cfg<C, CFG>;
-  set_smem(k2_gemm<C, CFG>, Cf::G::SMEM_BYTES);
-  k2_gemm<C, CFG><<<nitems, Cf::NT, Cf::G::SMEM_BYTES, st>>>(a);
+  const size_t sm = Cf::G::SMEM_BYTES + (size_t)((max_s + 3) & ~3) * sizeof(int);  // + column map
+  // the attribute is set to the largest size any level may use (a replayed CUDA graph checks every
+  // node against the attribute's final value); occupancy follows each launch's own size
+  set_smem(k2_gemm<C, CFG>, Cf::G::SMEM_BYTES + (size_t)K1_MAX_BLOCK * sizeof(int));
+  k2_gemm<C, CFG><<<nitems, Cf::NT, sm, st>>>(a);
 }
 
-void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, cudaStream_t st) {
+void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, int max_s, cudaStream_t st) {
   if (nitems > 0) {
     switch (cfg) {  // same tile shapes as the Schur update
-      case 9: cplx ? launch_k2_t<true, 9>(a, nitems, st) : launch_k2_t<false, 9>(a, nitems, st); break;
-      case 10: cplx ? launch_k2_t<true, 10>(a, nitems, st) : launch_k2_t<false, 10>(a, nitems, st); break;
-      case 11: cplx ? launch_k2_t<true, 11>(a, nitems, st) : launch_k2_t<false, 11>(a, nitems, st); break;
-      case 12: cplx ? launch_k2_t<true, 12>(a, nitems, st) : launch_k2_t<false, 12>(a, nitems, st); break;
-      case 13: cplx ? launch_k2_t<true, 13>(a, nitems, st) : launch_k2_t<false, 13>(a, nitems, st); break;
-      case 6: cplx ? launch_k2_t<true, 6>(a, nitems, st) : launch_k2_t<false, 6>(a, nitems, st); break;
-      case 5: cplx ? launch_k2_t<true, 5>(a, nitems, st) : launch_k2_t<false, 5>(a, nitems, st); break;
-      case 4: cplx ? launch_k2_t<true, 4>(a, nitems, st) : launch_k2_t<false, 4>(a, nitems, st); break;
-      case 1: cplx ? launch_k2_t<true, 1>(a, nitems, st) : launch_k2_t<false, 1>(a, nitems, st); break;
-      default: cplx ? launch_k2_t<true, 7>(a, nitems, st) : launch_k2_t<false, 7>(a, nitems, st); break;
+      case 9: cplx ? launch_k2_t<true, 9>(a, nitems, max_s, st) : launch_k2_t<false, 9>(a, nitems, max_s, st); break;
+      case 10: cplx ? launch_k2_t<true, 10>(a, nitems, max_s, st) : launch_k2_t<false, 10>(a, nitems, max_s, st); break;
+      case 11: cplx ? launch_k2_t<true, 11>(a, nitems, max_s, st) : launch_k2_t<false, 11>(a, nitems, max_s, st); break;
+      case 12: cplx ? launch_k2_t<true, 12>(a, nitems, max_s, st) : launch_k2_t<false, 12>(a, nitems, max_s, st); break;
+      case 13: cplx ? launch_k2_t<true, 13>(a, nitems, max_s, st) : launch_k2_t<false, 13>(a, nitems, max_s, st); break;
+      case 6: cplx ? launch_k2_t<true, 6>(a, nitems, max_s, st) : launch_k2_t<false, 6>(a, nitems, max_s, st); break;
+      case 5: cplx ? launch_k2_t<true, 5>(a, nitems, max_s, st) : launch_k2_t<false, 5>(a, nitems, max_s, st); break;
+      case 4: cplx ? launch_k2_t<true, 4>(a, nitems, max_s, st) : launch_k2_t<false, 4>(a, nitems, max_s, st); break;
+      case 1: cplx ? launch_k2_t<true, 1>(a, nitems, max_s, st) : launch_k2_t<false, 1>(a, nitems, max_s, st); break;
+      default: cplx ? launch_k2_t<true, 7>(a, nitems, max_s, st) : launch_k2_t<false, 7>(a, nitems, max_s, st); break;
     }
   }
   if (nstrips > 0) {

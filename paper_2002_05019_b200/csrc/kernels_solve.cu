@@ -379,15 +379,9 @@ __global__ void __launch_bounds__(256) k_spmv(SpmvArgs a) {
 // element-wise (interleaved complex at arbitrary offsets, so no 16-byte cp.async chunks): each
 // thread gathers its 8 A and 8 B elements of the next K-chunk into registers while the DMMAs
 // of the current chunk run, then stores them into the engine's MK / KN shared-memory tiles.
-// 64x64 tiles, complex in the 4M form (a 64x32 3M variant measured 1.9x slower on cfg3: 932 vs
-// 497 ms per 1000 right-hand sides, register-bound at 212 registers)
 using SpG_R = Gemm<64, 64, 16, 2, 2, 2, false, false, true>;
 using SpG_C = Gemm<64, 64, 16, 2, 2, 2, true, false, true>;
-constexpr int SPT_M = 64, SPT_K = 16;
-template <bool C>
-struct SpTN {
-  static constexpr int value = 64;
-};
+constexpr int SPT_M = 64, SPT_N = 64, SPT_K = 16;
 
 template <bool C>
 __global__ void __launch_bounds__(128) k_spmv_dmma(SpmvArgs a) {
@@ -395,12 +389,10 @@ __global__ void __launch_bounds__(128) k_spmv_dmma(SpmvArgs a) {
   extern __shared__ __align__(16) double smem[];
   const SpRow R = a.rows[blockIdx.x];
   const int I = R.I, sI = (int)a.blk_size[I];
-  constexpr int SPT_N = SpTN<C>::value;
   const int m0 = R.tm * SPT_M, n0 = blockIdx.y * SPT_N;
   const int tid = threadIdx.x;
-  constexpr int PER = SPT_M * SPT_K / 128;   // 8 elements of A per thread per chunk
-  constexpr int PERB = SPT_N * SPT_K / 128;  // 8 (real) / 4 (complex) elements of B
-  double ra[PER], ia[PER], rb[PERB], ib[PERB];
+  constexpr int PER = SPT_M * SPT_K / 128;  // 8 elements of A and of B per thread per chunk
+  double ra[PER], ia[PER], rb[PER], ib[PER];
   // chunk iterator over (segment, k0)
   int q = R.c0, k0 = 0;
   auto fetch = [&](int qq, int kk0) {
@@ -436,10 +428,6 @@ __global__ void __launch_bounds__(128) k_spmv_dmma(SpmvArgs a) {
       }
       ra[u] = vr;
       ia[u] = vi;
-    }
-#pragma unroll
-    for (int u = 0; u < PERB; ++u) {
-      const int e = tid + u * 128;
       // B(k, n) = X(oJ + k, n): k fastest
       const int kb = e % SPT_K, nb = e / SPT_K;
       const int gkb = kk0 + kb, gn = n0 + nb;
@@ -473,10 +461,6 @@ __global__ void __launch_bounds__(128) k_spmv_dmma(SpmvArgs a) {
       }
       As[k * G::A_LD + m] = ra[u];
       if (C) As[G::A_TILE + k * G::A_LD + m] = ia[u];
-    }
-#pragma unroll
-    for (int u = 0; u < PERB; ++u) {
-      const int e = tid + u * 128;
       const int kb = e % SPT_K, nb = e / SPT_K;
       Bs[nb * G::B_LD + kb] = rb[u];
       if (C) Bs[G::B_TILE + nb * G::B_LD + kb] = ib[u];
@@ -721,8 +705,7 @@ void launch_spmv(bool cplx, const SpmvArgs& a, int nrow_tiles, cudaStream_t st) 
     else k_spmv<false><<<grid, 256, 0, st>>>(a);
     return;
   }
-  const int spn = cplx ? SpTN<true>::value : SpTN<false>::value;
-  dim3 grid(nrow_tiles, (a.nrhs + spn - 1) / spn);
+  dim3 grid(nrow_tiles, (a.nrhs + SPT_N - 1) / SPT_N);
   if (cplx) {
     set_smem(k_spmv_dmma<true>, SpG_C::SMEM_BYTES);
     k_spmv_dmma<true><<<grid, 128, SpG_C::SMEM_BYTES, st>>>(a);

@@ -156,7 +156,7 @@ size_t k1_smem(bool cplx, int max_s, int nb_req);
 void launch_k1(bool cplx, const K1Args& a, int nnodes, int max_s, cudaStream_t st);
 constexpr int K1_MAX_BLOCK = 4096;  // largest interface (diagonal block) size K1 supports
 void launch_rowperm(bool cplx, const RowpermArgs& a, int nlist, int max_s, cudaStream_t st);
-void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, cudaStream_t st);
+void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, int max_s, cudaStream_t st);
 int k3_bm(bool cplx, int cfg);
 int k3_bn(bool cplx, int cfg);
 void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st);

@@ -336,3 +336,19 @@ def test_padded_ldb_zero_rhs_and_two_refinement_steps():
     Xo, _, _ = oracle.refine_solve(p, F, B, 2)
     assert rel_diff(X, Xo) <= TOL_REL
     assert residual_berr(p, X, B).max() <= TOL_BERR
+
+
+def test_isolated_max_size_block():
+    """The largest supported interface (K1_MAX_BLOCK = 4096 DoFs, real): backward error bound and
+    Sylvester inertia against numpy's eigvalsh (the oracle's O(s^3) Python BK is too slow here)."""
+    s = 4096
+    rng = np.random.default_rng(4096)
+    A = rng.standard_normal((s, s))
+    A = A + A.T
+    p = Problem(np.array([s]), np.array([0, 1]), np.array([0], dtype=np.int32),
+                np.asfortranarray(A).ravel(order="F"), np.array([0]), [])
+    B = random_rhs(s, 2, False, 3)
+    X, finfo, _ = run_gpu(p, B)
+    assert residual_berr(p, X, B).max() <= TOL_BERR
+    ev = np.linalg.eigvalsh(A)
+    assert (finfo["npos"], finfo["nneg"], finfo["nzero"]) == (int((ev > 0).sum()), int((ev < 0).sum()), 0)
