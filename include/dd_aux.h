@@ -96,7 +96,8 @@ void dd_aux_default_options(dd_aux_options* opt);
 
 /* Host-only symbolic phase ("very fast symbolic factorization step").
  *  nblk        number of interfaces (blocks), > 0
- *  blk_size    [nblk] interface sizes s_I > 0
+ *  blk_size    [nblk] interface sizes 0 < s_I <= 3328 (real) / 1664 (complex): the in-block
+ *              Bunch-Kaufman kernel keeps a panel copy of L_II in shared memory
  *  colptr      [nblk+1] block-CSC column pointers of the LOWER block pattern
  *  rowidx      [colptr[nblk]] row block ids: sorted ascending per column, >= column,
  *              diagonal block present (first), no duplicates

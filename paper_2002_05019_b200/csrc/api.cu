@@ -281,9 +281,10 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   std::string msg = validate_pattern(nblk, blk_size, colptr, rowidx);
   if (!msg.empty()) return fail(DD_ERR_PATTERN, msg);
   for (int64_t j = 0; j < nblk; ++j)
-    if (blk_size[j] > K1_MAX_BLOCK)
+    if (blk_size[j] > (dtype == DD_COMPLEX128 ? K1_MAX_BLOCK_CPLX : K1_MAX_BLOCK_REAL))
       return fail(DD_ERR_PATTERN, "interface size " + std::to_string(blk_size[j]) + " exceeds the supported maximum " +
-                                      std::to_string(K1_MAX_BLOCK));
+                                      std::to_string(dtype == DD_COMPLEX128 ? K1_MAX_BLOCK_CPLX : K1_MAX_BLOCK_REAL) +
+                                      (dtype == DD_COMPLEX128 ? " (complex)" : " (real)"));
   dd_aux_options opt;
   dd_aux_default_options(&opt);
   if (opt_in) opt = *opt_in;

@@ -154,7 +154,10 @@ void launch_load(bool cplx, const double* vals, const LoadBlock* lb, int nblocks
                  int64_t aim, cudaStream_t st);
 size_t k1_smem(bool cplx, int max_s, int nb_req);
 void launch_k1(bool cplx, const K1Args& a, int nnodes, int max_s, cudaStream_t st);
-constexpr int K1_MAX_BLOCK = 4096;  // largest interface (diagonal block) size K1 supports
+// largest interface (diagonal block) size K1 supports: its panel copy of L (s x 8 columns at the
+// narrowest panel) + the W window must fit the 210 KB shared-memory budget
+constexpr int K1_MAX_BLOCK_REAL = 3328, K1_MAX_BLOCK_CPLX = 1664;
+constexpr int K1_MAX_BLOCK = K1_MAX_BLOCK_REAL;
 void launch_rowperm(bool cplx, const RowpermArgs& a, int nlist, int max_s, cudaStream_t st);
 void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, int max_s, cudaStream_t st);
 int k3_bm(bool cplx, int cfg);

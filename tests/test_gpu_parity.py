@@ -273,7 +273,7 @@ def test_cuda_graphs_bitwise_equal_direct(name, grid, sizes, tol):
 
 @pytest.mark.parametrize("s,cplx", [(1100, False), (1100, True), (2100, False)])
 def test_isolated_large_block_pivots(s, cplx):
-    """Interfaces above 1024 DoFs take K1's 16-rows-per-thread path (up to K1_MAX_BLOCK = 4096):
+    """Interfaces above 1024 DoFs take K1's 16-rows-per-thread path (up to 3328 real / 1664 complex):
     BK decisions equal the oracle's on one isolated block; solution within the north_star bounds."""
     rng = np.random.default_rng(s + 7 * cplx)
     A = rng.standard_normal((s, s))
@@ -338,17 +338,21 @@ def test_padded_ldb_zero_rhs_and_two_refinement_steps():
     assert residual_berr(p, X, B).max() <= TOL_BERR
 
 
-def test_isolated_max_size_block():
-    """The largest supported interface (K1_MAX_BLOCK = 4096 DoFs, real): backward error bound and
-    Sylvester inertia against numpy's eigvalsh (the oracle's O(s^3) Python BK is too slow here)."""
-    s = 4096
-    rng = np.random.default_rng(4096)
+@pytest.mark.parametrize("s,cplx", [(3328, False), (1664, True)])
+def test_isolated_max_size_block(s, cplx):
+    """The largest supported interfaces (3328 real / 1664 complex DoFs, include/dd_aux.h):
+    backward error bound, and for the real case Sylvester inertia against numpy's eigvalsh (the
+    oracle's O(s^3) Python BK is too slow at this size)."""
+    rng = np.random.default_rng(s)
     A = rng.standard_normal((s, s))
+    if cplx:
+        A = A + 1j * rng.standard_normal((s, s))
     A = A + A.T
     p = Problem(np.array([s]), np.array([0, 1]), np.array([0], dtype=np.int32),
                 np.asfortranarray(A).ravel(order="F"), np.array([0]), [])
-    B = random_rhs(s, 2, False, 3)
+    B = random_rhs(s, 2, cplx, 3)
     X, finfo, _ = run_gpu(p, B)
     assert residual_berr(p, X, B).max() <= TOL_BERR
-    ev = np.linalg.eigvalsh(A)
-    assert (finfo["npos"], finfo["nneg"], finfo["nzero"]) == (int((ev > 0).sum()), int((ev < 0).sum()), 0)
+    if not cplx:
+        ev = np.linalg.eigvalsh(A)
+        assert (finfo["npos"], finfo["nneg"], finfo["nzero"]) == (int((ev > 0).sum()), int((ev < 0).sum()), 0)

@@ -152,10 +152,12 @@ def test_assemble_tables_host():
 
 
 def test_interface_size_limit():
-    """Interfaces above K1_MAX_BLOCK (4096) are rejected at analyze (DD_ERR_PATTERN)."""
+    """Interfaces above the in-block kernel's shared-memory limit (3328 real / 1664 complex DoFs)
+    are rejected at analyze (DD_ERR_PATTERN); the limits themselves are accepted."""
     dd = _lib()
-    with pytest.raises(dd.DDAuxError) as ei:
-        dd.dd_aux_analyze([4097], [0, 1], [0])
-    assert ei.value.code == dd.DD_ERR_PATTERN and "4096" in str(ei.value)
-    h = dd.dd_aux_analyze([4096], [0, 1], [0])
-    dd.dd_aux_destroy(h)
+    for dt, lim in ((dd.DD_REAL64, 3328), (dd.DD_COMPLEX128, 1664)):
+        with pytest.raises(dd.DDAuxError) as ei:
+            dd.dd_aux_analyze([lim + 1], [0, 1], [0], dtype=dt)
+        assert ei.value.code == dd.DD_ERR_PATTERN and str(lim) in str(ei.value)
+        h = dd.dd_aux_analyze([lim], [0, 1], [0], dtype=dt)
+        dd.dd_aux_destroy(h)
