@@ -7,9 +7,10 @@
 //     A_IJ = sum_{p : I, J in clique p} S_p[rows of I, cols of J]        (I >= J, lower blocks)
 // with the optional symmetric part (S_p + S_p^T)/2 taken first (reading L12).
 //
-// HBM-bound: every S_p entry that lands in a lower block is read once (twice with the
-// symmetric part: the transposed read goes through a 32x32 shared tile so both reads are
-// coalesced) and every output element is written once.  Owner-computes over output tiles
+// HBM-bound: every S_p entry that lands in an output block is read once (for an off-diagonal
+// block with the symmetric part also its mirror S_p[J, I], through a 32x32 shared tile so both
+// reads are coalesced; a diagonal block computes its lower tiles and stores each mirrored, so its
+// S_p entries are read once as well) and every output element is written once.  Owner-computes over output tiles
 // with the contributors summed in ascending clique order (deterministic, no atomics); the
 // additions are explicitly rounded (__dadd_rn / __dmul_rn) so no FMA contraction changes them.
 #include <cuda_runtime.h>
@@ -54,7 +55,12 @@ __global__ void __launch_bounds__(AT * ATY) k_assemble(AsmArgs a) {
   const T* S = reinterpret_cast<const T*>(a.S);
   T* out = reinterpret_cast<T*>(a.vals) + it.dst;
   const int tx = threadIdx.x % AT, ty = threadIdx.x / AT;
-  for (int r0 = 0; r0 < it.rows; r0 += AT) {
+  // diagonal block with the symmetric part: the result is symmetric, so only the tiles on and
+  // below the diagonal are computed and each off-diagonal one is also stored mirrored -- every
+  // S_p element of the block is then read from HBM once (the pair S[r0, c0] / S[c0, r0] is read by
+  // this CTA only)
+  const bool mirror = SYM && it.pad;
+  for (int r0 = mirror ? it.c0 : 0; r0 < it.rows; r0 += AT) {
     T acc[AT / ATY];
 #pragma unroll
     for (int j = 0; j < AT / ATY; ++j) acc[j] = E::zero();
@@ -87,6 +93,17 @@ __global__ void __launch_bounds__(AT * ATY) k_assemble(AsmArgs a) {
     for (int j = 0; j < AT / ATY; ++j) {
       const int row = r0 + tx, col = it.c0 + ty + ATY * j;
       if (row < it.rows && col < it.cols) out[row + (int64_t)col * it.rows] = acc[j];
+    }
+    if (SYM && mirror && r0 > it.c0) {  // the mirrored tile (c0.., r0..) = this tile transposed
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < AT / ATY; ++j) tileT[ty + ATY * j][tx] = acc[j];
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < AT / ATY; ++j) {
+        const int row = it.c0 + tx, col = r0 + ty + ATY * j;
+        if (row < it.rows && col < it.cols) out[row + (int64_t)col * it.rows] = tileT[tx][ty + ATY * j];
+      }
     }
   }
 }
