@@ -43,6 +43,28 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// mbarrier helpers (MBAR pipeline): per-stage "full" barriers completed by the threads' cp.async
+// groups (cp.async.mbarrier.arrive.noinc), "empty" barriers completed by one arrival per warp
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_cpasync_arrive(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n"
+      "DD_MBAR_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared.b64 P, [%0], %1;\n"
+      " @!P bra DD_MBAR_WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ void dmma16x8x4(double (&c)[4], double a0, double a1, double b0) {
   asm volatile(
       "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
@@ -64,7 +86,7 @@ __device__ __forceinline__ double dneg(double x) {  // sign flip on the integer 
 // adjacent in shared memory: one 16-byte LDS each instead of two 8-byte ones (bank-conflict free
 // with the ld = 4 (mod 16) padding).  The accumulator mapping (for_each, masks) follows.
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool CPLX, bool A_KM, bool B_KN,
-          bool C3M = false, bool FINE = true, bool VEC = false, bool RECT = false>
+          bool C3M = false, bool FINE = true, bool VEC = false, bool RECT = false, bool MBAR = false>
 struct Gemm {
   static constexpr int NTHR = WARPS_M * WARPS_N * 32;
   static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
@@ -454,6 +476,10 @@ struct Gemm {
   template <class SegFn>
   __device__ static void run(SegFn segfn, int nseg, int m0, int n0, int M, int N, int64_t aim, int64_t bim,
                              double* smem, Acc& acc, unsigned mask = ~0u) {
+    if constexpr (MBAR) {
+      run_mbar(segfn, nseg, m0, n0, M, N, aim, bim, smem, acc, mask);
+      return;
+    }
     int pseg = 0, pk = 0;
     Seg cur;
     while (pseg < nseg) {  // skip empty segments
@@ -496,6 +522,72 @@ struct Gemm {
       cp_async_commit();
       compute_stage(smem + (done % STAGES) * STAGE, acc, mask);
       ++done;
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+
+  // MBAR main loop: no CTA-wide barrier per stage.  A warp waits only for the data of the stage
+  // it computes (full[s]) and, before refilling a buffer, for every warp to have consumed it
+  // (empty[s], one stage of slack with STAGES >= 3), so warps drift within the pipeline depth.
+  template <class SegFn>
+  __device__ static void run_mbar(SegFn segfn, int nseg, int m0, int n0, int M, int N, int64_t aim, int64_t bim,
+                                  double* smem, Acc& acc, unsigned mask) {
+    static_assert(STAGES >= 3, "MBAR pipeline needs >= 3 stages");
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int q = 0; q < STAGES; ++q) {
+        mbar_init(&full[q], NTHR);
+        mbar_init(&empty[q], NTHR / 32);
+      }
+    }
+    __syncthreads();
+    int pseg = 0, pk = 0;
+    Seg cur;
+    while (pseg < nseg) {
+      cur = segfn(pseg);
+      if (cur.K > 0) break;
+      ++pseg;
+    }
+    auto advance = [&]() {
+      pk += BK;
+      if (pk >= cur.K) {
+        pk = 0;
+        ++pseg;
+        while (pseg < nseg) {
+          cur = segfn(pseg);
+          if (cur.K > 0) break;
+          ++pseg;
+        }
+      }
+    };
+    int issued = 0;
+#pragma unroll 1
+    for (int q = 0; q < STAGES - 1 && pseg < nseg; ++q) {
+      load_stage(smem + q * STAGE, cur, pk, m0, n0, M, N, aim, bim);
+      mbar_cpasync_arrive(&full[q]);
+      advance();
+      ++issued;
+    }
+    const int lane = threadIdx.x & 31;
+    int done = 0;
+#pragma unroll 1
+    while (done < issued) {
+      const int sb = done % STAGES;
+      mbar_wait(&full[sb], (unsigned)((done / STAGES) & 1));
+      compute_stage(smem + sb * STAGE, acc, mask);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sb]);
+      ++done;
+      if (pseg < nseg) {
+        const int nb = issued % STAGES;
+        if (issued >= STAGES) mbar_wait(&empty[nb], (unsigned)(((issued - STAGES) / STAGES) & 1));
+        load_stage(smem + nb * STAGE, cur, pk, m0, n0, M, N, aim, bim);
+        mbar_cpasync_arrive(&full[nb]);
+        advance();
+        ++issued;
+      }
     }
     cp_async_wait<0>();
     __syncthreads();

@@ -1147,6 +1147,17 @@ struct K3Cfg<true, 13> {  // complex 64x32 3M, 2 stages, coarse masking (no per-
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
 
+template <>
+struct K3Cfg<false, 14> {  // real 64x64, RECT, 3 stages, mbarrier pipeline (no CTA barrier per stage)
+  using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false, false, true, true>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
+};
+template <>
+struct K3Cfg<true, 14> {  // complex 64x32 3M VEC, 3 stages, mbarrier pipeline
+  using G = Gemm<64, 32, 16, 2, 2, 3, true, false, false, true, true, true, false, true>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 3;
+};
+
 template <bool C, int CFG>
 __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_update(K3Args a) {
   using Cf = K3Cfg<C, CFG>;
@@ -1426,6 +1437,7 @@ int k3_bm(bool cplx, int cfg) {
     case 11: return bm_of<11>(cplx);
     case 12: return bm_of<12>(cplx);
     case 13: return bm_of<13>(cplx);
+    case 14: return bm_of<14>(cplx);
     default: return bm_of<1>(cplx);
   }
 }
@@ -1444,6 +1456,7 @@ int k3_bn(bool cplx, int cfg) {
     case 11: return bn_of<11>(cplx);
     case 12: return bn_of<12>(cplx);
     case 13: return bn_of<13>(cplx);
+    case 14: return bn_of<14>(cplx);
     default: return bn_of<1>(cplx);
   }
 }
@@ -1477,6 +1490,7 @@ void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st)
     case 11: launch_k3_c<11>(cplx, a, ntiles, st); break;
     case 12: launch_k3_c<12>(cplx, a, ntiles, st); break;
     case 13: launch_k3_c<13>(cplx, a, ntiles, st); break;
+    case 14: launch_k3_c<14>(cplx, a, ntiles, st); break;
     default: launch_k3_c<1>(cplx, a, ntiles, st); break;
   }
 }
