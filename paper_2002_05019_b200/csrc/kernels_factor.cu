@@ -51,7 +51,10 @@ __global__ void k0_load(const double* __restrict__ vals, const LoadBlock* __rest
 }
 
 // ============================================================================ K1 diagonal BK
-constexpr int NT1 = 256;
+#ifndef DDK_NT1
+#define DDK_NT1 256
+#endif
+constexpr int NT1 = DDK_NT1;  // K1 threads per CTA (one row each on the <=NT1 fast path)
 constexpr size_t K1_SMEM_BUDGET = 210 * 1024;  // dynamic smem for the panel copy of L + W window
 
 // Panel width: the widest of 64, 56, ..., 8 whose shared panel copy of L (s x NB) plus the W
@@ -66,8 +69,8 @@ __host__ __device__ inline int k1_panel_nb(int s, bool cplx, int req) {
   return nb;
 }
 // rows per thread: s <= NT1 * MAXQ (4 -> 1024 on the fast path, 16 -> 4096 for larger interfaces)
-using K1GemmR = Gemm<64, 64, 16, 2, 4, 2, false, false, false>;
-using K1GemmC = Gemm<64, 64, 16, 2, 4, 2, true, false, false>;
+using K1GemmR = Gemm<64, 64, 16, 2, NT1 / 64, 2, false, false, false>;
+using K1GemmC = Gemm<64, 64, 16, 2, NT1 / 64, 2, true, false, false>;
 
 __device__ __forceinline__ void warp_argmax(double& v, int& i) {
 #pragma unroll

@@ -287,9 +287,25 @@ def test_isolated_large_block_pivots(s, cplx):
     piv = sv.pivots()
     sv.close()
     f = bk_factor(A)
+    # pivot agreement with the oracle is a diagnostic at this size: one near-tie decided the other
+    # way under a different (valid) rounding order changes every later decision (L3,
+    # "GPU <-> oracle pivot agreement"); the hard checks are the backward error, the inertia and a
+    # well-formed pivot sequence
     agree = float(np.mean(piv["ipiv"] == f["ipiv"]))
-    assert agree >= 0.99, agree  # near-ties may legitimately diverge at this size
+    print(f"ipiv agreement with the oracle: {agree:.3f}")
     assert residual_berr(p, X, B).max() <= TOL_BERR
+    ip = piv["ipiv"]
+    q = 0
+    while q < s:  # LAPACK convention: 1x1 -> kp+1 >= q+1, 2x2 -> the same negative entry twice
+        if ip[q] > 0:
+            assert q + 1 <= ip[q] <= s
+            q += 1
+        else:
+            assert q + 1 < s and ip[q + 1] == ip[q] and -ip[q] >= q + 2 and -ip[q] <= s
+            q += 2
+    if not cplx:
+        ev = np.linalg.eigvalsh(A)
+        assert (finfo["npos"], finfo["nneg"], finfo["nzero"]) == (int((ev > 0).sum()), int((ev < 0).sum()), 0)
 
 
 def test_complex_4m_parity():
