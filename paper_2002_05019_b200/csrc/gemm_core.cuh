@@ -331,8 +331,10 @@ struct Gemm {
   }
 
   // Sub-tiles a < NA, b < NB of the warp tile; PRED: per-mma predicate from mask (FINE mode).
+  // nks: k-steps of 4 holding data in this stage (a segment's last stage may be partly
+  // zero-filled: its empty k-steps issue no DMMA)
   template <int NA, int NB, bool PRED>
-  __device__ static void compute_body(const double* st, Acc& acc, unsigned mask) {
+  __device__ static void compute_body(const double* st, Acc& acc, unsigned mask, int nks = BK / 4) {
     if constexpr (!PRED) mask = ~0u;  // constant: the per-mma predicates fold away
     const double* As = st;
     const double* Bs = st + NPL * A_TILE;
@@ -341,6 +343,7 @@ struct Gemm {
     const int g = lane >> 2, tg = lane & 3;
 #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
+      if (ks > 0 && ks >= nks) break;  // warp-uniform
       const int k = ks * 4 + tg;
       double ar[MI][2], br[NI];
       double ai[CPLX ? MI : 1][2], bi[CPLX ? NI : 1];
@@ -449,25 +452,25 @@ struct Gemm {
     }
   }
 
-  __device__ static void compute_stage(const double* st, Acc& acc, unsigned mask = ~0u) {
+  __device__ static void compute_stage(const double* st, Acc& acc, unsigned mask = ~0u, int nks = BK / 4) {
     if constexpr (RECT) {
       if (mask == 0u) return;  // warp-uniform
       const int na = (mask >> 4) & 15, ncg = (mask >> 8) & 15;
       constexpr int BPG = VEC ? 2 : 1;  // sub-tiles per column group
-      if (na == MI && ncg == NCG) return compute_body<MI, NI, false>(st, acc, ~0u);
+      if (na == MI && ncg == NCG) return compute_body<MI, NI, false>(st, acc, ~0u, nks);
       if constexpr (MI >= 2) {
-        if (na == 1 && ncg == NCG) return compute_body<1, NI, false>(st, acc, ~0u);
+        if (na == 1 && ncg == NCG) return compute_body<1, NI, false>(st, acc, ~0u, nks);
       }
       if constexpr (NCG >= 2) {
-        if (na == MI && ncg == 1) return compute_body<MI, BPG, false>(st, acc, ~0u);
-        if (na == 1 && ncg == 1) return compute_body<1, BPG, false>(st, acc, ~0u);
+        if (na == MI && ncg == 1) return compute_body<MI, BPG, false>(st, acc, ~0u, nks);
+        if (na == 1 && ncg == 1) return compute_body<1, BPG, false>(st, acc, ~0u, nks);
       }
-      return compute_body<MI, NI, false>(st, acc, ~0u);  // other shapes: full warp tile
+      return compute_body<MI, NI, false>(st, acc, ~0u, nks);  // other shapes: full warp tile
     } else if constexpr (!FINE) {
       if (mask == 0u) return;  // warp-uniform
-      compute_body<MI, NI, false>(st, acc, ~0u);
+      compute_body<MI, NI, false>(st, acc, ~0u, nks);
     } else {
-      compute_body<MI, NI, true>(st, acc, mask);
+      compute_body<MI, NI, true>(st, acc, mask, nks);
     }
   }
 
@@ -500,10 +503,19 @@ struct Gemm {
       }
     };
     int issued = 0;
+    unsigned kvpack = 0;  // per stage slot: k-steps of 4 holding data (4 bits each)
+#ifndef DDK_KSKIP
+#define DDK_KSKIP 1
+#endif
+    auto note_k = [&](int slot) {
+      const int kv = DDK_KSKIP ? min(BK, cur.K - pk) : BK;
+      kvpack = (kvpack & ~(15u << (4 * slot))) | ((unsigned)((kv + 3) / 4) << (4 * slot));
+    };
 #pragma unroll 1
     for (int s = 0; s < STAGES - 1; ++s) {
       if (pseg < nseg) {
         load_stage(smem + (issued % STAGES) * STAGE, cur, pk, m0, n0, M, N, aim, bim);
+        note_k(issued % STAGES);
         advance();
         ++issued;
       }
@@ -516,11 +528,13 @@ struct Gemm {
       __syncthreads();
       if (pseg < nseg) {
         load_stage(smem + (issued % STAGES) * STAGE, cur, pk, m0, n0, M, N, aim, bim);
+        note_k(issued % STAGES);
         advance();
         ++issued;
       }
       cp_async_commit();
-      compute_stage(smem + (done % STAGES) * STAGE, acc, mask);
+      const int slot = done % STAGES;
+      compute_stage(smem + slot * STAGE, acc, mask, (int)((kvpack >> (4 * slot)) & 15u));
       ++done;
     }
     cp_async_wait<0>();

@@ -1161,6 +1161,17 @@ struct K3Cfg<true, 14> {  // complex 64x32 3M VEC, 3 stages, mbarrier pipeline
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 3;
 };
 
+template <>
+struct K3Cfg<false, 15> {  // cfg 13 register-capped for 5 CTAs per SM (20 warps)
+  using G = Gemm<64, 64, 16, 2, 2, 2, false, false, false, false, false, false, true>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 5;
+};
+template <>
+struct K3Cfg<true, 15> {  // complex 64x32 3M VEC, 5 CTAs per SM
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, true, true>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 5;
+};
+
 template <bool C, int CFG>
 __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_update(K3Args a) {
   using Cf = K3Cfg<C, CFG>;
@@ -1441,6 +1452,7 @@ int k3_bm(bool cplx, int cfg) {
     case 12: return bm_of<12>(cplx);
     case 13: return bm_of<13>(cplx);
     case 14: return bm_of<14>(cplx);
+    case 15: return bm_of<15>(cplx);
     default: return bm_of<1>(cplx);
   }
 }
@@ -1460,6 +1472,7 @@ int k3_bn(bool cplx, int cfg) {
     case 12: return bn_of<12>(cplx);
     case 13: return bn_of<13>(cplx);
     case 14: return bn_of<14>(cplx);
+    case 15: return bn_of<15>(cplx);
     default: return bn_of<1>(cplx);
   }
 }
@@ -1494,6 +1507,7 @@ void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st)
     case 12: launch_k3_c<12>(cplx, a, ntiles, st); break;
     case 13: launch_k3_c<13>(cplx, a, ntiles, st); break;
     case 14: launch_k3_c<14>(cplx, a, ntiles, st); break;
+    case 15: launch_k3_c<15>(cplx, a, ntiles, st); break;
     default: launch_k3_c<1>(cplx, a, ntiles, st); break;
   }
 }
