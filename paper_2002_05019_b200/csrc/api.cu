@@ -852,6 +852,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   k1.e_off = h->e_off;
   k1.stats = (int64_t*)(F + h->off_stats);
   k1.nb = getenv("DD_AUX_K1NB") ? atoi(getenv("DD_AUX_K1NB")) : 0;
+  k1.fullw = getenv("DD_AUX_K1FULLW") ? atoi(getenv("DD_AUX_K1FULLW")) : 1;
   int64_t* totals_d = (int64_t*)(F + h->off_totals);
   const int nLv = (int)h->lv.size();
   if (!h->side) {

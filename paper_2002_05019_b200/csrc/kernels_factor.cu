@@ -59,13 +59,16 @@ constexpr size_t K1_SMEM_BUDGET = 210 * 1024;  // dynamic smem for the panel cop
 
 // Panel width: the widest of 64, 56, ..., 8 whose shared panel copy of L (s x NB) plus the W
 // window cache (NB x (NB+1)) fits the budget; an explicit override (8..64) wins if it fits.
-__host__ __device__ inline size_t k1_panel_bytes(int s, bool cplx, int nb) {
-  return ((size_t)s * nb + (size_t)nb * (nb + 1)) * (cplx ? 16 : 8);
+// fullw: the W cache holds ALL rows of the block (s x (NB+1)) instead of the NB-row window, so W
+// never goes through global memory inside a panel (no row loads for an out-of-window imax, no
+// global row interchanges); W is written to global memory once per panel for the trailing update
+__host__ __device__ inline size_t k1_panel_bytes(int s, bool cplx, int nb, bool fullw = false) {
+  return ((size_t)s * nb + (size_t)(fullw ? s : nb) * (nb + 1)) * (cplx ? 16 : 8);
 }
-__host__ __device__ inline int k1_panel_nb(int s, bool cplx, int req) {
-  if (req >= 8 && req <= K1NB_MAX && k1_panel_bytes(s, cplx, req) <= K1_SMEM_BUDGET) return req;
+__host__ __device__ inline int k1_panel_nb(int s, bool cplx, int req, bool fullw = false) {
+  if (req >= 8 && req <= K1NB_MAX && k1_panel_bytes(s, cplx, req, fullw) <= K1_SMEM_BUDGET) return req;
   int nb = K1NB_MAX;
-  while (nb > 8 && k1_panel_bytes(s, cplx, nb) > K1_SMEM_BUDGET) nb -= 8;
+  while (nb > 8 && k1_panel_bytes(s, cplx, nb, fullw) > K1_SMEM_BUDGET) nb -= 8;
   return nb;
 }
 // rows per thread: s <= NT1 * MAXQ (4 -> 1024 on the fast path, 16 -> 4096 for larger interfaces)
@@ -251,12 +254,16 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
   // their current W values in registers, so a column without interchange costs two barriers.
   // Interchanges of rows inside L columns of EARLIER panels (explicit form, L5) are deferred
   // to the panel end (LAPACK xLASWP style): nothing in this kernel reads those columns before.
-  const int NB = k1_panel_nb(s, C, a.nb);
+  // full-W mode when the panel width it allows is still >= 32 (a.fullw: 1 auto, 0 off)
+  const bool FW = a.fullw != 0 && k1_panel_nb(s, C, a.nb, true) >= 32 &&
+                  k1_panel_bytes(s, C, k1_panel_nb(s, C, a.nb, true), true) <= K1_SMEM_BUDGET;
+  const int NB = FW ? k1_panel_nb(s, C, a.nb, true) : k1_panel_nb(s, C, a.nb);
+  const int WIN = FW ? s : NB;               // rows held by the W cache, from c0
   double* Lpr = smem;                       // Lp(i, m) = Lpr[m * s + i]
   double* Lpi = smem + (size_t)s * NB;
-  // W window cache wt(r, m) = W(c0 + r, m), row stride NB+1 (after the panel copy of L)
+  // W cache wt(r, m) = W(c0 + r, m), row stride NB+1 (after the panel copy of L)
   double* wtr = smem + (size_t)s * NB * (C ? 2 : 1);
-  double* wti = wtr + (size_t)NB * (NB + 1);
+  double* wti = wtr + (size_t)WIN * (NB + 1);
   const int WLD = NB + 1;
   auto LP = [&](int i, int m) { return (size_t)m * s + i; };
   cz Ak[K1_MAXQ], wv[K1_MAXQ], wv2[K1_MAXQ];
@@ -313,8 +320,8 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           v = fms<C>(v, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0), mk(wtr[(kk) * WLD + (m)], C ? wti[(kk) * WLD + (m)] : 0.0));
         if (DDK_K1_CHAINS == 2) v = v + v1;
         wv[q] = v;
-        st<C>(W, Wel(i, kk), wim, v);
-        if (i - c0 < NB) {
+        if (!FW) st<C>(W, Wel(i, kk), wim, v);
+        if (i - c0 < WIN) {
           wtr[(i - c0) * WLD + (kk)] = v.r;
           if constexpr (C) wti[(i - c0) * WLD + (kk)] = v.i;
         }
@@ -339,7 +346,7 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
         kp = k;
       } else {
         // updated column imax -> W(:, kk+1) (symmetric access of the not-yet-updated trailing A)
-        const bool inwin = imax - c0 < NB;
+        const bool inwin = imax - c0 < WIN;
         if (!inwin) {
           for (int m = tid; m < kk; m += NT1) {
             cz w = ld<C>(W, Wel(imax, m), wim);
@@ -367,8 +374,8 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           for (; m < kk; ++m) v = fms<C>(v, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0), mk(wr[m], C ? wi[m] : 0.0));
           if (DDK_K1_CHAINS == 2) v = v + v1;
           wv2[q] = v;
-          st<C>(W, Wel(i, kk + 1), wim, v);
-          if (i - c0 < NB) {
+          if (!FW) st<C>(W, Wel(i, kk + 1), wim, v);
+          if (i - c0 < WIN) {
             wtr[(i - c0) * WLD + (kk + 1)] = v.r;
             if constexpr (C) wti[(i - c0) * WLD + (kk + 1)] = v.i;
           }
@@ -394,8 +401,8 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
               const int i = tid + q * NT1;
               if (i < k || i >= s) continue;
               wv[q] = wv2[q];
-              st<C>(W, Wel(i, kk), wim, wv2[q]);
-              if (i - c0 < NB) {
+              if (!FW) st<C>(W, Wel(i, kk), wim, wv2[q]);
+              if (i - c0 < WIN) {
                 wtr[(i - c0) * WLD + (kk)] = wv2[q].r;
                 if constexpr (C) wti[(i - c0) * WLD + (kk)] = wv2[q].i;
               }
@@ -425,11 +432,18 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           }
         }
         // rows kkk, kp of W columns 0..kk+kstep-1 (global, and the window cache)
-        const bool kpwin = kp - c0 < NB;
+        const bool kpwin = kp - c0 < WIN;
         for (int m = tid; m < kk + kstep; m += NT1) {
-          cz x = ld<C>(W, Wel(kkk, m), wim), y = ld<C>(W, Wel(kp, m), wim);
-          st<C>(W, Wel(kkk, m), wim, y);
-          st<C>(W, Wel(kp, m), wim, x);
+          cz x, y;
+          if (FW) {  // the whole W lives in the cache
+            x = mk(wtr[(kkk - c0) * WLD + m], C ? wti[(kkk - c0) * WLD + m] : 0.0);
+            y = mk(wtr[(kp - c0) * WLD + m], C ? wti[(kp - c0) * WLD + m] : 0.0);
+          } else {
+            x = ld<C>(W, Wel(kkk, m), wim);
+            y = ld<C>(W, Wel(kp, m), wim);
+            st<C>(W, Wel(kkk, m), wim, y);
+            st<C>(W, Wel(kp, m), wim, x);
+          }
           wtr[(kkk - c0) * WLD + (m)] = y.r;
           if constexpr (C) wti[(kkk - c0) * WLD + (m)] = y.i;
           if (kpwin) {
@@ -561,6 +575,12 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
       // A(k:s, k:s) -= L(k:s, c0:k) W(k:s, 0:kb)^T.  The GEMM window starts at the even
       // row ke <= k (16-byte aligned cp.async chunks); row/column ke < k is masked.
       const int kb = k - c0, ke = k & ~1, M = s - ke;
+      if (FW) {  // W rows [ke, s) of this panel: cache -> global (the GEMM's B operand)
+        for (int e = tid; e < (s - ke) * kb; e += NT1) {
+          const int i = ke + e % (s - ke), m = e / (s - ke);
+          st<C>(W, Wel(i, m), wim, mk(wtr[(i - c0) * WLD + m], C ? wti[(i - c0) * WLD + m] : 0.0));
+        }
+      }
       // the barrier orders this CTA's earlier global stores (L panel, W) before the cp.async reads
       __syncthreads();
       Seg sg;

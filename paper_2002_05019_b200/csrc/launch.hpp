@@ -31,6 +31,7 @@ struct K1Args {
   int64_t d_off, e_off;
   int64_t* stats;
   int nb;  // K1 panel width override (0 = automatic; env DD_AUX_K1NB, A/B only)
+  int fullw;  // 1: whole-block W cache when it fits with a >= 32-column panel (env DD_AUX_K1FULLW=0 off)
 };
 
 struct RowpermArgs {
