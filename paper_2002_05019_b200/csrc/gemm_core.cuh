@@ -419,8 +419,7 @@ struct Gemm {
 #pragma unroll
           for (int b = 0; b < NB; ++b)
             if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.t[a][b], sa[a][0], sa[a][1], sb[b]);
-        continue;
-      }
+      } else {
 #pragma unroll
       for (int a = 0; a < NA; ++a)
 #pragma unroll
@@ -449,6 +448,7 @@ struct Gemm {
           for (int b = 0; b < NB; ++b)
             if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.i[a][b], ai[a][0], ai[a][1], br[b]);
       }
+      }  // 4M / real
     }
   }
 

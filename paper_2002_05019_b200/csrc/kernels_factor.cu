@@ -220,7 +220,6 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
   int aslot = 0;
   __shared__ double wrow_r[K1NB_MAX], wrow_i[K1NB_MAX];
   __shared__ int s_swa[K1NB_MAX], s_swb[K1NB_MAX], s_nswp;
-  __shared__ int s_kp, s_kstep, s_zero, s_imax;
   __shared__ double s_absakk2[2];  // parity-buffered: no barrier between a read and the next write
   __shared__ double s_xw[2][4];    // register copies (wv, wv2) of the two interchanged rows
 
