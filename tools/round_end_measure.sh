@@ -1,4 +1,4 @@
-# Round-end measurement set (session 2, final kernels)
+# Round-end measurement set (one B200 via gpurun): GPU tests, smoke, every bench line, the default command's ncu launch list and ncu --set full captures of the dominant kernels.  Usage: gpurun -- bash tools/round_end_measure.sh
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/final3_pytest.log 2>&1; tail -2 gpurun_out/final3_pytest.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final3_smoke.log 2>&1; tail -1 gpurun_out/final3_smoke.log
 timeout 1200 python bench.py > gpurun_out/final3_bench_cfg2.json 2> gpurun_out/final3_bench_cfg2.err
