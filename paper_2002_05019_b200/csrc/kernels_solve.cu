@@ -10,6 +10,7 @@
 //                        k_bdiag       y_t = L_tt^{-T} y_t
 //   x = P^T y            k_perm_out    (store, or accumulate a refinement correction)
 //   r = b - A x          k_spmv        (refinement residual over the ORIGINAL blocks, L7)
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -163,7 +164,10 @@ __global__ void __launch_bounds__(128) k_fupd(SolveArgs a) {
 // Backward pull update y_t -= sum_{i in struct(t)} L_it^T y_i.  With split-K (G > 1) CTA
 // (tile, g) sums the g-th contiguous chunk of struct(t) into a partial buffer and
 // k_bupd_reduce subtracts the G partials in fixed order g = 0..G-1 (deterministic).
-template <bool C, bool M3>
+// CL (thread-block cluster of the G chunk CTAs of one tile, G <= 8): the partial tiles are reduced
+// through distributed shared memory in the same fixed order g = 0..G-1 (bitwise the same result
+// as the two-kernel partial-buffer path, without its HBM round trip and second launch).
+template <bool C, bool M3, bool CL>
 __global__ void __launch_bounds__(128) k_bupd(SolveArgs a, int G, double* part, int64_t pim) {
   if (a.flag && *a.flag == 0) return;
   using G_ = typename SolveG<C, M3>::BU;
@@ -204,6 +208,31 @@ __global__ void __launch_bounds__(128) k_bupd(SolveArgs a, int G, double* part, 
   if (G == 1) {
     G_::template store_tile<1>(acc, smem, a.y + nt.ydof + m0 + (int64_t)n0 * a.ldy, a.ldy, a.yim, nt.s - m0,
                                a.nrhs - n0);
+  } else if constexpr (CL) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    constexpr int E = SUBM * SBN;
+    double* Pr = smem;      // this CTA's partial tile, SUBM x SBN, ld SUBM (pipeline smem is idle)
+    double* Pi = smem + E;
+    G_::for_each(acc, [&](int r, int c, double vr, double vi) {
+      Pr[r + c * SUBM] = vr;
+      if (C) Pi[r + c * SUBM] = vi;
+    });
+    cl.sync();
+    const int e0 = (int)((int64_t)E * g / G), e1 = (int)((int64_t)E * (g + 1) / G);
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const int r = e % SUBM, c = e / SUBM;
+      if (m0 + r >= nt.s || n0 + c >= a.nrhs) continue;
+      double sr = 0.0, si = 0.0;
+      for (int h = 0; h < G; ++h) {
+        sr += cl.map_shared_rank(Pr, h)[e];
+        if (C) si += cl.map_shared_rank(Pi, h)[e];
+      }
+      const int64_t o = nt.ydof + (int64_t)(m0 + r) + (int64_t)(n0 + c) * a.ldy;
+      a.y[o] -= sr;
+      if (C) a.y[o + a.yim] -= si;
+    }
+    cl.sync();  // the partial tiles stay alive until every remote read is done
   } else {
     double* P = part + (int64_t)blockIdx.x * SUBM * a.nrhs;  // SUBM x nrhs, ld SUBM
     G_::for_each(acc, [&](int r, int c, double vr, double vi) {
@@ -656,21 +685,44 @@ int bupd_split(bool cplx, int ntiles, int nrhs, int max_rp) {
 }
 
 template <bool C, bool M3>
-static void bupd_t(const SolveArgs& a, int ntiles, int G, double* part, int64_t pim, cudaStream_t st) {
+static void bupd_t(const SolveArgs& a, int ntiles, int G, double* part, int64_t pim, bool cluster, cudaStream_t st) {
   using GB = typename SolveG<C, M3>::BU;
   dim3 grid(ntiles * G, ntn(C, a.nrhs));
-  set_smem(k_bupd<C, M3>, GB::SMEM_BYTES);
-  k_bupd<C, M3><<<grid, 128, GB::SMEM_BYTES, st>>>(a, G, part, pim);
+  if (cluster && G > 1) {
+    set_smem(k_bupd<C, M3, true>, GB::SMEM_BYTES);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = GB::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_bupd<C, M3, true>, a, G, part, pim);
+    return;
+  }
+  set_smem(k_bupd<C, M3, false>, GB::SMEM_BYTES);
+  k_bupd<C, M3, false><<<grid, 128, GB::SMEM_BYTES, st>>>(a, G, part, pim);
 }
 
 void launch_bupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, int max_rp, double* part, cudaStream_t st) {
   if (ntiles == 0 || a.nrhs == 0) return;
-  const int G = part ? bupd_split(cplx, ntiles, a.nrhs, max_rp) : 1;
+  // split-K reduction: partial buffer + fixed-order reduction kernel (default), or through a
+  // thread-block cluster with distributed shared memory (DD_AUX_BUPD_CLUSTER=1, G capped at 8):
+  // correct but measured slower -- cfg3 backward update 1518 -> 1620 ms, cfg2 528 -> 625 ms per
+  // step (the cap on G costs more parallelism than the saved partial round trip gains)
+  static const bool cluster = getenv("DD_AUX_BUPD_CLUSTER") && atoi(getenv("DD_AUX_BUPD_CLUSTER")) == 1;
+  int G = part ? bupd_split(cplx, ntiles, a.nrhs, max_rp) : 1;
+  if (cluster) G = std::min(G, 8);
   const int64_t pim = (int64_t)BUPD_MAX_PARTS * SUBM * a.nrhs;
-  if (!cplx) bupd_t<false, false>(a, ntiles, G, part, pim, st);
-  else if (m3) bupd_t<true, true>(a, ntiles, G, part, pim, st);
-  else bupd_t<true, false>(a, ntiles, G, part, pim, st);
-  if (G > 1) {
+  if (!cplx) bupd_t<false, false>(a, ntiles, G, part, pim, cluster, st);
+  else if (m3) bupd_t<true, true>(a, ntiles, G, part, pim, cluster, st);
+  else bupd_t<true, false>(a, ntiles, G, part, pim, cluster, st);
+  if (G > 1 && !cluster) {
     dim3 g2(ntiles, std::min(64, (SUBM * a.nrhs + 255) / 256));
     if (cplx) k_bupd_reduce<true><<<g2, 256, 0, st>>>(a, G, part, pim);
     else k_bupd_reduce<false><<<g2, 256, 0, st>>>(a, G, part, pim);
