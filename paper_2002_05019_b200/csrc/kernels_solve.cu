@@ -681,7 +681,8 @@ int bupd_split(bool cplx, int ntiles, int nrhs, int max_rp) {
   int G = (want + ctas - 1) / ctas;
   G = std::min(G, std::max(1, max_rp / 128));
   G = std::min(G, std::max(1, BUPD_MAX_PARTS / std::max(ntiles, 1)));
-  return std::max(1, std::min(G, 32));
+  static const int gmax = getenv("DD_AUX_BUPD_GMAX") ? atoi(getenv("DD_AUX_BUPD_GMAX")) : 32;  // A/B only
+  return std::max(1, std::min(G, gmax));
 }
 
 template <bool C, bool M3>
