@@ -128,11 +128,13 @@ struct dd_aux_handle_s {
   double nnz_full = 0;  // entries of the full symmetric A (K6 flops)
   // lookahead: high-priority side stream + per-level events
   cudaStream_t side = nullptr;
+  cudaStream_t side2 = nullptr;   // k_rowperm: concurrent with k_linv / K2 of the same level
+  cudaEvent_t evR = nullptr;      // joins side2 back into the caller's stream
   bool norm_valid = false;  // ||A||_inf of the current factorization's d_vals computed on device
   bool m3 = false;         // complex products in the 3M form (options.complex_3m)
   int k3cfg = 1;           // K3 tile configuration (env DD_AUX_K3CFG, read at analyze)
   bool lookahead = true;   // env DD_AUX_LOOKAHEAD=0 disables the side-stream overlap
-  std::vector<cudaEvent_t> evA, evA2, evB;
+  std::vector<cudaEvent_t> evA, evA2, evB, evK;  // evK[l]: K1 of level l done (perm ready)
   cudaEvent_t evLoad = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr;  // factor timing (finfo.ms_load / ms_factor)
   // f1 assembly tables (host images kept alive for the async upload)
@@ -166,10 +168,13 @@ struct dd_aux_handle_s {
     for (auto e : evA) cudaEventDestroy(e);
     for (auto e : evB) cudaEventDestroy(e);
     for (auto e : evA2) cudaEventDestroy(e);
+    for (auto e : evK) cudaEventDestroy(e);
     if (evLoad) cudaEventDestroy(evLoad);
     for (auto e : {t0, t1, t2})
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
+    if (side2) cudaStreamDestroy(side2);
+    if (evR) cudaEventDestroy(evR);
     if (gfactor.exec) cudaGraphExecDestroy(gfactor.exec);
     if (gsolve.exec) cudaGraphExecDestroy(gsolve.exec);
     if (cap) cudaStreamDestroy(cap);
@@ -860,15 +865,19 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CUDA_TRY(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi));
     CUDA_TRY(cudaEventCreateWithFlags(&h->evLoad, cudaEventDisableTiming));
+    CUDA_TRY(cudaStreamCreateWithPriority(&h->side2, cudaStreamNonBlocking, hi));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->evR, cudaEventDisableTiming));
   }
   while ((int)h->evA.size() < nLv) {
-    cudaEvent_t a, a2, b;
+    cudaEvent_t a, a2, b, kk;
     CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&a2, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&kk, cudaEventDisableTiming));
     h->evA.push_back(a);
     h->evA2.push_back(a2);
     h->evB.push_back(b);
+    h->evK.push_back(kk);
   }
   // a2-a6 as one enqueue function of the stream, so it can be captured once into a CUDA graph
   // (options.use_graphs; SURVEY.md §8(a) a5 "graph-capture the whole level sequence")
@@ -897,6 +906,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
         launch_k1(C, k1, R.n1 - R.n0, R.max_s, sd);
       }
       LAUNCH_CHECK("k1_diag_bk");
+      CUDA_TRY(cudaEventRecord(h->evK[l], sd));  // the level's in-block permutations are final
       {
         LinvArgs li{(const DTile*)(F + h->off_litems) + R.i0, dnodes, arena, aim};
         double fl = 0;
@@ -912,14 +922,22 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     };
     // rowperm + K2 of level l: need every K3 update of level l-1 into level l's panels (K3a2:
     // it reads the rows of block t in earlier panels, which rowperm permutes)
-    auto panel_phase = [&](int l) -> int {
+    // k_rowperm (rows of block t inside EARLIER panels) and K2 (panel t itself) touch disjoint
+    // rows: rowperm runs on a third stream, gated by the same event (ready), joined at the end
+    static const bool rp3 = !(getenv("DD_AUX_ROWPERM3") && atoi(getenv("DD_AUX_ROWPERM3")) == 0);  // A/B
+    cudaStream_t s3 = h->lookahead ? (rp3 ? h->side2 : sd) : st;
+    auto panel_phase = [&](int l, cudaEvent_t ready) -> int {
       const LevelRanges& R = h->lv[l];
       h->cur_level = l;
       RowpermArgs r = rp;
       r.list = rp.list + R.r0;
       if (R.r1 > R.r0) {
-        TraceScope ts(h, DD_PH_ROWPERM, 0.0, sd);
-        launch_rowperm(C, r, R.r1 - R.r0, h->max_s, sd);
+        if (s3 != st && s3 != sd) {  // needs the level's K1 (perm) and every K3 read of those rows (ready)
+          CUDA_TRY(cudaStreamWaitEvent(s3, ready, 0));
+          CUDA_TRY(cudaStreamWaitEvent(s3, h->evK[l], 0));
+        }
+        TraceScope ts(h, DD_PH_ROWPERM, 0.0, s3);
+        launch_rowperm(C, r, R.r1 - R.r0, h->max_s, s3);
       }
       LAUNCH_CHECK("k_rowperm");
       K2Args a2 = k2;
@@ -938,7 +956,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     CUDA_TRY(cudaStreamWaitEvent(sd, h->evLoad, 0));
     if (nL > 0) {
       int rc = diag_phase(0);
-      if (!rc) rc = panel_phase(0);
+      if (!rc) rc = panel_phase(0, h->evLoad);
       if (rc) return rc;
     }
     for (int l = 0; l < nL; ++l) {
@@ -978,7 +996,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
       CUDA_TRY(cudaEventRecord(h->evA2[l], st));
       if (l + 1 < nL) {
         CUDA_TRY(cudaStreamWaitEvent(sd, h->evA2[l], 0));
-        int rc = panel_phase(l + 1);
+        int rc = panel_phase(l + 1, h->evA2[l]);
         if (rc) return rc;
       }
       a3.targets = k3.targets + R.ta;
@@ -993,6 +1011,10 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
       LAUNCH_CHECK("k3_update");
     }
     h->cur_level = -1;
+    if (s3 != st && s3 != sd) {  // join the rowperm stream (the solve reads the permuted rows)
+      CUDA_TRY(cudaEventRecord(h->evR, s3));
+      CUDA_TRY(cudaStreamWaitEvent(st, h->evR, 0));
+    }
     // ---- a6: statistics
       {
       TraceScope ts(h, DD_PH_STATS, 0.0, st);
