@@ -32,11 +32,15 @@ template <bool C>
 struct SolveN {
   static constexpr int value = C ? 32 : 64;
 };
+#ifndef DDK_SOLVE_STAGES_REAL
+#define DDK_SOLVE_STAGES_REAL 2
+#endif
 template <bool C, bool M3>
 struct SolveG {
   static constexpr int BN = SolveN<C>::value;
-  using FU = Gemm<SUBM, BN, 16, 2, 2, C ? 2 : 3, C, false, true, C && M3, C>;  // MK x KN (FINE = C)
-  using BU = Gemm<SUBM, BN, 16, 2, 2, C ? 2 : 3, C, true, true, C && M3, C>;   // KM x KN
+  static constexpr int ST = C ? 2 : DDK_SOLVE_STAGES_REAL;
+  using FU = Gemm<SUBM, BN, 16, 2, 2, ST, C, false, true, C && M3, C>;  // MK x KN (FINE = C)
+  using BU = Gemm<SUBM, BN, 16, 2, 2, ST, C, true, true, C && M3, C>;   // KM x KN
 };
 
 // ---------------------------------------------------------------------------- permutations
