@@ -41,7 +41,7 @@ import numpy as np
 
 __all__ = ["Problem", "grid_interfaces", "build_problem", "build_clique_buffer", "config", "config_cliques",
            "CONFIGS", "random_rhs",
-           "dense_expand", "block_pattern_from_cliques"]
+           "dense_expand", "block_pattern_from_cliques", "tie_block", "single_block_problem"]
 
 
 @dataclasses.dataclass
@@ -436,6 +436,51 @@ def dense_expand(prob: Problem) -> np.ndarray:
             A[off[i]:off[i + 1], off[j]:off[j + 1]] = blk
             A[off[j]:off[j + 1], off[i]:off[i + 1]] = blk.T
     return A
+
+
+def tie_block(s: int, seed: int = 0) -> np.ndarray:
+    """Integer-valued symmetric s x s block with many exact IDAMAX ties (reading L3 tests).
+
+    The block is a random interleaving of small decoupled groups whose local matrices are
+        T1 = [[0, s1, s2], [s1, 0, 0], [s2, 0, c]]                  c in {+-1, +-2, +-4}
+        T2 = [[1, 2 s1, 2 s2], [2 s1, 4, 0], [2 s2, 0, c]]          c in {+-1, +-2, +-4}
+        T0 = [[c]]                                                    (filler, c = +-1)
+    with random signs s1, s2 = +-1.  The first column of T1 / T2 has two entries of equal
+    magnitude (a tie the smallest-index rule must break), and every entry is a small integer
+    chosen so that the pivots that occur are +-1, +-2, +-4 or the 2x2 [[0, x], [x, y]] with
+    x = +-1, +-2: every value a Bunch-Kaufman factorization produces is then a short dyadic
+    rational, i.e. exact in binary64 in any evaluation order.  Pure data construction.
+    """
+    rng = np.random.default_rng([seed, 4242])
+    A = np.zeros((s, s))
+    posn = rng.permutation(s)
+    q = 0
+    while q < s:
+        left = s - q
+        kind = 0 if left < 3 else int(rng.integers(0, 3))
+        if kind == 0:
+            p0 = int(posn[q])
+            A[p0, p0] = float(rng.choice([-1.0, 1.0]))
+            q += 1
+            continue
+        loc = np.sort(posn[q:q + 3])
+        q += 3
+        s1, s2 = (float(v) for v in rng.choice([-1.0, 1.0], 2))
+        c = float(rng.choice([-4.0, -2.0, -1.0, 1.0, 2.0, 4.0]))
+        if kind == 1:
+            M = np.array([[0.0, s1, s2], [s1, 0.0, 0.0], [s2, 0.0, c]])
+        else:
+            M = np.array([[1.0, 2 * s1, 2 * s2], [2 * s1, 4.0, 0.0], [2 * s2, 0.0, c]])
+        A[np.ix_(loc, loc)] = M
+    return A
+
+
+def single_block_problem(A: np.ndarray) -> Problem:
+    """One interface whose diagonal block is the dense symmetric A (C-ABI input layout)."""
+    A = np.asarray(A)
+    n = A.shape[0]
+    return Problem(np.array([n], dtype=np.int64), np.array([0, 1], dtype=np.int64), np.array([0], dtype=np.int32),
+                   np.asfortranarray(A).ravel(order="F"), np.array([0], dtype=np.int64), [])
 
 
 # --------------------------------------------------------------------------- configs

@@ -24,4 +24,5 @@ function is pinned; none is "parity unpinned".
 from .bk import bk_factor, ALPHA, cabs1  # noqa: F401
 from .assemble import assemble  # noqa: F401
 from .block_ldlt import (symbolic, block_factor, block_solve, refine_solve, inertia,  # noqa: F401
-                         flops_factor, flops_solve_per_rhs, residual_berr, OracleFactor)
+                         flops_factor, flops_solve_per_rhs, residual_berr, OracleFactor, max_abs_L,
+                         norm_inf_A, matvec_blocks)

@@ -28,7 +28,20 @@ Output (P A P^T = L D L^T, (P A P^T)[i, j] = A[perm[i], perm[j]]):
   ipiv LAPACK convention (1-based): ipiv[k] = kp+1 for a 1x1 pivot, and
        ipiv[k] = ipiv[k+1] = -(kp+1) for a 2x2 pivot
   perm composite permutation
-  info 0, or 1 + first column with a zero pivot (LAPACK INFO)
+  info 0, or 1 + first column with a zero or non-finite pivot (LAPACK INFO)
+  nonfinite  number of pivot columns whose decision quantities (absakk, colmax,
+       or rowmax when it is evaluated) were not finite (reading L4b)
+  nperturbed number of exactly-zero pivot columns given d = perturb_delta
+       (opt-in static perturbation, reading L4)
+
+Failure readings (L4, L4b): LAPACK's xSYTF2 treats
+max(absakk, colmax) == 0 or DISNAN(absakk) as a zero pivot (INFO = k, no
+elimination).  This oracle extends the non-finite test to colmax and rowmax
+(NaN or Inf anywhere in the pivot column or the imax row), where LAPACK's
+IDAMAX would silently skip a NaN; on finite input the rule is LAPACK's exactly.
+With perturb_delta > 0 an exactly-zero pivot column is instead given the 1x1
+pivot d = +perturb_delta ("perturbation fallback ... flagged")
+and does not set info.
 """
 from __future__ import annotations
 
@@ -51,7 +64,7 @@ def _argmax_first(v):
     return int(np.argmax(v))  # numpy returns the first occurrence
 
 
-def bk_factor(A):
+def bk_factor(A, perturb_delta=0.0):
     """Restricted Bunch-Kaufman LDL^T of one symmetric block; lower triangle read."""
     A = np.asarray(A)
     n = A.shape[0]
@@ -60,6 +73,8 @@ def bk_factor(A):
     perm = np.arange(n)
     info = 0
     n2x2 = 0
+    nonfinite = 0
+    nperturbed = 0
 
     def sym(i, j):  # a(i, j) of the symmetric working matrix from its lower triangle
         return a[i, j] if i >= j else a[j, i]
@@ -74,7 +89,13 @@ def bk_factor(A):
             colmax = float(col[imax - k - 1])
         else:
             imax, colmax = k, 0.0
-        if max(absakk, colmax) == 0.0 or math.isnan(absakk):
+        bad = not (math.isfinite(absakk) and math.isfinite(colmax))
+        if not bad and max(absakk, colmax) == 0.0 and perturb_delta > 0.0:
+            a[k, k] = perturb_delta          # static perturbation (L4 opt-in): 1x1 pivot, no swap
+            absakk = float(cabs1(a[k, k]))
+            nperturbed += 1
+        elif bad or max(absakk, colmax) == 0.0:
+            nonfinite += int(bad)
             if info == 0:
                 info = k + 1
             kp = k
@@ -85,8 +106,15 @@ def bk_factor(A):
             kp = k
         else:
             # rowmax over row imax of the trailing block, excluding the diagonal entry
-            rowvals = [cabs1(sym(imax, j)) for j in range(k, n) if j != imax]
-            rowmax = float(max(rowvals))
+            rowvals = np.array([cabs1(sym(imax, j)) for j in range(k, n) if j != imax])
+            rowmax = float(np.max(rowvals))      # np.max propagates NaN (L4b)
+            if not math.isfinite(rowmax):
+                nonfinite += 1
+                if info == 0:
+                    info = k + 1
+                ipiv[k] = k + 1
+                k += 1
+                continue
             if absakk >= ALPHA * colmax * (colmax / rowmax):
                 kp = k
             elif float(cabs1(a[imax, imax])) >= ALPHA * rowmax:
@@ -141,7 +169,8 @@ def bk_factor(A):
             k += 2
         else:
             k += 1
-    return dict(L=L, d=d, e=e, ipiv=ipiv, perm=perm, info=info, n2x2=n2x2)
+    return dict(L=L, d=d, e=e, ipiv=ipiv, perm=perm, info=info, n2x2=n2x2, nonfinite=nonfinite,
+                nperturbed=nperturbed)
 
 
 def d_matrix(d, e, ipiv):

@@ -118,6 +118,8 @@ class OracleFactor:
     perm: Dict[int, np.ndarray]
     info: int                                  # 0 or 1 + first zero-pivot global DoF (orig numbering)
     n2x2: int
+    nonfinite: int = 0                         # pivot columns with non-finite decision values (L4b)
+    nperturbed: int = 0                        # statically perturbed zero pivots (L4 opt-in)
 
 
 def _lower_blocks(prob_blocks, sym):
@@ -141,27 +143,35 @@ def _lower_blocks(prob_blocks, sym):
     return A
 
 
-def block_factor(prob, order) -> OracleFactor:
-    """Right-looking block LDL^T with restricted BK (O3 a-c)."""
+def block_factor(prob, order, perturb_tau=0.0) -> OracleFactor:
+    """Right-looking block LDL^T with restricted BK (O3 a-c).
+
+    perturb_tau > 0 (reading L4, opt-in): an exactly-zero pivot column gets
+    the 1x1 pivot d = perturb_tau * ||A||_inf instead of reporting a zero pivot.
+    `info` is the FIRST zero / non-finite pivot in elimination order (block order pi, then the
+    column order inside the block), as LAPACK's INFO is for one block."""
+    delta = perturb_tau * norm_inf_A(prob) if perturb_tau > 0 else 0.0
     sym = symbolic(prob.nblk, prob.colptr, prob.rowidx, order)
     A = _lower_blocks(prob.blocks(), sym)
     sizes = np.asarray(prob.blk_size)
     off = prob.dof_offset
     Lkk, L, d, e, ipiv, perm = {}, {}, {}, {}, {}, {}
     info = 0
-    n2x2 = 0
+    n2x2 = nonfinite = nperturbed = 0
     for k in sym["order"]:
         # a. in-block restricted Bunch-Kaufman on the updated diagonal block
-        f = bk_factor(A[(k, k)])
+        f = bk_factor(A[(k, k)], perturb_delta=delta)
         Lkk[k], d[k], e[k], ipiv[k], perm[k] = f["L"], f["d"], f["e"], f["ipiv"], f["perm"]
         n2x2 += f["n2x2"]
+        nonfinite += f["nonfinite"]
+        nperturbed += f["nperturbed"]
         if f["info"] and not info:
             info = int(off[k]) + int(perm[k][f["info"] - 1]) + 1
         # b. panel: column permutation, triangular solve, D scaling
         W = {}
         for i in sym["struct"][k]:
             Ahat = A[(i, k)][:, perm[k]]
-            W[i] = solve_triangular(Lkk[k], Ahat.T, lower=True, unit_diagonal=True).T  # Ahat Lkk^{-T}
+            W[i] = solve_triangular(Lkk[k], Ahat.T, lower=True, unit_diagonal=True, check_finite=False).T  # Ahat Lkk^{-T}
             L[(i, k)] = apply_dinv(W[i], d[k], e[k], ipiv[k])
         # c. Schur update of every target pair in struct(k)
         st = sym["struct"][k]
@@ -171,7 +181,19 @@ def block_factor(prob, order) -> OracleFactor:
         A[(k, k)] = None  # consumed
         for i in st:
             A[(i, k)] = None
-    return OracleFactor(sizes, sym, Lkk, L, d, e, ipiv, perm, info, n2x2)
+    return OracleFactor(sizes, sym, Lkk, L, d, e, ipiv, perm, info, n2x2, nonfinite, nperturbed)
+
+
+def max_abs_L(F: OracleFactor) -> float:
+    """max |L_ij| over the whole unit-lower factor (diagonal ones included; modulus for complex):
+    the element-growth diagnostic of the restricted BK factorization (SURVEY.md §8(b) max_abs_L)."""
+    m = 1.0
+    for k in F.sym["order"]:
+        m = max(m, float(np.abs(F.Lkk[k]).max()) if F.Lkk[k].size else 1.0)
+        for i in F.sym["struct"][k]:
+            if F.L[(i, k)].size:
+                m = max(m, float(np.abs(F.L[(i, k)]).max()))
+    return m
 
 
 # ------------------------------------------------------------------ O4 inertia
@@ -195,7 +217,7 @@ def block_solve(F: OracleFactor, B, off):
     y = {k: np.array(B[off[k]:off[k + 1]], dtype=dtype) for k in F.sym["order"]}
     z = {}
     for k in F.sym["order"]:                        # forward: L
-        z[k] = solve_triangular(F.Lkk[k], y[k][F.perm[k]], lower=True, unit_diagonal=True)
+        z[k] = solve_triangular(F.Lkk[k], y[k][F.perm[k]], lower=True, unit_diagonal=True, check_finite=False)
         for i in F.sym["struct"][k]:
             y[i] = y[i] - F.L[(i, k)] @ z[k]
     for k in F.sym["order"]:                        # D
@@ -204,7 +226,7 @@ def block_solve(F: OracleFactor, B, off):
     for k in reversed(F.sym["order"]):              # backward: L^T
         for i in F.sym["struct"][k]:
             z[k] = z[k] - F.L[(i, k)].T @ x[i]
-        zk = solve_triangular(F.Lkk[k].T, z[k], lower=False, unit_diagonal=True)
+        zk = solve_triangular(F.Lkk[k].T, z[k], lower=False, unit_diagonal=True, check_finite=False)
         x[k] = np.empty_like(zk)
         x[k][F.perm[k]] = zk
     X = np.empty(B.shape, dtype=dtype)
