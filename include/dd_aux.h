@@ -50,7 +50,9 @@ enum { DD_ORDER_AUTO = 0, DD_ORDER_ND = 1, DD_ORDER_MINDEG = 2, DD_ORDER_NATURAL
 
 enum {
   DD_OK = 0,
-  DD_ZERO_PIVOT = 1,
+  DD_ZERO_PIVOT = 1,           /* D is singular (reading L4): first_zero_pivot names the DoF     */
+  DD_NONFINITE = 2,            /* a pivot column held NaN/Inf (reading L4b); first_zero_pivot names
+                                  the first such (or zero) pivot in elimination order             */
   DD_ERR_CUDA = -100,          /* message carries the cudaError_t string                 */
   DD_ERR_WORKSPACE = -101,     /* a buffer size argument is smaller than required        */
   DD_ERR_NOT_FACTORED = -102,  /* dd_aux_solve before a successful dd_aux_factor         */
@@ -70,7 +72,11 @@ typedef struct {
                                  every column already has berr <= refine_tol; 0 = always refine */
   int32_t complex_3m;         /* complex Schur update with 3 real products (Gauss/3M, default 1) or
                                  4 (0); flop counts stay in the standard 8-flop convention */
-  int32_t reserved;
+  int32_t perturb;            /* reading L4 (opt-in, "perturbation fallback ... flagged"):
+                                 1 = an EXACTLY zero pivot column (max(|a_kk|, colmax) == 0) gets the 1x1
+                                 pivot d = perturb_tau * ||A||_inf instead of reporting DD_ZERO_PIVOT;
+                                 counted in dd_aux_factor_info.nperturbed.  Default 0 (LAPACK semantics). */
+  double perturb_tau;         /* > 0 when perturb = 1 (e.g. 1e-12)                                */
 } dd_aux_options;
 
 typedef struct {
@@ -87,8 +93,14 @@ typedef struct {
 typedef struct {
   int64_t npos, nneg, nzero;    /* inertia from D (real only; complex: all zero)  (a6)        */
   int64_t n2x2, nswaps;         /* 2x2 pivots, symmetric interchanges                          */
-  int64_t first_zero_pivot;     /* 0, or 1 + ORIGINAL global DoF index of the first zero pivot */
+  int64_t first_zero_pivot;     /* 0, or 1 + ORIGINAL global DoF index of the first zero or
+                                   non-finite pivot in ELIMINATION order (block order, then the
+                                   pivoted column order inside the block: LAPACK INFO order)   */
   float ms_load, ms_factor;     /* device time of the load and factor phases (CUDA events)     */
+  int64_t nperturbed;           /* zero pivots replaced by the static perturbation (opt-in)    */
+  int64_t nonfinite;            /* pivot columns with NaN/Inf decision values (reading L4b)    */
+  double max_abs_L;             /* max |L_ij| over the unit-lower factor (>= 1; modulus for
+                                   complex): the element-growth diagnostic of the restricted BK */
 } dd_aux_factor_info;
 
 /* Default options: AUTO order, 1 refinement step, 3M complex products. */
@@ -134,7 +146,10 @@ int dd_aux_solve_work_bytes(dd_aux_handle_t h, int64_t nrhs, size_t* bytes);
  *  stream      cudaStream_t (as void*); the call enqueues all work on it and synchronizes it
  *              once at exit to return finfo
  *  finfo       host out (may be NULL)
- * Returns DD_OK, DD_ZERO_PIVOT, or an error. */
+ * Returns DD_OK, DD_ZERO_PIVOT (D singular), DD_NONFINITE (NaN/Inf met in a pivot column; the
+ * factor is unusable), or an error.  With options.perturb an exactly zero pivot is perturbed
+ * instead (DD_OK, finfo.nperturbed > 0).  After DD_ZERO_PIVOT / DD_NONFINITE a solve returns
+ * DD_ERR_SINGULAR. */
 int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offset, void* d_factor,
                   void* d_work, void* stream, dd_aux_factor_info* finfo);
 

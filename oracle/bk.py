@@ -64,8 +64,20 @@ def _argmax_first(v):
     return int(np.argmax(v))  # numpy returns the first occurrence
 
 
-def bk_factor(A, perturb_delta=0.0):
-    """Restricted Bunch-Kaufman LDL^T of one symmetric block; lower triangle read."""
+def _rel_gap(x, y):
+    """Relative distance of the two sides of a pivot-test comparison (diagnostic only)."""
+    den = max(abs(x), abs(y))
+    return abs(x - y) / den if den > 0 else 0.0
+
+
+def bk_factor(A, perturb_delta=0.0, margins=None):
+    """Restricted Bunch-Kaufman LDL^T of one symmetric block; lower triangle read.
+
+    margins (optional list, diagnostic only -- it changes no decision): receives, per pivot
+    step, (k, m) with m the smallest relative gap between the two sides of every comparison the
+    step evaluated (the alpha tests, and the largest vs second-largest |a_ik| that fixes imax).
+    A decision another correct implementation may legitimately take the other way under a
+    different rounding order is one with a tiny m (DESIGN.md "near-tie" reading of L3)."""
     A = np.asarray(A)
     n = A.shape[0]
     a = np.tril(A).astype(np.complex128 if np.iscomplexobj(A) else np.float64)  # working copy, lower used
@@ -102,6 +114,12 @@ def bk_factor(A, perturb_delta=0.0):
             ipiv[k] = kp + 1
             k += 1
             continue
+        gaps = []
+        if margins is not None and k + 1 < n and col.size > 1:
+            top2 = np.partition(col, col.size - 2)[-2:]
+            gaps.append(_rel_gap(float(top2[1]), float(top2[0])))
+        if margins is not None:
+            gaps.append(_rel_gap(absakk, ALPHA * colmax))
         if absakk >= ALPHA * colmax:
             kp = k
         else:
@@ -115,6 +133,9 @@ def bk_factor(A, perturb_delta=0.0):
                 ipiv[k] = k + 1
                 k += 1
                 continue
+            if margins is not None:
+                gaps.append(_rel_gap(absakk, ALPHA * colmax * (colmax / rowmax)))
+                gaps.append(_rel_gap(float(cabs1(a[imax, imax])), ALPHA * rowmax))
             if absakk >= ALPHA * colmax * (colmax / rowmax):
                 kp = k
             elif float(cabs1(a[imax, imax])) >= ALPHA * rowmax:
@@ -122,6 +143,8 @@ def bk_factor(A, perturb_delta=0.0):
             else:
                 kp = imax
                 kstep = 2
+        if margins is not None:
+            margins.append((k, min(gaps) if gaps else 1.0))
         kk = k + kstep - 1
         if kp != kk:
             # symmetric interchange of indices kk < kp, lower-triangle storage:

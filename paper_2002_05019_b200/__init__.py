@@ -17,7 +17,7 @@ from typing import Optional
 import numpy as np
 
 __all__ = ["DD_REAL64", "DD_COMPLEX128", "DD_ORDER_AUTO", "DD_ORDER_ND", "DD_ORDER_MINDEG", "DD_ORDER_NATURAL",
-           "DD_ORDER_USER", "DD_OK", "DD_ZERO_PIVOT", "DDAuxError", "dd_aux_default_options", "dd_aux_analyze",
+           "DD_ORDER_USER", "DD_OK", "DD_ZERO_PIVOT", "DD_NONFINITE", "DDAuxError", "dd_aux_default_options", "dd_aux_analyze",
            "dd_aux_get_info", "dd_aux_get_order", "dd_aux_get_etree", "dd_aux_solve_work_bytes", "dd_aux_factor",
            "dd_aux_solve", "dd_aux_get_pivots", "dd_aux_destroy", "dd_aux_last_error", "dd_aux_version",
            "dd_aux_set_refine", "dd_aux_set_graphs", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_get_level_trace", "dd_aux_assemble_work_bytes", "dd_aux_assemble",
@@ -27,7 +27,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdd_aux.s
 
 DD_REAL64, DD_COMPLEX128 = 0, 1
 DD_ORDER_AUTO, DD_ORDER_ND, DD_ORDER_MINDEG, DD_ORDER_NATURAL, DD_ORDER_USER = 0, 1, 2, 3, 4
-DD_OK, DD_ZERO_PIVOT = 0, 1
+DD_OK, DD_ZERO_PIVOT, DD_NONFINITE = 0, 1, 2
 DD_ERR_CUDA, DD_ERR_WORKSPACE, DD_ERR_NOT_FACTORED, DD_ERR_SINGULAR, DD_ERR_PATTERN = -100, -101, -102, -103, -104
 
 EXPORTED_SYMBOLS = ["dd_aux_default_options", "dd_aux_analyze", "dd_aux_get_info", "dd_aux_get_order",
@@ -48,7 +48,7 @@ class DDAuxError(RuntimeError):
 class dd_aux_options(ctypes.Structure):
     _fields_ = [("order", ctypes.c_int32), ("user_order", ctypes.POINTER(ctypes.c_int32)),
                 ("refine_steps", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("refine_tol", ctypes.c_double),
-                ("complex_3m", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("complex_3m", ctypes.c_int32), ("perturb", ctypes.c_int32), ("perturb_tau", ctypes.c_double)]
 
 
 class dd_aux_info(ctypes.Structure):
@@ -63,7 +63,8 @@ class dd_aux_info(ctypes.Structure):
 class dd_aux_factor_info(ctypes.Structure):
     _fields_ = [("npos", ctypes.c_int64), ("nneg", ctypes.c_int64), ("nzero", ctypes.c_int64),
                 ("n2x2", ctypes.c_int64), ("nswaps", ctypes.c_int64), ("first_zero_pivot", ctypes.c_int64),
-                ("ms_load", ctypes.c_float), ("ms_factor", ctypes.c_float)]
+                ("ms_load", ctypes.c_float), ("ms_factor", ctypes.c_float), ("nperturbed", ctypes.c_int64),
+                ("nonfinite", ctypes.c_int64), ("max_abs_L", ctypes.c_double)]
 
 
 class dd_aux_trace(ctypes.Structure):
@@ -144,9 +145,11 @@ def dd_aux_version() -> str:
 
 
 def dd_aux_default_options(order=DD_ORDER_AUTO, refine_steps=1, user_order=None, refine_tol=None,
-                           complex_3m=True, use_graphs=False) -> dd_aux_options:
-    o = dd_aux_options()
-    _lib.dd_aux_default_options(ctypes.byref(o))
+                           complex_3m=True, use_graphs=False, perturb_tau=None) -> dd_aux_options:
+    o = dd_aux_default_options_raw()
+    if perturb_tau is not None:
+        o.perturb = 1
+        o.perturb_tau = float(perturb_tau)
     o.use_graphs = int(bool(use_graphs))
     o.order = int(order)
     o.complex_3m = int(bool(complex_3m))
@@ -158,6 +161,12 @@ def dd_aux_default_options(order=DD_ORDER_AUTO, refine_steps=1, user_order=None,
         o._user_order_keepalive = uo
         o.user_order = _np_ptr(uo, ctypes.c_int32)
         o.order = DD_ORDER_USER
+    return o
+
+
+def dd_aux_default_options_raw() -> dd_aux_options:
+    o = dd_aux_options()
+    _lib.dd_aux_default_options(ctypes.byref(o))
     return o
 
 
@@ -203,12 +212,12 @@ def dd_aux_solve_work_bytes(h, nrhs: int) -> int:
 
 
 def dd_aux_factor(h, d_vals, val_offset, d_factor, d_work, stream=None):
-    """Returns (rc, finfo dict); rc is DD_OK or DD_ZERO_PIVOT, errors raise DDAuxError."""
+    """Returns (rc, finfo dict); rc is DD_OK, DD_ZERO_PIVOT or DD_NONFINITE, errors raise DDAuxError."""
     vo = np.ascontiguousarray(val_offset, dtype=np.int64)
     fi = dd_aux_factor_info()
     rc = _lib.dd_aux_factor(h, _dev_ptr(d_vals), _np_ptr(vo, ctypes.c_int64), _dev_ptr(d_factor), _dev_ptr(d_work),
                             _stream_ptr(stream), ctypes.byref(fi))
-    _check(rc, allow=(DD_OK, DD_ZERO_PIVOT))
+    _check(rc, allow=(DD_OK, DD_ZERO_PIVOT, DD_NONFINITE))
     return rc, {f: getattr(fi, f) for f, _ in dd_aux_factor_info._fields_}
 
 
@@ -312,11 +321,13 @@ class AuxSolver:
     """
 
     def __init__(self, blk_size, colptr, rowidx, complex_=False, order=DD_ORDER_AUTO, refine_steps=1,
-                 user_order=None, device="cuda", refine_tol=None, complex_3m=True, use_graphs=False):
+                 user_order=None, device="cuda", refine_tol=None, complex_3m=True, use_graphs=False,
+                 perturb_tau=None):
         import torch
         self.torch = torch
         self.cplx = bool(complex_)
-        self.opt = dd_aux_default_options(order, refine_steps, user_order, refine_tol, complex_3m, use_graphs)
+        self.opt = dd_aux_default_options(order, refine_steps, user_order, refine_tol, complex_3m, use_graphs,
+                                          perturb_tau)
         self.h = dd_aux_analyze(blk_size, colptr, rowidx, DD_COMPLEX128 if self.cplx else DD_REAL64, self.opt)
         self._bs = np.asarray(blk_size, dtype=np.int64)
         self._rows = np.asarray(rowidx, dtype=np.int64)

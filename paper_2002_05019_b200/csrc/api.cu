@@ -296,6 +296,7 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   if (opt.order < DD_ORDER_AUTO || opt.order > DD_ORDER_USER) return fail(-6, "invalid order option");
   if (opt.refine_steps < 0) return fail(-6, "refine_steps must be >= 0");
   if (!(opt.refine_tol >= 0)) return fail(-6, "refine_tol must be >= 0");
+  if (opt.perturb && !(opt.perturb_tau > 0 && opt.perturb_tau < 1)) return fail(-6, "perturb needs 0 < perturb_tau < 1");
 
   dd_aux_handle_s* h = new (std::nothrow) dd_aux_handle_s();
   if (!h) return fail(DD_ERR_INTERNAL, "out of host memory");
@@ -464,6 +465,9 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
     // 4 CTAs/SM with per-warp masking; complex 64x32, 2 stages, 4 CTAs/SM: 3M (Gauss) by default,
     // 4M with per-warp masking when complex_3m = 0; all with 16-byte fragment loads (VEC)
     h->k3cfg = ev ? atoi(ev) : (h->cplx ? (opt.complex_3m ? 9 : 10) : 13);
+#ifndef DD_AUX_AB
+    if (h->k3cfg != 9 && h->k3cfg != 10 && h->k3cfg != 13) h->k3cfg = h->cplx ? (opt.complex_3m ? 9 : 10) : 13;
+#endif
     h->m3 = h->cplx && opt.complex_3m;
     const char* la = getenv("DD_AUX_LOOKAHEAD");
     h->lookahead = la ? atoi(la) != 0 : true;
@@ -745,10 +749,17 @@ int dd_aux_get_etree(dd_aux_handle_t h, int32_t* parent, int32_t* level, int64_t
   return DD_OK;
 }
 
+// The solve's column-indexed grids put the right-hand-side tile on gridDim.y (<= 65535): a call
+// with more columns runs in chunks of SOLVE_MAX_COLS (columns are independent, and every kernel's
+// per-column result is independent of how many columns are solved together, so chunking is
+// bitwise neutral).
+static constexpr int64_t SOLVE_MAX_COLS = 32768;
+
 int dd_aux_solve_work_bytes(dd_aux_handle_t h, int64_t nrhs, size_t* bytes) {
   if (!h) return fail(-1, "handle is NULL");
   if (nrhs < 0) return fail(-2, "nrhs must be >= 0");
   if (!bytes) return fail(-3, "bytes is NULL");
+  nrhs = std::min(nrhs, SOLVE_MAX_COLS);
   const int planes = h->cplx ? 2 : 1;
   const size_t ldy = (size_t)pad8(h->n_pad);
   size_t w = align256(ldy * (size_t)nrhs * planes * sizeof(double));   // y
@@ -859,6 +870,11 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   k1.nb = getenv("DD_AUX_K1NB") ? atoi(getenv("DD_AUX_K1NB")) : 0;
   k1.fullw = getenv("DD_AUX_K1FULLW") ? atoi(getenv("DD_AUX_K1FULLW")) : 1;
   int64_t* totals_d = (int64_t*)(F + h->off_totals);
+  unsigned long long* maxL_d = (unsigned long long*)(totals_d + 8);
+  unsigned long long* norm_d = (unsigned long long*)(F + h->off_norm);
+  k1.perturb_tau = h->opt.perturb ? h->opt.perturb_tau : 0.0;
+  k1.normA = norm_d;
+  k1.maxL = maxL_d;
   const int nLv = (int)h->lv.size();
   if (!h->side) {
     int lo, hi;
@@ -881,11 +897,23 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   }
   // a2-a6 as one enqueue function of the stream, so it can be captured once into a CUDA graph
   // (options.use_graphs; SURVEY.md §8(a) a5 "graph-capture the whole level sequence")
-  auto levels = [&](cudaStream_t st) -> int {
+  auto levels_body = [&](cudaStream_t st) -> int {
     CUDA_TRY(cudaMemsetAsync(k1.ipiv, 0, (size_t)h->n_pad * 4, st));
+    CUDA_TRY(cudaMemsetAsync(totals_d, 0, 16 * sizeof(int64_t), st));
+    if (k1.perturb_tau > 0) {  // reading L4 (opt-in): ||A||_inf of the caller's blocks before K1
+      CUDA_TRY(cudaMemsetAsync(norm_d, 0, sizeof(unsigned long long), st));
+      SpmvArgs sa{};
+      sa.rows = (const SpRow*)(F + h->off_sprows);
+      sa.segs = (const SpSeg*)(F + h->off_spsegs);
+      sa.blk_size = (const int64_t*)(F + h->off_blksize);
+      sa.odof = (const int64_t*)(F + h->off_odof);
+      sa.vals = (const double*)d_vals;
+      launch_norm_a(C, sa, h->n_sprows, norm_d, st);
+      LAUNCH_CHECK("k_norm_a");
+    }
     RowpermArgs rp{(const RowPerm*)(F + h->off_rowperm), dnodes, arena, aim, k1.perm};
-    K2Args k2{(const Tile*)(F + h->off_k2items), (const Strip*)(F + h->off_strips), dnodes, arena, aim, work, wim,
-              k1.perm, k1.ipiv, h->d_off, h->e_off};
+    K2Args k2{maxL_d, (const Tile*)(F + h->off_k2items), (const Strip*)(F + h->off_strips), dnodes, arena, aim, work,
+              wim, k1.perm, k1.ipiv, h->d_off, h->e_off};
     K3Args k3{(const UpdTarget*)(F + h->off_targets), (const int64_t*)(F + h->off_tiles), 0, 0,
               (const UpdContrib*)(F + h->off_contribs), dnodes, arena, aim, work, wim};
     const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
@@ -1018,10 +1046,21 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     // ---- a6: statistics
       {
       TraceScope ts(h, DD_PH_STATS, 0.0, st);
-      launch_k4((const int64_t*)(F + h->off_stats), N, totals_d, st);
+      launch_k4((const int64_t*)(F + h->off_stats), N, k1.gperm, totals_d, st);
     }
     LAUNCH_CHECK("k4_stats");
     return DD_OK;
+  };
+  // on an error part-way through, join the side streams into the caller's stream before returning,
+  // so no queued lookahead kernel can outlive the caller's buffers (the caller may free them)
+  auto levels = [&](cudaStream_t st) -> int {
+    const int rc = levels_body(st);
+    if (rc && h->lookahead)
+      for (cudaStream_t x : {h->side, h->side2}) {
+        cudaEventRecord(h->evR, x);
+        cudaStreamWaitEvent(st, h->evR, 0);
+      }
+    return rc;
   };
   {
     const std::vector<uintptr_t> key = {(uintptr_t)d_factor, (uintptr_t)d_work};
@@ -1030,7 +1069,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   }
   cudaEventRecord(e2, st);
   int64_t totals[16] = {0};
-  CUDA_TRY(cudaMemcpyAsync(totals, totals_d, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(totals, totals_d, 9 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   float ms_load = 0, ms_fac = 0;
   cudaEventElapsedTime(&ms_load, e0, e1);
@@ -1044,11 +1083,17 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     finfo->first_zero_pivot = totals[5];
     finfo->ms_load = ms_load;
     finfo->ms_factor = ms_fac;
+    finfo->nperturbed = totals[6];
+    finfo->nonfinite = totals[7];
+    double ml;
+    std::memcpy(&ml, &totals[8], sizeof(double));
+    finfo->max_abs_L = ml;
   }
   h->factored = true;
   h->factored_ptr = d_factor;
   h->singular = totals[5] != 0;
-  return h->singular ? DD_ZERO_PIVOT : DD_OK;
+  if (h->opt.perturb) h->norm_valid = true;  // ||A||_inf of these values is on the device now
+  return totals[7] ? DD_NONFINITE : (h->singular ? DD_ZERO_PIVOT : DD_OK);
 }
 
 static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t yim, int64_t ldy, int nrhs,
@@ -1138,7 +1183,17 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
   if (h->singular) return fail(DD_ERR_SINGULAR, "the factorization reported a zero pivot");
   const int refine = h->opt.refine_steps;
   if (refine > 0 && !d_vals) return fail(-3, "d_vals is NULL but refine_steps > 0");
-  if (nrhs > (1 << 30)) return fail(-4, "nrhs too large");
+  if (nrhs > SOLVE_MAX_COLS) {  // column chunks (direct launches; see SOLVE_MAX_COLS)
+    const int g = h->opt.use_graphs;
+    h->opt.use_graphs = 0;
+    int rc = DD_OK;
+    const size_t es = h->cplx ? 16 : 8;
+    for (int64_t c0 = 0; c0 < nrhs && rc == DD_OK; c0 += SOLVE_MAX_COLS)
+      rc = dd_aux_solve(h, d_factor, d_vals, std::min(SOLVE_MAX_COLS, nrhs - c0), (uint8_t*)d_B + (size_t)c0 * ldb * es,
+                        ldb, d_work, stream);
+    h->opt.use_graphs = g;
+    return rc;
+  }
   cudaStream_t st0 = (cudaStream_t)stream;
   const bool in_graph = h->opt.use_graphs && !h->trace;
   auto body = [&](cudaStream_t st) -> int {

@@ -29,8 +29,7 @@ namespace ddk {
 template <bool C>
 __global__ void k0_load(const double* __restrict__ vals, const LoadBlock* __restrict__ lb, int nblocks,
                         double* __restrict__ arena, int64_t aim) {
-  int b = blockIdx.y;
-  if (b >= nblocks) return;
+  for (int b = blockIdx.y; b < nblocks; b += gridDim.y) {  // grid-stride over blocks (gridDim.y <= 65535)
   LoadBlock L = lb[b];
   const int64_t total = (int64_t)L.rows * L.cols;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -47,6 +46,7 @@ __global__ void k0_load(const double* __restrict__ vals, const LoadBlock* __rest
     int64_t dst = L.trans ? (L.dst + c + r * L.ld) : (L.dst + r + c * L.ld);
     arena[dst] = re;
     if (C) arena[dst + aim] = im;
+  }
   }
 }
 
@@ -74,6 +74,27 @@ __host__ __device__ inline int k1_panel_nb(int s, bool cplx, int req, bool fullw
 // rows per thread: s <= NT1 * MAXQ (4 -> 1024 on the fast path, 16 -> 4096 for larger interfaces)
 using K1GemmR = Gemm<64, 64, 16, 2, NT1 / 64, 2, false, false, false>;
 using K1GemmC = Gemm<64, 64, 16, 2, NT1 / 64, 2, true, false, false>;
+
+// pivot-search magnitude with non-finite values mapped to +Inf (reading L4b): a NaN would be
+// invisible to the (value desc, index asc) max reduction; as +Inf it makes colmax / rowmax non-finite
+template <bool C>
+__device__ __forceinline__ double mag_nf(cz v) {
+  const double a = cabs1<C>(v);
+  return a <= 1.79769313486231570e308 ? a : __longlong_as_double(0x7ff0000000000000LL);
+}
+__device__ __forceinline__ bool finite_d(double x) { return x <= 1.79769313486231570e308; }
+
+// max |L| of the calling thread's values -> one atomicMax per warp on the factor-wide slot
+__device__ __forceinline__ void warp_max_to(unsigned long long* slot, double m) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0 && slot) atomicMax(slot, (unsigned long long)__double_as_longlong(m));
+}
+template <bool C>
+__device__ __forceinline__ double modulus(cz v) {
+  if constexpr (C) return hypot(v.r, v.i);
+  else return fabs(v.r);
+}
 
 __device__ __forceinline__ void warp_argmax(double& v, int& i) {
 #pragma unroll
@@ -121,7 +142,8 @@ __device__ __forceinline__ void block_argmax(double& v, int& i, double (*shv)[NT
 // maps and the per-node statistics (inertia from D for real matrices, a6).
 template <bool C>
 __device__ void k1_finish(const K1Args& a, int t, const NodeDev& nd, double* A, double* smem, const int* perm,
-                          const int* ipiv, const double* dv_, const double* ev_, int n2x2, int nswap, int zero_col) {
+                          const int* ipiv, const double* dv_, const double* ev_, int n2x2, int nswap, int zero_col,
+                          int nperturbed = 0, int nonfinite = 0) {
   const int s = nd.s;
   const int64_t ldA = nd.ld, aim = a.aim;
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -205,9 +227,11 @@ __device__ void k1_finish(const K1Args& a, int t, const NodeDev& nd, double* A, 
     S[2] = nz;
     S[3] = n2x2;
     S[4] = nswap;
-    S[5] = zero_col >= 0 ? nd.odof + perm[zero_col] + 1 : 0;
-    S[6] = 0;
-    S[7] = 0;
+    // first zero / non-finite pivot as an ELIMINATION-order key (padded position row + 1); k4 takes
+    // the minimum over nodes and maps it to the original DoF through gperm (LAPACK INFO order)
+    S[5] = zero_col >= 0 ? nd.ydof + zero_col + 1 : 0;
+    S[6] = nperturbed;
+    S[7] = nonfinite;
   }
 }
 
@@ -243,7 +267,8 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
   auto Wel = [&](int i, int m) { return (int64_t)i + (int64_t)m * ldW; };
 
   for (int i = tid; i < s; i += NT1) perm[i] = i;
-  int n2x2 = 0, nswap = 0, zero_col = -1;
+  int n2x2 = 0, nswap = 0, zero_col = -1, nonfinite = 0, nperturbed = 0;
+  double maxl = 0.0;  // max |L| of the entries this thread writes (SURVEY.md §8(b) max_abs_L)
   __syncthreads();
 
   // Panel width NB: the current panel's L columns live in shared memory (Lp, <= K1_LP_BUDGET
@@ -324,7 +349,7 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           wtr[(i - c0) * WLD + (kk)] = v.r;
           if constexpr (C) wti[(i - c0) * WLD + (kk)] = v.i;
         }
-        double av = cabs1<C>(v);
+        double av = mag_nf<C>(v);
         if (i == k) s_absakk2[k & 1] = av;
         else if (av > bv) {
           bv = av;
@@ -337,9 +362,12 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
       const double colmax = bv > 0.0 ? bv : 0.0;
       const int imax = bi;
       int kp, kstep = 1;
-      bool zero = false;
-      if (fmax(absakk, colmax) == 0.0) {
-        zero = true;
+      bool zero = false, nonfin = !finite_d(absakk) || !finite_d(colmax), perturbed = false;
+      if (!nonfin && fmax(absakk, colmax) == 0.0 && a.perturb_tau > 0.0) {
+        perturbed = true;  // reading L4 (opt-in): 1x1 pivot d = tau * ||A||_inf, no swap
+        kp = k;
+      } else if (nonfin || fmax(absakk, colmax) == 0.0) {
+        zero = true;  // LAPACK: zero (or, L4b, non-finite) pivot column, no elimination
         kp = k;
       } else if (absakk >= alpha * colmax) {
         kp = k;
@@ -379,7 +407,7 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
             if constexpr (C) wti[(i - c0) * WLD + (kk + 1)] = v.i;
           }
           if (i != imax) {
-            double av = cabs1<C>(v);
+            double av = mag_nf<C>(v);
             if (av > rv) {
               rv = av;
               ri = i;
@@ -388,7 +416,10 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
         }
         block_argmax(rv, ri, shv, shi, aslot);
         const double rowmax = rv;
-        if (absakk >= alpha * colmax * (colmax / rowmax)) {
+        if (!finite_d(rowmax)) {  // L4b: the imax row holds a non-finite value
+          zero = nonfin = true;
+          kp = k;
+        } else if (absakk >= alpha * colmax * (colmax / rowmax)) {
           kp = k;
         } else {
           const double aii = cabs1<C>(inwin ? mk(wtr[(imax - c0) * WLD + (kk + 1)], C ? wti[(imax - c0) * WLD + (kk + 1)] : 0.0)
@@ -484,7 +515,8 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
       }
       // ---- L columns (shared panel copy) and D; the next column is prefetched
       if (kstep == 1) {
-        const cz D = mk(wtr[(kk) * WLD + (kk)], C ? wti[(kk) * WLD + (kk)] : 0.0);
+        const cz D = perturbed ? mk(a.perturb_tau * __longlong_as_double((long long)*a.normA), 0.0)
+                               : mk(wtr[(kk) * WLD + (kk)], C ? wti[(kk) * WLD + (kk)] : 0.0);
         const cz rD = zero ? mk(1.0, 0.0) : dv<C>(mk(1.0, 0.0), D);
 #pragma unroll
         for (int q = 0; q < K1_MAXQ; ++q) {
@@ -499,6 +531,8 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
           st<C>(ev_, 0 + k, aim, mk(0.0, 0.0));
           ipiv[k] = kp + 1;
           if (zero && zero_col < 0) zero_col = k;
+          nonfinite += nonfin;
+          nperturbed += perturbed;
           if (kp != k) ++nswap;
         }
       } else {
@@ -555,8 +589,11 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
       // the panel's L columns and D diagonal to global memory
       for (int m = 0; m < kb; ++m) {
         const int col = c0 + m;
-        for (int i = col + 1 + tid; i < s; i += NT1)
-          st<C>(A, Ael(i, col), aim, mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0));
+        for (int i = col + 1 + tid; i < s; i += NT1) {
+          const cz l = mk(Lpr[LP(i, m)], C ? Lpi[LP(i, m)] : 0.0);
+          maxl = fmax(maxl, modulus<C>(l));
+          st<C>(A, Ael(i, col), aim, l);
+        }
         if (tid == 0) st<C>(A, Ael(col, col), aim, ld<C>(dv_, col, aim));
       }
       // deferred interchanges in the L columns of earlier panels (in pivot order)
@@ -614,9 +651,11 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
     }
   }
 
-  k1_finish<C>(a, t, nd, A, smem, perm, ipiv, dv_, ev_, n2x2, nswap, zero_col);
+  warp_max_to(a.maxL, fmax(maxl, 1.0));  // unit diagonal included
+  k1_finish<C>(a, t, nd, A, smem, perm, ipiv, dv_, ev_, n2x2, nswap, zero_col, nperturbed, nonfinite);
 }
 
+#ifdef DD_AUX_AB  // A/B-only variant (measured slower; not in the default build)
 // ============================================================================ K1, warp variant
 // For small diagonal blocks (real s <= 256, complex s <= 128) the column loop runs on ONE warp
 // with the panel's L and W entirely in shared memory: argmax by shuffles, __syncwarp only, no
@@ -923,6 +962,8 @@ size_t k1w_smem(bool cplx, int max_s) {
   return std::max(lp, std::max(g, inv));
 }
 
+#endif  // DD_AUX_AB
+
 // ============================================================================ full inverse of L_tt
 // X = L_tt^{-1} (unit lower) by column tiles of width TB, one CTA per (node, column tile c):
 //   X_cc = Linv_cc (the K1 tile inverse);  X_pc = -Linv_pp * sum_{q=c}^{p-1} L_pq X_qc  (p > c)
@@ -988,8 +1029,9 @@ __global__ void __launch_bounds__(128) k_linv(LinvArgs a) {
 // ============================================================================ row permutation
 // rows [ro, ro + s_t) of panel k are block t's rows of L_tk; reorder them by perm_t.
 template <bool C>
-__global__ void k_rowperm(RowpermArgs a) {
-  const RowPerm R = a.list[blockIdx.y];
+__global__ void k_rowperm(RowpermArgs a, int nlist) {
+  for (int li = blockIdx.y; li < nlist; li += gridDim.y) {  // grid-stride (gridDim.y <= 65535)
+  const RowPerm R = a.list[li];
   const NodeDev nt = a.nd[R.t];
   const NodeDev nk = a.nd[R.k];
   const int s = nt.s;
@@ -1011,6 +1053,7 @@ __global__ void k_rowperm(RowpermArgs a) {
     }
     __syncwarp();
   }
+  }
 }
 
 // ============================================================================ K3 Schur update
@@ -1020,101 +1063,137 @@ __global__ void k_rowperm(RowpermArgs a) {
 //      overlap the MMA of the other)
 template <bool C, int CFG>
 struct K3Cfg;
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<false, 0> {
   using G = Gemm<128, 128, 16, 2, 4, 4, false, false, false>;
   static constexpr int NT = 256, BM = 128, BN = 128, MINB = 1;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<true, 0> {
   using G = Gemm<64, 128, 16, 2, 4, 3, true, false, false>;
   static constexpr int NT = 256, BM = 64, BN = 128, MINB = 1;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<false, 1> {
   using G = Gemm<128, 64, 16, 2, 2, 3, false, false, false>;
   static constexpr int NT = 128, BM = 128, BN = 64, MINB = 2;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<true, 1> {
   using G = Gemm<64, 64, 16, 2, 2, 3, true, false, false>;
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 2;
 };
+#endif
 
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<false, 2> {  // real 128x64, 4 stages (deeper prefetch for DRAM-resident W panels)
   using G = Gemm<128, 64, 16, 2, 2, 4, false, false, false>;
   static constexpr int NT = 128, BM = 128, BN = 64, MINB = 2;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<true, 2> {
   using G = Gemm<64, 64, 16, 2, 2, 4, true, false, false>;
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 1;
 };
+#endif
 
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<false, 3> {  // real 128x64, register-capped for 3 CTAs per SM (12 warps)
   using G = Gemm<128, 64, 16, 2, 2, 3, false, false, false>;
   static constexpr int NT = 128, BM = 128, BN = 64, MINB = 3;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<true, 3> {
   using G = Gemm<64, 64, 16, 2, 2, 3, true, false, false>;
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 2;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<false, 4> {  // real 64x64, 4 CTAs per SM (16 warps), least ragged-tile padding
   using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false>;
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<true, 4> {
   using G = Gemm<64, 64, 16, 2, 2, 3, true, false, false>;
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 2;
 };
+#endif
 
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<false, 5> {  // real 64x32, 3 stages, 5 CTAs per SM
   using G = Gemm<64, 32, 16, 2, 2, 3, false, false, false>;
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 5;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<true, 5> {  // complex 64x32, 2 stages, 4 CTAs per SM (dense microbench: 94% of ZGEMM)
   using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false>;
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
+#endif
 
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<false, 6> {
   using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false>;
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<true, 6> {  // complex 64x32 3M (Gauss): 3 real DMMA products per complex product
   using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true>;
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
+#endif
 
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<false, 7> {  // real 64x64, coarse (per-warp) masking
   using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false>;
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<true, 7> {  // complex 64x32 4M, coarse masking
   using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, false, false>;
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<false, 8> {
   using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false>;
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<true, 8> {  // complex 64x32 3M, coarse masking
   using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, false>;
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
+#endif
 
 template <>
 struct K3Cfg<false, 9> {  // real 64x64, coarse masking, vectorised (16-byte) fragment loads
@@ -1137,26 +1216,34 @@ struct K3Cfg<true, 10> {  // complex 64x32 4M, coarse masking, vectorised fragme
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
 
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<false, 11> {  // real 64x64, VEC, rectangular 16x16-granular edge masking (RECT)
   using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false, true, true>;
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<true, 11> {  // complex 64x32 3M, VEC, RECT
   using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, false, true, true>;
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<false, 12> {  // real 64x64, scalar fragments, RECT (16x8-granular)
   using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false, false, true>;
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<true, 12> {  // complex 64x32 4M, VEC, RECT
   using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, false, false, true, true>;
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
+#endif
 
 template <>
 struct K3Cfg<false, 13> {  // real 64x64, RECT, 2 stages (34 KB smem; dense microbench +1.5% at K=576)
@@ -1169,27 +1256,35 @@ struct K3Cfg<true, 13> {  // complex 64x32 3M, 2 stages, coarse masking (no per-
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
 
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<false, 14> {  // real 64x64, RECT, 3 stages, mbarrier pipeline (no CTA barrier per stage)
   using G = Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false, false, true, true>;
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<true, 14> {  // complex 64x32 3M VEC, 3 stages, mbarrier pipeline
   using G = Gemm<64, 32, 16, 2, 2, 3, true, false, false, true, true, true, false, true>;
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 3;
 };
+#endif
 
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<false, 15> {  // cfg 13 register-capped for 5 CTAs per SM (20 warps)
   using G = Gemm<64, 64, 16, 2, 2, 2, false, false, false, false, false, false, true>;
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 5;
 };
+#endif
+#ifdef DD_AUX_AB
 template <>
 struct K3Cfg<true, 15> {  // complex 64x32 3M VEC, 5 CTAs per SM
   using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, true, true>;
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 5;
 };
+#endif
 
 template <bool C, int CFG>
 __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_update(K3Args a) {
@@ -1309,6 +1404,7 @@ __global__ void __launch_bounds__(NT2) k2_dinv(K2Args a) {
   const double* dv_ = a.arena + a.d_off + nd.ydof;
   const double* ev_ = a.arena + a.e_off + nd.ydof;
   const int* ipiv = a.ipiv + nd.ydof;
+  double maxl = 0.0;
   for (int c = blockIdx.y; c < s; c += gridDim.y) {
     const bool two = ipiv[c] < 0;
     // a 2x2 pivot is only taken when colmax > 0, so e != 0 exactly on the first column of a pair
@@ -1329,22 +1425,27 @@ __global__ void __launch_bounds__(NT2) k2_dinv(K2Args a) {
         const cz s21 = dv<C>(tt, d21);
         out = (c == c1) ? mul<C>(s21, mul<C>(a11, wk) - wk1) : mul<C>(s21, mul<C>(a22, wk1) - wk);
       }
+      maxl = fmax(maxl, modulus<C>(out));
       st<C>(Ahat, (int64_t)r + (int64_t)c * ldA, aim, out);
     }
   }
+  warp_max_to(a.maxL, maxl);
 }
 
 // ============================================================================ K4 stats
-__global__ void k4_stats(const int64_t* __restrict__ node_stats, int nnodes, int64_t* __restrict__ out) {
-  __shared__ int64_t sh[8][8];
-  int64_t acc[6] = {0, 0, 0, 0, 0, INT64_MAX};
+__global__ void k4_stats(const int64_t* __restrict__ node_stats, int nnodes, const int* __restrict__ gperm,
+                         int64_t* __restrict__ out) {
+  constexpr int NQ = 8;  // npos, nneg, nzero, n2x2, nswaps, first-zero key (min), nperturbed, nonfinite
+  __shared__ int64_t sh[8][NQ];
+  int64_t acc[NQ] = {0, 0, 0, 0, 0, INT64_MAX, 0, 0};
   for (int t = threadIdx.x; t < nnodes; t += blockDim.x) {
     const int64_t* S = node_stats + (int64_t)t * 8;
-    for (int q = 0; q < 5; ++q) acc[q] += S[q];
-    if (S[5] > 0 && S[5] < acc[5]) acc[5] = S[5];  // NOTE: smallest original DoF among zero pivots
+    for (int q = 0; q < NQ; ++q)
+      if (q != 5) acc[q] += S[q];
+    if (S[5] > 0 && S[5] < acc[5]) acc[5] = S[5];  // elimination-order key of the first zero pivot
   }
   // simple two-level reduction (256 threads)
-  for (int q = 0; q < 6; ++q) {
+  for (int q = 0; q < NQ; ++q) {
     int64_t v = acc[q];
     for (int o = 16; o; o >>= 1) {
       int64_t u = __shfl_xor_sync(0xffffffffu, v, o);
@@ -1354,11 +1455,12 @@ __global__ void k4_stats(const int64_t* __restrict__ node_stats, int nnodes, int
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int64_t r[6] = {0, 0, 0, 0, 0, INT64_MAX};
+    int64_t r[NQ] = {0, 0, 0, 0, 0, INT64_MAX, 0, 0};
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
-      for (int q = 0; q < 6; ++q) r[q] = (q == 5) ? (sh[w][q] < r[q] ? sh[w][q] : r[q]) : r[q] + sh[w][q];
-    for (int q = 0; q < 5; ++q) out[q] = r[q];
-    out[5] = r[5] == INT64_MAX ? 0 : r[5];
+      for (int q = 0; q < NQ; ++q) r[q] = (q == 5) ? (sh[w][q] < r[q] ? sh[w][q] : r[q]) : r[q] + sh[w][q];
+    for (int q = 0; q < NQ; ++q) out[q] = r[q];
+    // position row -> 1 + original DoF (gperm is final once every level's K1 has run)
+    out[5] = r[5] == INT64_MAX ? 0 : (int64_t)gperm[r[5] - 1] + 1;
   }
 }
 
@@ -1372,7 +1474,7 @@ void launch_load(bool cplx, const double* vals, const LoadBlock* lb, int nblocks
                  int64_t aim, cudaStream_t st) {
   if (nblocks == 0) return;
   int gx = (int)std::min<int64_t>((max_elems + 255) / 256, 64);
-  dim3 grid(gx, nblocks);
+  dim3 grid(gx, std::min(nblocks, 65535));
   if (cplx) k0_load<true><<<grid, 256, 0, st>>>(vals, lb, nblocks, arena, aim);
   else k0_load<false><<<grid, 256, 0, st>>>(vals, lb, nblocks, arena, aim);
 }
@@ -1396,6 +1498,7 @@ static void launch_k1_t(const K1Args& a, int nnodes, int max_s, cudaStream_t st)
 void launch_k1(bool cplx, const K1Args& a, int nnodes, int max_s, cudaStream_t st) {
   // warp variant: opt-in (DD_AUX_K1WARP=1); measured slower than the 256-thread kernel on cfg1
   // (59 vs 42 ms), kept for the next round's latency work
+#ifdef DD_AUX_AB
   static const bool warp = getenv("DD_AUX_K1WARP") && atoi(getenv("DD_AUX_K1WARP"));
   if (warp && max_s <= (cplx ? 128 : 256)) {
     const size_t sm = k1w_smem(cplx, max_s);
@@ -1408,6 +1511,7 @@ void launch_k1(bool cplx, const K1Args& a, int nnodes, int max_s, cudaStream_t s
     }
     return;
   }
+#endif
   // rows per thread sized to the level's largest block: the per-row loops are unrolled over
   // K1_MAXQ, so a tighter bound removes dead per-column work for small interfaces
   static const int maxq_env = getenv("DD_AUX_K1MAXQ") ? atoi(getenv("DD_AUX_K1MAXQ")) : 0;
@@ -1440,13 +1544,18 @@ void launch_linv(bool cplx, const LinvArgs& a, int nitems, cudaStream_t st) {
 void launch_rowperm(bool cplx, const RowpermArgs& a, int nlist, int max_s, cudaStream_t st) {
   if (nlist == 0) return;
   size_t sm = (size_t)4 * 2 * max_s * sizeof(double);  // 4 warps
-  dim3 grid(8, nlist);
+  dim3 grid(8, std::min(nlist, 65535));
+  // the attribute is set once to the largest size any handle can need (a replayed CUDA graph is
+  // checked against the attribute's value at replay time); each launch uses its own size
+  const size_t sm_max = (size_t)4 * 2 * K1_MAX_BLOCK * sizeof(double);
   if (cplx) {
-    set_smem(k_rowperm<true>, sm);
-    k_rowperm<true><<<grid, 128, sm, st>>>(a);
+    static bool once = (set_smem(k_rowperm<true>, sm_max), true);
+    (void)once;
+    k_rowperm<true><<<grid, 128, sm, st>>>(a, nlist);
   } else {
-    set_smem(k_rowperm<false>, sm);
-    k_rowperm<false><<<grid, 128, sm, st>>>(a);
+    static bool once = (set_smem(k_rowperm<false>, sm_max), true);
+    (void)once;
+    k_rowperm<false><<<grid, 128, sm, st>>>(a, nlist);
   }
 }
 
@@ -1457,42 +1566,90 @@ static int bn_of(bool cplx) { return cplx ? K3Cfg<true, CFG>::BN : K3Cfg<false, 
 
 int k3_bm(bool cplx, int cfg) {
   switch (cfg) {
+#ifdef DD_AUX_AB
     case 0: return bm_of<0>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 2: return bm_of<2>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 3: return bm_of<3>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 4: return bm_of<4>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 5: return bm_of<5>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 6: return bm_of<6>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 7: return bm_of<7>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 8: return bm_of<8>(cplx);
+#endif
     case 9: return bm_of<9>(cplx);
     case 10: return bm_of<10>(cplx);
+#ifdef DD_AUX_AB
     case 11: return bm_of<11>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 12: return bm_of<12>(cplx);
+#endif
     case 13: return bm_of<13>(cplx);
+#ifdef DD_AUX_AB
     case 14: return bm_of<14>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 15: return bm_of<15>(cplx);
-    default: return bm_of<1>(cplx);
+#endif
+    default: return bm_of<13>(cplx);
   }
 }
 int k3_bn(bool cplx, int cfg) {
   switch (cfg) {
+#ifdef DD_AUX_AB
     case 0: return bn_of<0>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 2: return bn_of<2>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 3: return bn_of<3>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 4: return bn_of<4>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 5: return bn_of<5>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 6: return bn_of<6>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 7: return bn_of<7>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 8: return bn_of<8>(cplx);
+#endif
     case 9: return bn_of<9>(cplx);
     case 10: return bn_of<10>(cplx);
+#ifdef DD_AUX_AB
     case 11: return bn_of<11>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 12: return bn_of<12>(cplx);
+#endif
     case 13: return bn_of<13>(cplx);
+#ifdef DD_AUX_AB
     case 14: return bn_of<14>(cplx);
+#endif
+#ifdef DD_AUX_AB
     case 15: return bn_of<15>(cplx);
-    default: return bn_of<1>(cplx);
+#endif
+    default: return bn_of<13>(cplx);
   }
 }
 
@@ -1512,22 +1669,46 @@ static void launch_k3_c(bool cplx, const K3Args& a, int ntiles, cudaStream_t st)
 void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st) {
   if (ntiles == 0) return;
   switch (cfg) {
+#ifdef DD_AUX_AB
     case 0: launch_k3_c<0>(cplx, a, ntiles, st); break;
+#endif
+#ifdef DD_AUX_AB
     case 2: launch_k3_c<2>(cplx, a, ntiles, st); break;
+#endif
+#ifdef DD_AUX_AB
     case 3: launch_k3_c<3>(cplx, a, ntiles, st); break;
+#endif
+#ifdef DD_AUX_AB
     case 4: launch_k3_c<4>(cplx, a, ntiles, st); break;
+#endif
+#ifdef DD_AUX_AB
     case 5: launch_k3_c<5>(cplx, a, ntiles, st); break;
+#endif
+#ifdef DD_AUX_AB
     case 6: launch_k3_c<6>(cplx, a, ntiles, st); break;
+#endif
+#ifdef DD_AUX_AB
     case 7: launch_k3_c<7>(cplx, a, ntiles, st); break;
+#endif
+#ifdef DD_AUX_AB
     case 8: launch_k3_c<8>(cplx, a, ntiles, st); break;
+#endif
     case 9: launch_k3_c<9>(cplx, a, ntiles, st); break;
     case 10: launch_k3_c<10>(cplx, a, ntiles, st); break;
+#ifdef DD_AUX_AB
     case 11: launch_k3_c<11>(cplx, a, ntiles, st); break;
+#endif
+#ifdef DD_AUX_AB
     case 12: launch_k3_c<12>(cplx, a, ntiles, st); break;
+#endif
     case 13: launch_k3_c<13>(cplx, a, ntiles, st); break;
+#ifdef DD_AUX_AB
     case 14: launch_k3_c<14>(cplx, a, ntiles, st); break;
+#endif
+#ifdef DD_AUX_AB
     case 15: launch_k3_c<15>(cplx, a, ntiles, st); break;
-    default: launch_k3_c<1>(cplx, a, ntiles, st); break;
+#endif
+    default: launch_k3_c<13>(cplx, a, ntiles, st); break;
   }
 }
 
@@ -1546,14 +1727,26 @@ void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, int
     switch (cfg) {  // same tile shapes as the Schur update
       case 9: cplx ? launch_k2_t<true, 9>(a, nitems, max_s, st) : launch_k2_t<false, 9>(a, nitems, max_s, st); break;
       case 10: cplx ? launch_k2_t<true, 10>(a, nitems, max_s, st) : launch_k2_t<false, 10>(a, nitems, max_s, st); break;
+#ifdef DD_AUX_AB
       case 11: cplx ? launch_k2_t<true, 11>(a, nitems, max_s, st) : launch_k2_t<false, 11>(a, nitems, max_s, st); break;
+#endif
+#ifdef DD_AUX_AB
       case 12: cplx ? launch_k2_t<true, 12>(a, nitems, max_s, st) : launch_k2_t<false, 12>(a, nitems, max_s, st); break;
+#endif
       case 13: cplx ? launch_k2_t<true, 13>(a, nitems, max_s, st) : launch_k2_t<false, 13>(a, nitems, max_s, st); break;
+#ifdef DD_AUX_AB
       case 6: cplx ? launch_k2_t<true, 6>(a, nitems, max_s, st) : launch_k2_t<false, 6>(a, nitems, max_s, st); break;
+#endif
+#ifdef DD_AUX_AB
       case 5: cplx ? launch_k2_t<true, 5>(a, nitems, max_s, st) : launch_k2_t<false, 5>(a, nitems, max_s, st); break;
+#endif
+#ifdef DD_AUX_AB
       case 4: cplx ? launch_k2_t<true, 4>(a, nitems, max_s, st) : launch_k2_t<false, 4>(a, nitems, max_s, st); break;
+#endif
+#ifdef DD_AUX_AB
       case 1: cplx ? launch_k2_t<true, 1>(a, nitems, max_s, st) : launch_k2_t<false, 1>(a, nitems, max_s, st); break;
-      default: cplx ? launch_k2_t<true, 7>(a, nitems, max_s, st) : launch_k2_t<false, 7>(a, nitems, max_s, st); break;
+#endif
+      default: cplx ? launch_k2_t<true, 13>(a, nitems, max_s, st) : launch_k2_t<false, 13>(a, nitems, max_s, st); break;
     }
   }
   if (nstrips > 0) {
@@ -1563,8 +1756,8 @@ void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, int
   }
 }
 
-void launch_k4(const int64_t* node_stats, int nnodes, int64_t* out, cudaStream_t st) {
-  k4_stats<<<1, 256, 0, st>>>(node_stats, nnodes, out);
+void launch_k4(const int64_t* node_stats, int nnodes, const int* gperm, int64_t* out, cudaStream_t st) {
+  k4_stats<<<1, 256, 0, st>>>(node_stats, nnodes, gperm, out);
 }
 
 }  // namespace ddk

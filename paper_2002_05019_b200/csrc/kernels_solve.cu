@@ -693,6 +693,7 @@ template <bool C, bool M3>
 static void bupd_t(const SolveArgs& a, int ntiles, int G, double* part, int64_t pim, bool cluster, cudaStream_t st) {
   using GB = typename SolveG<C, M3>::BU;
   dim3 grid(ntiles * G, ntn(C, a.nrhs));
+#ifdef DD_AUX_AB
   if (cluster && G > 1) {
     set_smem(k_bupd<C, M3, true>, GB::SMEM_BYTES);
     cudaLaunchConfig_t cfg{};
@@ -710,6 +711,9 @@ static void bupd_t(const SolveArgs& a, int ntiles, int G, double* part, int64_t 
     cudaLaunchKernelEx(&cfg, k_bupd<C, M3, true>, a, G, part, pim);
     return;
   }
+#else
+  (void)cluster;
+#endif
   set_smem(k_bupd<C, M3, false>, GB::SMEM_BYTES);
   k_bupd<C, M3, false><<<grid, 128, GB::SMEM_BYTES, st>>>(a, G, part, pim);
 }
@@ -720,7 +724,11 @@ void launch_bupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, int max_rp,
   // thread-block cluster with distributed shared memory (DD_AUX_BUPD_CLUSTER=1, G capped at 8):
   // correct but measured slower -- cfg3 backward update 1518 -> 1620 ms, cfg2 528 -> 625 ms per
   // step (the cap on G costs more parallelism than the saved partial round trip gains)
+#ifdef DD_AUX_AB
   static const bool cluster = getenv("DD_AUX_BUPD_CLUSTER") && atoi(getenv("DD_AUX_BUPD_CLUSTER")) == 1;
+#else
+  constexpr bool cluster = false;
+#endif
   int G = part ? bupd_split(cplx, ntiles, a.nrhs, max_rp) : 1;
   if (cluster) G = std::min(G, 8);
   const int64_t pim = (int64_t)BUPD_MAX_PARTS * SUBM * a.nrhs;

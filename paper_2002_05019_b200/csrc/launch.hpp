@@ -32,6 +32,11 @@ struct K1Args {
   int64_t* stats;
   int nb;  // K1 panel width override (0 = automatic; env DD_AUX_K1NB, A/B only)
   int fullw;  // 1: whole-block W cache when it fits with a >= 32-column panel (env DD_AUX_K1FULLW=0 off)
+  // reading L4 (opt-in): an exactly-zero pivot column gets d = perturb_tau * ||A||_inf, with
+  // ||A||_inf read from *normA (bits of a double, computed on the device before K1); 0 = off
+  double perturb_tau;
+  const unsigned long long* normA;
+  unsigned long long* maxL;  // atomicMax of max |L_ij| (bits of a non-negative double)
 };
 
 struct RowpermArgs {
@@ -43,6 +48,7 @@ struct RowpermArgs {
 };
 
 struct K2Args {
+  unsigned long long* maxL;  // atomicMax of max |L_ik| (bits of a non-negative double)
   const Tile* items;      // GEMM tiles (node, row strip, column tile)
   const Strip* strips;    // row strips for L = W D^{-1}
   const NodeDev* nd;
@@ -164,7 +170,9 @@ void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, int
 int k3_bm(bool cplx, int cfg);
 int k3_bn(bool cplx, int cfg);
 void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st);
-void launch_k4(const int64_t* node_stats, int nnodes, int64_t* out, cudaStream_t st);
+// totals: [npos, nneg, nzero, n2x2, nswaps, first zero/non-finite pivot (1 + original DoF, in
+// elimination order; 0 = none), nperturbed, nonfinite]
+void launch_k4(const int64_t* node_stats, int nnodes, const int* gperm, int64_t* out, cudaStream_t st);
 
 int solve_bm(bool cplx);   // row tile of the forward/backward update kernels
 void launch_perm_in(bool cplx, const PermArgs& a, cudaStream_t st);

@@ -7,13 +7,13 @@ def to_dev_colmajor(B, torch):
     return torch.from_numpy(np.ascontiguousarray(B.T)).cuda().t()
 
 
-def run_gpu(p, B, *, order=None, user_order=None, refine=1, keep=False):
+def run_gpu(p, B, *, order=None, user_order=None, refine=1, keep=False, perturb_tau=None):
     """Factor + solve on cuda:0. Returns (X, finfo, solver) -- solver only if keep."""
     import torch
     import paper_2002_05019_b200 as dd
     o = dd.DD_ORDER_AUTO if order is None else order
     s = dd.AuxSolver(p.blk_size, p.colptr, p.rowidx, complex_=p.is_complex, order=o, refine_steps=refine,
-                     user_order=user_order)
+                     user_order=user_order, perturb_tau=perturb_tau)
     vals = torch.from_numpy(p.values).cuda()
     rc, finfo = s.factor(vals, p.val_offset)
     finfo["rc"] = rc

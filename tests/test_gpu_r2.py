@@ -1,0 +1,207 @@
+"""Round-2 GPU parity: failure semantics, pivot ties, the K1 paths full-size configs take.
+
+* NaN / Inf in a pivot column -> DD_NONFINITE with the oracle's first DoF (reading L4b);
+* opt-in static perturbation (reading L4) against the oracle's perturbed factorization;
+* first zero pivot in ELIMINATION order (reading L4), max |L| against the oracle;
+* IDAMAX ties (reading L3) on exact integer blocks: ipiv == oracle == LAPACK, bit for bit;
+* large isolated blocks: at the first column where GPU and oracle pivots differ, the oracle's
+  decision must have been a near-tie (relative margin <= NEAR_TIE);
+* principal corner samples of configs[2] / configs[3] at FULL interface sizes (U[128,1024] real,
+  512 complex), nrhs >= 130 (several split-K chunks in the backward update), element-wise
+  against the oracle with the north_star tolerances, plus the unrefined backward error of the
+  GPU's explicit-inverse TRSM against the oracle's triangular substitution.
+"""
+import numpy as np
+import pytest
+
+import dd_inputs
+from dd_inputs import random_rhs, single_block_problem, tie_block
+import oracle
+from oracle.bk import bk_factor
+from oracle.block_ldlt import block_solve, residual_berr
+
+from tests._gpu import rel_diff, run_gpu, to_dev_colmajor
+from tests.test_oracle_pins import _zero_dof_problem
+
+pytestmark = pytest.mark.gpu
+
+TOL_REL = 1e-9
+TOL_BERR = 1e-12
+NEAR_TIE = 1e-8   # a decision whose two sides differ by less than this (relative) may flip under a
+                  # different valid rounding order; GPU vs oracle values differ by ~1e-13 relative
+
+
+def test_nonfinite_pivot_reports_first_dof():
+    import torch
+    import paper_2002_05019_b200 as dd
+    rng = np.random.default_rng(9)
+    p, _ = _zero_dof_problem(rng, [], sizes=(40, 33, 70))
+    order = [1, 2, 0]
+    for where, bad in [((3, 0), np.nan), ((0, 0), np.nan), ((17, 5), np.inf)]:
+        q = dd_inputs.Problem(p.blk_size, p.colptr, p.rowidx, p.values.copy(), p.val_offset, [])
+        q.block(int(q.colptr[1]))[where] = bad
+        F = oracle.block_factor(q, order)
+        X, fi, s = run_gpu(q, None, user_order=order, keep=True)
+        assert fi["rc"] == dd.DD_NONFINITE and fi["nonfinite"] >= 1, fi
+        assert fi["first_zero_pivot"] == F.info, (fi["first_zero_pivot"], F.info)
+        with pytest.raises(dd.DDAuxError) as ei:
+            s.solve_(torch.zeros(q.n, 1, dtype=torch.float64, device="cuda"))
+        assert ei.value.code == dd.DD_ERR_SINGULAR
+        s.close()
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_static_perturbation(cplx):
+    import paper_2002_05019_b200 as dd
+    rng = np.random.default_rng(3 + cplx)
+    zero = [3, 15, 40]
+    p, A = _zero_dof_problem(rng, zero, sizes=(20, 15, 33, 18), cplx=cplx)
+    order = [2, 0, 3, 1]
+    _, fi0, _ = run_gpu(p, None, user_order=order)
+    assert fi0["rc"] == dd.DD_ZERO_PIVOT and fi0["nperturbed"] == 0
+    tau = 1e-3
+    B = random_rhs(p.n, 5, cplx, 1)
+    X, fi, _ = run_gpu(p, B, user_order=order, refine=0, perturb_tau=tau)
+    F = oracle.block_factor(p, order, perturb_tau=tau)
+    assert fi["rc"] == dd.DD_OK and fi["nperturbed"] == F.nperturbed == len(zero)
+    Xo = block_solve(F, B, p.dof_offset)
+    assert rel_diff(X, Xo) <= TOL_REL
+    Ap = A.copy()
+    for m in zero:
+        Ap[m, m] = tau * float(np.abs(A).sum(axis=1).max())
+    assert rel_diff(X, np.linalg.solve(Ap, B)) <= TOL_REL
+
+
+def test_first_zero_pivot_elimination_order():
+    import paper_2002_05019_b200 as dd
+    rng = np.random.default_rng(8)
+    sizes = (37, 25, 49, 26)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    zero = [int(off[1]) + 2, int(off[3]) + 4]
+    p, _ = _zero_dof_problem(rng, zero, sizes)
+    for order, want in (([0, 1, 2, 3], zero[0]), ([3, 2, 1, 0], zero[1]), ([2, 3, 0, 1], zero[1])):
+        _, fi, _ = run_gpu(p, None, user_order=order)
+        F = oracle.block_factor(p, order)
+        assert fi["rc"] == dd.DD_ZERO_PIVOT
+        assert fi["first_zero_pivot"] == F.info == want + 1
+
+
+@pytest.mark.parametrize("name,grid,sizes", [("cfg1", (2, 2, 2), 96), ("cfg3", (2, 2, 2), 80),
+                                             ("cfg2", (3, 3, 2), lambda n, r: r.integers(60, 300, n))])
+def test_max_abs_L_matches_oracle(name, grid, sizes):
+    p = dd_inputs.config(name, grid=grid, sizes=sizes)
+    _, fi, s = run_gpu(p, None, keep=True)
+    F = oracle.block_factor(p, list(s.order()))
+    s.close()
+    assert fi["max_abs_L"] == pytest.approx(oracle.max_abs_L(F), rel=1e-9)
+
+
+@pytest.mark.parametrize("s", [96, 300, 1031])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_idamax_ties_bitwise(s, cplx):
+    """Exact-arithmetic blocks full of ties: every decision, D and L are THE LAPACK answer."""
+    A = tie_block(s, seed=s)
+    if cplx:
+        A = A.astype(np.complex128)
+    p = single_block_problem(A)
+    X, fi, sv = run_gpu(p, random_rhs(s, 2, cplx, 0), keep=True)
+    piv = sv.pivots()
+    sv.close()
+    f = bk_factor(A)
+    np.testing.assert_array_equal(piv["ipiv"], f["ipiv"])
+    np.testing.assert_array_equal(piv["perm"], f["perm"])
+    np.testing.assert_array_equal(piv["d"], f["d"])
+    assert residual_berr(p, X, random_rhs(s, 2, cplx, 0)).max() <= TOL_BERR
+
+
+@pytest.mark.parametrize("s,cplx", [(1100, False), (1100, True), (2100, False)])
+def test_large_block_pivots_near_tie_aware(s, cplx):
+    """K1's 16-rows-per-thread path: the pivot sequences may differ only after a near-tie."""
+    rng = np.random.default_rng(s + 7 * cplx)
+    A = rng.standard_normal((s, s))
+    if cplx:
+        A = A + 1j * rng.standard_normal((s, s))
+    A = A + A.T
+    p = single_block_problem(A)
+    B = random_rhs(s, 3, cplx, 1)
+    X, fi, sv = run_gpu(p, B, keep=True)
+    piv = sv.pivots()
+    sv.close()
+    margins = []
+    f = bk_factor(A, margins=margins)
+    assert residual_berr(p, X, B).max() <= TOL_BERR
+    diff = np.nonzero(piv["ipiv"] != f["ipiv"])[0]
+    if diff.size:
+        c = int(diff[0])
+        # the pivot step that decided column c (a 2x2 step covers two columns)
+        step = max(k for k, _ in margins if k <= c)
+        m = dict(margins)[step]
+        print(f"first ipiv difference at column {c} (step {step}), oracle margin {m:.3e}")
+        assert m <= NEAR_TIE, (c, m)
+
+
+def _corner(cfg, sub_grid):
+    """Principal sub-matrix of the interfaces inside a corner sub-grid of the FULL workload
+    (device-drawn like bench.py, carved to host numpy): full interface sizes."""
+    import torch
+    prob = dd_inputs.config(cfg, seed=0, backend="torch", device="cuda")
+    keep = dd_inputs.corner_interfaces(prob, sub_grid)
+    sub = dd_inputs.subproblem(prob, keep)
+    del prob
+    torch.cuda.empty_cache()
+    return sub
+
+
+def _corner_parity(sub, nrhs):
+    import time
+    import torch
+    import paper_2002_05019_b200 as dd
+    B = random_rhs(sub.n, nrhs, sub.is_complex, 11)
+    X, fi, s = run_gpu(sub, B, keep=True)
+    # unrefined GPU solve of a few columns (explicit-inverse TRSM path, no correction step)
+    dd.dd_aux_set_refine(s.h, 0, 0.0)
+    cols = [0, 1, nrhs - 1]
+    b0 = to_dev_colmajor(B[:, cols], torch)
+    s.solve_(b0)
+    torch.cuda.synchronize()
+    X0 = b0.cpu().numpy()
+    order = list(s.order())
+    s.close()
+    t = time.time()
+    F = oracle.block_factor(sub, order)
+    Xo, berr0_o, berr_o = oracle.refine_solve(sub, F, B, 1)
+    print(f"n={sub.n} nblk={sub.nblk} max_s={int(sub.blk_size.max())} oracle {time.time() - t:.1f} s")
+    berr = residual_berr(sub, X, B)
+    assert berr.max() <= TOL_BERR, berr.max()
+    assert berr_o.max() <= TOL_BERR
+    rd = rel_diff(X, Xo)
+    assert rd <= TOL_REL, rd
+    if not sub.is_complex:
+        assert (fi["npos"], fi["nneg"], fi["nzero"]) == oracle.inertia(F)
+    gpu0 = residual_berr(sub, X0, B[:, cols]).max()
+    orc0 = berr0_o[cols].max()
+    print(f"unrefined berr: gpu {gpu0:.2e} oracle {orc0:.2e}; refined gpu {berr.max():.2e}; rel diff {rd:.2e}")
+    assert gpu0 <= 10 * orc0, (gpu0, orc0)
+    assert fi["max_abs_L"] == pytest.approx(oracle.max_abs_L(F), rel=1e-8)
+
+
+def test_cfg2_corner_full_sizes():
+    """configs[2] 3x2x2 corner (bench.py's cpu_baseline sample): sizes U[128,1024] -> K1 takes the
+    4-rows-per-thread windowed path inside a multi-level factorization."""
+    sub = _corner("cfg2", (3, 2, 2))
+    assert int(sub.blk_size.max()) > 512
+    _corner_parity(sub, 136)
+
+
+def test_cfg3_corner_full_sizes():
+    """configs[3] 3x2x2 corner: complex symmetric, s = 512 (K1 2-rows-per-thread path)."""
+    sub = _corner("cfg3", (3, 2, 2))
+    assert int(sub.blk_size.min()) == 512
+    _corner_parity(sub, 136)
+
+
+def test_cfg2_larger_corner_full_sizes():
+    """A larger configs[2] corner (4x3x3 sub-grid): deeper elimination tree, more levels of the
+    lookahead schedule, more K3 contributors per target."""
+    sub = _corner("cfg2", (4, 3, 3))
+    _corner_parity(sub, 130)
