@@ -146,29 +146,41 @@ def berr_check(prob, Bsrc, X, ncols=8):
     return float(berr.max()), cols
 
 
-def oracle_sample(prob, cfg):
-    """Time the CPU oracle (as it stands) on a bounded sample of the workload."""
+def oracle_sample(prob, cfg, nrhs, config_flops=None, sub=None):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload: its factor, then
+    its solve (O5 sweeps + O6 refinement, refine_steps=1) of one batch of nrhs right-hand sides."""
     import oracle
-    from oracle.block_ldlt import flops_factor
+    from oracle.block_ldlt import flops_factor, flops_solve_per_rhs
     try:
         from threadpoolctl import threadpool_info
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
     keep = dd_inputs.corner_interfaces(prob, SAMPLE_GRID[cfg])
-    sub = dd_inputs.subproblem(prob, keep)
+    if sub is None:
+        sub = dd_inputs.subproblem(prob, keep)
     order = list(range(sub.nblk))
     t0 = time.perf_counter()
     F = oracle.block_factor(sub, order)
     dt = time.perf_counter() - t0
     mu = 4 if sub.is_complex else 1
     fl = flops_factor(sub.blk_size, F.sym, mu)
+    B = dd_inputs.random_rhs(sub.n, nrhs, sub.is_complex, 1)
+    t0 = time.perf_counter()
+    oracle.refine_solve(sub, F, B, 1)
+    ds = time.perf_counter() - t0
     g = SAMPLE_GRID[cfg]
-    sample = (f"oracle.block_factor on the principal sub-matrix of the {len(keep)} interfaces inside the "
-              f"{g[0]}x{g[1]}x{g[2]} corner sub-grid of this workload (n={sub.n}, same bytes), natural order, "
-              f"{fl:.3g} algorithmic flops, {dt:.2f} s")
+    share = fl / config_flops if config_flops else None
+    sample = (f"oracle.block_factor + oracle.refine_solve (nrhs={nrhs}, 1 refinement step) on the principal "
+              f"sub-matrix of the {len(keep)} interfaces inside the {g[0]}x{g[1]}x{g[2]} corner sub-grid of this "
+              f"workload (n={sub.n}, same bytes), natural order: factor {fl:.3g} algorithmic flops in {dt:.2f} s"
+              + (f" ({100 * share:.2f}% of the config's factor flops)" if share else "")
+              + f", solve {ds:.2f} s")
     return {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": int(cores), "kind": "oracle", "sample": sample,
-            "seconds": dt}
+            "seconds": dt + ds, "factor_s": dt, "solve_s": ds, "sample_n": sub.n, "sample_flops_factor": fl,
+            "flops_share_of_config": share,
+            "solve_ms_per_1000_rhs": ds * 1e6 / nrhs,
+            "solve_gflops": 2 * mu * flops_solve_per_rhs(sub.blk_size, F.sym) * nrhs / ds / 1e9}
 
 
 def dist_setup(args):
@@ -214,12 +226,14 @@ def reference_arm(args, rank, world):
         prob = dd_inputs.config(cfg, seed=args.seed, backend="torch", device="cuda")
     else:
         prob = dd_inputs.config(cfg, seed=args.seed, grid=SAMPLE_GRID[cfg])
+    sub = dd_inputs.subproblem(prob, dd_inputs.corner_interfaces(prob, SAMPLE_GRID[cfg]))
+    nr = min(c["nrhs"], 256)
     for _ in range(args.warmup):
-        oracle_sample(prob, cfg)
+        oracle_sample(prob, cfg, nr, sub=sub)
     vals, secs = [], 0.0
     cb = None
     for _ in range(args.steps):
-        cb = oracle_sample(prob, cfg)
+        cb = oracle_sample(prob, cfg, nr, sub=sub)
         vals.append(cb["value"])
         secs += cb["seconds"]
     v = float(np.median(vals))
@@ -228,7 +242,8 @@ def reference_arm(args, rank, world):
             "ms_per_step": secs * 1e3 / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128" if c["complex_"] else "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD_TXT[cfg], "nrhs": c["nrhs"], "sample": SAMPLE_GRID[cfg]},
-            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cb["cores"], "kind": "oracle", "sample": cb["sample"]},
+            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cb["cores"], "kind": "oracle", "sample": cb["sample"],
+                             "solve_ms_per_1000_rhs": cb["solve_ms_per_1000_rhs"]},
             "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -282,6 +297,16 @@ def gpu_arm(args, rank, world, local, dist):
     solver.factor(vals, prob.val_offset)  # allocates factor/work buffers
     solver._work(max(info["work_bytes"], dd.dd_aux_solve_work_bytes(solver.h, nrhs)))
     stream = torch.cuda.current_stream()
+    bgen = torch.Generator(device=dev)
+
+    def load_batch(b):
+        """Right-hand sides of batch b: batch 0 is Bsrc; configs[4]'s other batches are distinct
+        N(0,1) draws (seeded per batch, drawn on the device: 2 ms against a 3.5 s solve)."""
+        if b == 0:
+            Bw.copy_(Bsrc)
+        else:
+            bgen.manual_seed(7919 * (b + 1) + args.seed)
+            Bw.t().copy_(torch.randn((nrhs, prob.n), dtype=tdt, device=dev, generator=bgen))
 
     def step(ev):
         ev[0].record(stream)
@@ -290,8 +315,8 @@ def gpu_arm(args, rank, world, local, dist):
             raise RuntimeError(f"factor rc={rc}")
         ev[1].record(stream)
         ev[2].record(stream)
-        for _ in my_batches:
-            Bw.copy_(Bsrc)
+        for b in my_batches:
+            load_batch(b)
             solver.solve_(Bw)
         ev[3].record(stream)
         return fi
@@ -300,14 +325,14 @@ def gpu_arm(args, rank, world, local, dist):
     for _ in range(args.warmup):
         step(mk())
     torch.cuda.synchronize()
-    dd.dd_aux_set_trace(solver.h, True)
-    dd.dd_aux_get_trace(solver.h, reset=True)
+    # ---- timed region: UNTRACED (no per-launch events), CUDA events on the launching stream
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = Clocks(local)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     evs = [mk() for _ in range(args.steps)]
+    dd.dd_aux_get_trace(solver.h, reset=True)  # launch counters are kept even with tracing off
     start.record(stream)
     finfo = None
     for k in range(args.steps):
@@ -320,21 +345,50 @@ def gpu_arm(args, rank, world, local, dist):
     total_ms = start.elapsed_time(end)
     fac_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
     sol_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
+    launches = sum(v["launches"] for v in dd.dd_aux_get_trace(solver.h, reset=True).values())
+    # ---- per-kernel breakdown from a SEPARATE traced pass of the same step (event pair around
+    # every launch on its own stream); its step time is reported beside the untraced one
+    step_s = total_ms / args.steps / 1e3
+    KT = max(1, min(args.steps, int(np.ceil(20.0 / max(step_s, 1e-3)))))
+    dd.dd_aux_set_trace(solver.h, True)
+    dd.dd_aux_get_trace(solver.h, reset=True)
+    tev = [mk() for _ in range(KT)]
+    for k in range(KT):
+        step(tev[k])
+    torch.cuda.synchronize()
+    traced_fac_ms = sum(e[0].elapsed_time(e[1]) for e in tev) / KT
+    traced_sol_ms = sum(e[2].elapsed_time(e[3]) for e in tev) / KT
     trace = dd.dd_aux_get_trace(solver.h, reset=False)
     lvl = dd.dd_aux_get_level_trace(solver.h)
     dd.dd_aux_get_trace(solver.h, reset=True)
     dd.dd_aux_set_trace(solver.h, False)
 
     # ---- accuracy evidence (harness, outside the timed region): berr of the timed result and of
-    # an unrefined solve of the same right-hand sides
-    berr, cols = berr_check(prob, Bsrc, Bw)
+    # an unrefined solve of the same right-hand sides; configs[4]: EVERY column of every batch
+    load_batch(my_batches[-1])
+    Bref = Bw.clone()               # b of the step's last batch
+    solver.solve_(Bw)               # x (deterministic: bitwise the timed result)
+    berr, cols = berr_check(prob, Bref, Bw)
+    berr_all = None
+    if batches > 1:  # configs[4] (ledger L15): berr of all nrhs x batches columns
+        berr_all = {"max": 0.0, "columns": 0}
+        for b in my_batches:
+            load_batch(b)
+            Bb = Bw.clone()
+            solver.solve_(Bw)
+            be, cl = berr_check(prob, Bb, Bw, ncols=nrhs)
+            berr_all["max"] = max(berr_all["max"], be)
+            berr_all["columns"] += len(cl)
+            del Bb
+        load_batch(0)
+        solver.solve_(Bw)
     Bu = torch.empty((len(cols), prob.n), dtype=tdt, device=dev).t()
-    Bu.copy_(Bsrc[:, cols])
+    Bu.copy_(Bref[:, cols])
     dd.dd_aux_set_refine(solver.h, 0, 0.0)
     solver.solve_(Bu)
     dd.dd_aux_set_refine(solver.h, args.refine, args.refine_tol)
-    berr0, _ = berr_check(prob, Bsrc[:, cols], Bu, ncols=len(cols))
-    del Bu
+    berr0, _ = berr_check(prob, Bref[:, cols], Bu, ncols=len(cols))
+    del Bu, Bref
 
     # ---- max over ranks (device-timed), NCCL all-reduce of three scalars (plumbing only)
     total_ms, fac_ms, sol_ms = reduce_max([total_ms, fac_ms, sol_ms], dist, dev)
@@ -410,9 +464,8 @@ def gpu_arm(args, rank, world, local, dist):
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_sample(prob, cfg)
+        cpu = oracle_sample(prob, cfg, min(nrhs, 256), config_flops=info["flops_factor"])
         cpu.pop("seconds", None)
-    launches = sum(v["launches"] for v in trace.values())
     line = {
         "metric": "aux-matrix LDL^T factor FP64 GFLOP/s (% of FP64 peak); solve ms per 1000 RHS",
         "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -437,7 +490,12 @@ def gpu_arm(args, rank, world, local, dist):
         # diagonal blocks); (1 + refine_steps) sweeps per batch; achieved = those bytes / solve time
         "solve_hbm_gbs": (1 + args.refine) * info["factor_value_bytes"] * len(my_batches) * K / (sol_ms * 1e-3) / 1e9,
         "flops_factor": flops, "flops_solve_per_rhs": info["flops_solve_per_rhs"],
+        "trace_pass": {"steps": KT, "factor_ms": traced_fac_ms, "solve_ms": traced_sol_ms,
+                       "what": "per-kernel ms/launches/flops (phases, roofline) come from this separate "
+                               "traced pass (CUDA-event pair around every launch); the timed region above "
+                               "runs untraced"},
         "accuracy": {"berr_max": berr, "berr_unrefined_max": berr0, "columns_checked": len(cols),
+                     "berr_all_columns": berr_all,
                      "tolerance": 1e-12, "refine_steps": args.refine, "refine_tol": args.refine_tol,
                      "pivots": {"n2x2": finfo["n2x2"], "nswaps": finfo["nswaps"]},
                      "inertia": None if cplx else [finfo["npos"], finfo["nneg"], finfo["nzero"]]},
@@ -445,7 +503,7 @@ def gpu_arm(args, rank, world, local, dist):
                      "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved / peak_tf, "traffic": traffic, "traffic_src": traffic_src,
                      "peak_src": f"measured cuBLAS {'ZGEMM' if cplx else 'DGEMM'} 8192^3 ({peak_src})"},
-        "phases": {p: {"ms_per_step": v["ms"] / K, "launches_per_step": v["launches"] / K,
+        "phases": {p: {"ms_per_step": v["ms"] / KT, "launches_per_step": v["launches"] / KT,
                        "tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["ms"] > 0 and v["flops"] > 0 else None}
                    for p, v in trace.items() if v["launches"]},
         "assemble": {"kernel": "k_assemble", "bound": "hbm", "ms": asm_ms, "bytes": asm_bytes,
@@ -461,7 +519,7 @@ def gpu_arm(args, rank, world, local, dist):
     }
     if args.trace_out:
         json.dump({"trace": trace, "line": line, "phases": dd.PHASES,
-                   "level_ms": (lvl["ms"] / K).tolist(), "level_flops": (lvl["flops"] / K).tolist()},
+                   "level_ms": (lvl["ms"] / KT).tolist(), "level_flops": (lvl["flops"] / KT).tolist()},
                   open(args.trace_out, "w"), indent=1)
     print(json.dumps(line), flush=True)
 
