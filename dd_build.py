@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 HERE = os.path.join(ROOT, "paper_2002_05019_b200")
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdd_aux.so")
-SOURCES = ["api.cu", "kernels_factor.cu", "kernels_solve.cu", "kernels_assemble.cu", "analyze.cpp"]
+SOURCES = ["api.cu", "kernels_factor.cu", "kernels_solve.cu", "kernels_assemble.cu", "kernels_schur.cu", "analyze.cpp"]
 HEADERS = ["analyze.hpp", "layout.hpp", "launch.hpp", "common.cuh", "gemm_core.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -88,6 +88,8 @@ typedef struct {
   size_t factor_bytes;          /* size of d_factor                                            */
   size_t work_bytes;            /* size of d_work for dd_aux_factor                            */
   int32_t dtype, order_used;
+  int64_t n_schur, n_groups;    /* Schur mode (dd_aux_analyze_partial): kept blocks, groups; else 0 */
+  int64_t n_aux_dof;            /* Schur mode: DoFs of the auxiliary numbering (rows of G / X_b)   */
 } dd_aux_info;
 
 typedef struct {
@@ -218,7 +220,7 @@ int dd_aux_set_graphs(dd_aux_handle_t h, int32_t enable);
 enum {
   DD_PH_LOAD = 0, DD_PH_K1, DD_PH_ROWPERM, DD_PH_K2, DD_PH_K3, DD_PH_STATS,
   DD_PH_PERM, DD_PH_FDIAG, DD_PH_FUPD, DD_PH_DSOLVE, DD_PH_BUPD, DD_PH_BDIAG, DD_PH_SPMV,
-  DD_PH_LINV, DD_PH_ASSEMBLE, DD_NPHASE
+  DD_PH_LINV, DD_PH_ASSEMBLE, DD_PH_SCHUR, DD_NPHASE
 };
 typedef struct {
   double ms[16];        /* device milliseconds per kernel class (tracing enabled only) */
@@ -230,6 +232,63 @@ int dd_aux_get_trace(dd_aux_handle_t h, dd_aux_trace* out, int32_t reset);
 /* Per-level factor trace since the last reset, row-major [n_levels][16] (DD_PH_* columns):
  * device ms (tracing enabled) and algorithmic flops.  Call after dd_aux_get_trace(reset=0). */
 int dd_aux_get_level_trace(dd_aux_handle_t h, double* ms, double* flops);
+
+/* ---------------------------------------------------------------------------------------------
+ * f3 / f2: partial factorization ("Schur mode"), subdomain elimination and
+ * primal recovery.  PAPER.md:27 (§II): the arrowhead system [K C; C^T A_bb] "is then reduced in
+ * size by eliminating via many independent sparse direct factorizations the primal DoFs";
+ * "the solution of all or a subset of primal unknowns are recovered in an
+ * embarrassingly parallel manner via many smaller size sparse forward backward substitutions".
+ *
+ * The caller lays out every subdomain's arrowhead rows as ONE block-sparse symmetric matrix (same
+ * input format as dd_aux_analyze): the primal DoFs of each subdomain grouped into blocks (a
+ * supernode partition, e.g. a nested dissection -- the ordering input), followed by the KEPT
+ * blocks: the last n_schur block ids, one per (subdomain, interface) pair, holding that
+ * subdomain's copy of the interface's dual DoFs with A_bb,p on the diagonal block and C_p^T
+ * against the primal blocks.  Subdomains share no block, so their eliminations are independent
+ * and the level scheduler runs them side by side ("many independent ... factorizations").
+ * dd_aux_factor then eliminates every non-kept block (restricted BK, as for the auxiliary matrix)
+ * and leaves in the kept blocks of subdomain p its dense Schur contribution
+ *     S_p = A_bb,p - C_p^T K_p^{-1} C_p.
+ *  schur_target [n_schur] auxiliary block id I of kept block (nblk - n_schur + k); sizes must match
+ *  schur_group  [n_schur] subdomain (clique) id of kept block k; one target per group at most
+ *  n_aux, aux_blk_size [n_aux]  sizes of the auxiliary blocks (the auxiliary DoF numbering
+ *               sum_{I'<I} s_I' + local is the row order of G and X_b below)
+ *  opt->order   applies to the eliminated blocks (DD_ORDER_USER: a permutation of
+ *               [0, nblk - n_schur)); the kept blocks follow in ascending id
+ * dd_aux_factor on such a handle returns the inertia / pivot statistics of the eliminated part;
+ * dd_aux_solve returns an error (use dd_aux_condense / dd_aux_recover).                        */
+int dd_aux_analyze_partial(int64_t nblk, const int64_t* blk_size, const int64_t* colptr, const int32_t* rowidx,
+                           int32_t dtype, const dd_aux_options* opt, int64_t n_schur, const int32_t* schur_target,
+                           const int32_t* schur_group, int64_t n_aux, const int64_t* aux_blk_size,
+                           dd_aux_handle_t* out);
+
+/* Cliques of the exported Schur complements: groups g = distinct schur_group values ascending;
+ * clq_blk[clq_ptr[g] .. clq_ptr[g+1]) = the targets of g's kept blocks, ascending (the clique
+ * format of dd_aux_assemble).  Host out: ngroups, clq_ptr [ngroups+1], clq_blk [n_schur]; any
+ * pointer may be NULL. */
+int dd_aux_schur_cliques(dd_aux_handle_t h, int64_t* ngroups, int64_t* clq_ptr, int32_t* clq_blk);
+
+/* f3 output: write every group's dense S_g (m_g x m_g, both triangles, column-major, ld = m_g,
+ * DoFs = its kept blocks concatenated in clique order) at element offset S_offset[g] of d_S
+ * (complex interleaved).  These are exactly the per-subdomain cliques dd_aux_assemble sums into
+ * the auxiliary matrix.  Asynchronous on `stream`; HBM-bound gather from the factor arena. */
+int dd_aux_schur_export(dd_aux_handle_t h, const void* d_factor, void* d_S, const int64_t* S_offset, void* stream);
+
+/* Condensation of the right-hand side onto the auxiliary DoFs (forward sweep of the partial
+ * factorization):  G <- G - sum_p R_p^T C_p^T K_p^{-1} f_p,  R_p = the auxiliary rows of p's
+ * kept blocks.  d_F: n x nrhs (ld ldf, the handle's DoF numbering; kept rows are ignored);
+ * d_G: n_aux_dof x nrhs (ld ldg), accumulated in a fixed order (pass G = b_b to obtain the
+ * auxiliary right-hand side).  d_work: dd_aux_solve_work_bytes(h, nrhs).  Asynchronous. */
+int dd_aux_condense(dd_aux_handle_t h, const void* d_factor, int64_t nrhs, const void* d_F, int64_t ldf, void* d_G,
+                    int64_t ldg, void* d_work, void* stream);
+
+/* f2 primal recovery (forward + backward sweep of the partial factorization with the kept rows
+ * set to the auxiliary solution):  x_p = K_p^{-1} (f_p - C_p R_p x_b)  for every subdomain.
+ * d_F as above; d_Xb: n_aux_dof x nrhs (ld ldxb); d_X: n x nrhs out (ld ldx; primal rows = x_p,
+ * kept rows = the copies of x_b; d_X may equal d_F).  Asynchronous. */
+int dd_aux_recover(dd_aux_handle_t h, const void* d_factor, int64_t nrhs, const void* d_F, int64_t ldf,
+                   const void* d_Xb, int64_t ldxb, void* d_X, int64_t ldx, void* d_work, void* stream);
 
 int dd_aux_destroy(dd_aux_handle_t h);
 

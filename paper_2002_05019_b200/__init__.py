@@ -21,7 +21,9 @@ __all__ = ["DD_REAL64", "DD_COMPLEX128", "DD_ORDER_AUTO", "DD_ORDER_ND", "DD_ORD
            "dd_aux_get_info", "dd_aux_get_order", "dd_aux_get_etree", "dd_aux_solve_work_bytes", "dd_aux_factor",
            "dd_aux_solve", "dd_aux_get_pivots", "dd_aux_destroy", "dd_aux_last_error", "dd_aux_version",
            "dd_aux_set_refine", "dd_aux_set_graphs", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_get_level_trace", "dd_aux_assemble_work_bytes", "dd_aux_assemble",
-           "dd_aux_last_assemble_bytes", "cliques_to_csr", "AuxSolver", "LIB_PATH", "EXPORTED_SYMBOLS", "PHASES"]
+           "dd_aux_last_assemble_bytes", "cliques_to_csr", "AuxSolver", "LIB_PATH", "EXPORTED_SYMBOLS", "PHASES",
+           "dd_aux_analyze_partial", "dd_aux_schur_cliques", "dd_aux_schur_export", "dd_aux_condense",
+           "dd_aux_recover", "SchurSolver"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdd_aux.so")
 
@@ -34,9 +36,10 @@ EXPORTED_SYMBOLS = ["dd_aux_default_options", "dd_aux_analyze", "dd_aux_get_info
                     "dd_aux_get_etree", "dd_aux_solve_work_bytes", "dd_aux_factor", "dd_aux_solve",
                     "dd_aux_get_pivots", "dd_aux_set_refine", "dd_aux_set_graphs", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_get_level_trace", "dd_aux_destroy",
                     "dd_aux_last_error", "dd_aux_version", "dd_aux_assemble_work_bytes", "dd_aux_assemble",
-                    "dd_aux_last_assemble_bytes"]
+                    "dd_aux_last_assemble_bytes", "dd_aux_analyze_partial", "dd_aux_schur_cliques",
+                    "dd_aux_schur_export", "dd_aux_condense", "dd_aux_recover"]
 PHASES = ["load", "k1_diag_bk", "rowperm", "k2_panel", "k3_update", "stats", "perm", "fdiag", "fupd", "dsolve",
-          "bupd", "bdiag", "spmv", "linv", "assemble"]
+          "bupd", "bdiag", "spmv", "linv", "assemble", "schur"]
 
 
 class DDAuxError(RuntimeError):
@@ -57,7 +60,8 @@ class dd_aux_info(ctypes.Structure):
                 ("max_level_width", ctypes.c_int64), ("flops_factor", ctypes.c_double),
                 ("flops_solve_per_rhs", ctypes.c_double), ("factor_value_bytes", ctypes.c_double),
                 ("factor_bytes", ctypes.c_size_t), ("work_bytes", ctypes.c_size_t), ("dtype", ctypes.c_int32),
-                ("order_used", ctypes.c_int32)]
+                ("order_used", ctypes.c_int32), ("n_schur", ctypes.c_int64), ("n_groups", ctypes.c_int64),
+                ("n_aux_dof", ctypes.c_int64)]
 
 
 class dd_aux_factor_info(ctypes.Structure):
@@ -97,6 +101,12 @@ def _load():
         "dd_aux_assemble_work_bytes": (ctypes.c_int, [P, i64, pi64, pi32, ctypes.POINTER(ctypes.c_size_t)]),
         "dd_aux_assemble": (ctypes.c_int, [P, i64, pi64, pi32, P, pi64, i32, pi64, P, P, P]),
         "dd_aux_last_assemble_bytes": (ctypes.c_double, [P]),
+        "dd_aux_analyze_partial": (ctypes.c_int, [i64, pi64, pi64, pi32, i32, ctypes.POINTER(dd_aux_options), i64,
+                                                   pi32, pi32, i64, pi64, ctypes.POINTER(P)]),
+        "dd_aux_schur_cliques": (ctypes.c_int, [P, pi64, pi64, pi32]),
+        "dd_aux_schur_export": (ctypes.c_int, [P, P, P, pi64, P]),
+        "dd_aux_condense": (ctypes.c_int, [P, P, i64, P, i64, P, i64, P, P]),
+        "dd_aux_recover": (ctypes.c_int, [P, P, i64, P, i64, P, i64, P, i64, P, P]),
         "dd_aux_destroy": (ctypes.c_int, [P]),
         "dd_aux_last_error": (ctypes.c_char_p, []),
         "dd_aux_version": (ctypes.c_char_p, []),
@@ -308,6 +318,69 @@ def dd_aux_last_assemble_bytes(h) -> float:
     return float(_lib.dd_aux_last_assemble_bytes(h))
 
 
+def dd_aux_analyze_partial(blk_size, colptr, rowidx, schur_target, schur_group, aux_blk_size, dtype=DD_REAL64,
+                           opt: Optional[dd_aux_options] = None):
+    """f3: Schur-mode handle; the last len(schur_target) block ids are kept (include/dd_aux.h)."""
+    bs = np.ascontiguousarray(blk_size, dtype=np.int64)
+    cp = np.ascontiguousarray(colptr, dtype=np.int64)
+    ri = np.ascontiguousarray(rowidx, dtype=np.int32)
+    st = np.ascontiguousarray(schur_target, dtype=np.int32)
+    sg = np.ascontiguousarray(schur_group, dtype=np.int32)
+    ab = np.ascontiguousarray(aux_blk_size, dtype=np.int64)
+    h = ctypes.c_void_p()
+    rc = _lib.dd_aux_analyze_partial(len(bs), _np_ptr(bs, ctypes.c_int64), _np_ptr(cp, ctypes.c_int64),
+                                     _np_ptr(ri, ctypes.c_int32), int(dtype),
+                                     ctypes.byref(opt) if opt is not None else None, len(st),
+                                     _np_ptr(st, ctypes.c_int32), _np_ptr(sg, ctypes.c_int32), len(ab),
+                                     _np_ptr(ab, ctypes.c_int64), ctypes.byref(h))
+    _check(rc)
+    return h
+
+
+def dd_aux_schur_cliques(h):
+    """[[auxiliary block ids of group g, ascending], ...] (the cliques of the exported S_g)."""
+    ng = ctypes.c_int64()
+    _check(_lib.dd_aux_schur_cliques(h, ctypes.byref(ng), None, None))
+    ptr = np.empty(ng.value + 1, dtype=np.int64)
+    ns = dd_aux_get_info(h)["n_schur"]
+    blk = np.empty(ns, dtype=np.int32)
+    _check(_lib.dd_aux_schur_cliques(h, None, _np_ptr(ptr, ctypes.c_int64), _np_ptr(blk, ctypes.c_int32)))
+    return [blk[ptr[g]:ptr[g + 1]].tolist() for g in range(ng.value)]
+
+
+def dd_aux_schur_export(h, d_factor, d_S, S_offset, stream=None):
+    so = np.ascontiguousarray(S_offset, dtype=np.int64)
+    _check(_lib.dd_aux_schur_export(h, _dev_ptr(d_factor), _dev_ptr(d_S), _np_ptr(so, ctypes.c_int64),
+                                    _stream_ptr(stream)))
+    return so
+
+
+def _cm(t):
+    """(rows, cols, ld) of a column-major 2-D CUDA tensor (stride (1, ld))."""
+    if t.dim() == 1:
+        return t.shape[0], 1, t.shape[0]
+    if t.shape[1] > 1 and t.stride(0) != 1:
+        raise ValueError("buffers must be column-major (stride(0) == 1)")
+    return t.shape[0], t.shape[1], (t.stride(1) if t.shape[1] > 1 else t.shape[0])
+
+
+def dd_aux_condense(h, d_factor, d_F, d_G, d_work, stream=None):
+    """G <- G - sum_p R_p^T C_p^T K_p^-1 f_p (column-major CUDA tensors)."""
+    _, nrhs, ldf = _cm(d_F)
+    _, _, ldg = _cm(d_G)
+    _check(_lib.dd_aux_condense(h, _dev_ptr(d_factor), int(nrhs), _dev_ptr(d_F), int(ldf), _dev_ptr(d_G), int(ldg),
+                                _dev_ptr(d_work), _stream_ptr(stream)))
+
+
+def dd_aux_recover(h, d_factor, d_F, d_Xb, d_X, d_work, stream=None):
+    """X <- primal K_p^-1 (f_p - C_p R_p x_b) (kept rows: x_b copies)."""
+    _, nrhs, ldf = _cm(d_F)
+    _, _, ldxb = _cm(d_Xb)
+    _, _, ldx = _cm(d_X)
+    _check(_lib.dd_aux_recover(h, _dev_ptr(d_factor), int(nrhs), _dev_ptr(d_F), int(ldf), _dev_ptr(d_Xb), int(ldxb),
+                               _dev_ptr(d_X), int(ldx), _dev_ptr(d_work), _stream_ptr(stream)))
+
+
 def dd_aux_destroy(h):
     if h:
         _lib.dd_aux_destroy(h)
@@ -397,3 +470,59 @@ class AuxSolver:
             self.close()
         except Exception:
             pass
+
+
+class SchurSolver(AuxSolver):
+    """Owner of a Schur-mode (partial factorization) handle: f3 subdomain elimination + f2 primal
+    recovery.  Marshalling only (see include/dd_aux.h dd_aux_analyze_partial)."""
+
+    def __init__(self, blk_size, colptr, rowidx, schur_target, schur_group, aux_blk_size, complex_=False,
+                 order=DD_ORDER_NATURAL, user_order=None, device="cuda", complex_3m=True):
+        import torch
+        self.torch = torch
+        self.cplx = bool(complex_)
+        self.opt = dd_aux_default_options(order, 0, user_order, None, complex_3m, False, None)
+        self.h = dd_aux_analyze_partial(blk_size, colptr, rowidx, schur_target, schur_group, aux_blk_size,
+                                        DD_COMPLEX128 if self.cplx else DD_REAL64, self.opt)
+        self._bs = np.asarray(blk_size, dtype=np.int64)
+        self._rows = np.asarray(rowidx, dtype=np.int64)
+        self._col = np.repeat(np.arange(len(self._bs)), np.diff(np.asarray(colptr, dtype=np.int64)))
+        self.info = dd_aux_get_info(self.h)
+        self.device = device
+        self.factor_buf = None
+        self.work = None
+        self.vals = None
+        self.finfo = None
+
+    def cliques(self):
+        return dd_aux_schur_cliques(self.h)
+
+    def export(self, d_S=None, S_offset=None, stream=None):
+        """Dense S_g of every group into one buffer (allocated if None); returns (d_S, S_offset)."""
+        torch = self.torch
+        cl = self.cliques()
+        ms = [int(sum(self._aux_size(I) for I in c)) for c in cl]
+        if S_offset is None:
+            S_offset = np.concatenate([[0], np.cumsum([m * m for m in ms])[:-1]]).astype(np.int64)
+        if d_S is None:
+            d_S = torch.empty(int(S_offset[-1] + ms[-1] * ms[-1]),
+                              dtype=torch.complex128 if self.cplx else torch.float64, device=self.device)
+        dd_aux_schur_export(self.h, self.factor_buf, d_S, S_offset, stream)
+        return d_S, S_offset
+
+    def _aux_size(self, I):
+        if not hasattr(self, "_auxs"):
+            raise RuntimeError("set .aux_sizes")
+        return self._auxs[I]
+
+    def condense_(self, d_F, d_G, stream=None):
+        w = self._work(dd_aux_solve_work_bytes(self.h, d_F.shape[1] if d_F.dim() == 2 else 1))
+        dd_aux_condense(self.h, self.factor_buf, d_F, d_G, w, stream)
+        return d_G
+
+    def recover(self, d_F, d_Xb, d_X=None, stream=None):
+        if d_X is None:
+            d_X = self.torch.empty_like(d_F.t().contiguous()).t() if d_F.dim() == 2 else self.torch.empty_like(d_F)
+        w = self._work(dd_aux_solve_work_bytes(self.h, d_F.shape[1] if d_F.dim() == 2 else 1))
+        dd_aux_recover(self.h, self.factor_buf, d_F, d_Xb, d_X, w, stream)
+        return d_X

@@ -137,6 +137,21 @@ struct dd_aux_handle_s {
   std::vector<cudaEvent_t> evA, evA2, evB, evK;  // evK[l]: K1 of level l done (perm ready)
   cudaEvent_t evLoad = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr;  // factor timing (finfo.ms_load / ms_factor)
+  // f3/f2 Schur mode (dd_aux_analyze_partial): the last n_schur block ids are kept (not eliminated)
+  int64_t n_schur = 0;
+  int n_elim = 0;                  // eliminated positions [0, n_elim); kept positions [n_elim, N)
+  int64_t r0 = 0;                  // first padded solve row of the kept blocks
+  int64_t n_aux = 0, n_aux_dof = 0;
+  std::vector<int64_t> aux_odof;   // [n_aux] first auxiliary DoF of each auxiliary block
+  std::vector<int32_t> schur_target, schur_group;  // per kept block (0-based among the kept)
+  std::vector<int64_t> grp_ptr;    // groups (distinct schur_group, ascending): members in clq_blk order
+  std::vector<int32_t> grp_kept;   // kept indices sorted by (group, target)
+  std::vector<int64_t> grp_m;      // m_g
+  std::vector<int32_t> kept_gperm, kept_ginv;  // identity maps of the kept rows (uploaded per factor)
+  size_t off_sx_items = 0, off_sx_tiles = 0, off_sg_items = 0, off_sg_contrib = 0, off_ss_items = 0,
+         off_soff = 0;
+  int n_sx_tiles = 0, n_sg_items = 0, n_ss_items = 0;
+  std::vector<int64_t> soff_host;  // S_offset of the last export (kept alive for the async upload)
   // f1 assembly tables (host images kept alive for the async upload)
   std::vector<AsmItem> asm_items;
   std::vector<AsmContrib> asm_cons;
@@ -275,8 +290,22 @@ void dd_aux_default_options(dd_aux_options* opt) {
 const char* dd_aux_last_error(void) { return g_err.c_str(); }
 const char* dd_aux_version(void) { return "dd_aux 0.1 (sm_100a, FP64 DMMA)"; }
 
-int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr, const int32_t* rowidx,
-                   int32_t dtype, const dd_aux_options* opt_in, dd_aux_handle_t* out) {
+}  // extern "C"
+
+static int build_schur_tables(dd_aux_handle_t h);
+struct SchurIn {  // dd_aux_analyze_partial's kept-block description
+  const int32_t* target;
+  const int32_t* group;
+  int64_t n_aux;
+  const int64_t* aux_size;
+};
+
+// dd_aux_analyze and dd_aux_analyze_partial: with n_schur > 0 the last n_schur block ids are kept
+// (their Schur complement is formed, they are not eliminated); the order option then applies to
+// the eliminated blocks and the kept ones follow in ascending id.
+static int analyze_impl(int64_t nblk, const int64_t* blk_size, const int64_t* colptr, const int32_t* rowidx,
+                        int32_t dtype, const dd_aux_options* opt_in, int64_t n_schur, const SchurIn* sin,
+                        dd_aux_handle_t* out) {
   if (nblk <= 0) return fail(-1, "nblk must be > 0");
   if (!blk_size) return fail(-2, "blk_size is NULL");
   if (!colptr) return fail(-3, "colptr is NULL");
@@ -322,36 +351,50 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
     tprev = now;
   };
   // ---------------------------------------------------------------- ordering (reading L8)
+  const int NE = (int)(nblk - n_schur);  // eliminated blocks: ids [0, NE)
+  h->n_schur = n_schur;
+  h->n_elim = NE;
+  Graph ge;                               // the block graph of the eliminated blocks
+  if (n_schur > 0) {
+    ge.n = NE;
+    ge.adj.assign(NE, {});
+    ge.w.assign(h->g.w.begin(), h->g.w.begin() + NE);
+    for (int v = 0; v < NE; ++v)
+      for (int u : h->g.adj[v])
+        if (u < NE) ge.adj[v].push_back(u);
+  }
+  const Graph& go = n_schur > 0 ? ge : h->g;
   std::vector<int> order;
   if (opt.order == DD_ORDER_USER) {
     if (!opt.user_order) {
       delete h;
       return fail(-6, "DD_ORDER_USER needs user_order");
     }
-    order.assign(opt.user_order, opt.user_order + N);
-    std::vector<char> seen(N, 0);
+    order.assign(opt.user_order, opt.user_order + NE);
+    std::vector<char> seen(NE, 0);
     for (int v : order) {
-      if (v < 0 || v >= N || seen[v]) {
+      if (v < 0 || v >= NE || seen[v]) {
         delete h;
-        return fail(-6, "user_order is not a permutation");
+        return fail(-6, n_schur ? "user_order is not a permutation of the eliminated blocks [0, nblk - n_schur)"
+                                : "user_order is not a permutation");
       }
       seen[v] = 1;
     }
     h->order_used = DD_ORDER_USER;
   } else if (opt.order == DD_ORDER_NATURAL) {
-    order.resize(N);
-    for (int i = 0; i < N; ++i) order[i] = i;
+    order.resize(NE);
+    for (int i = 0; i < NE; ++i) order[i] = i;
     h->order_used = DD_ORDER_NATURAL;
   } else if (opt.order == DD_ORDER_MINDEG) {
-    order = order_mindeg(h->g);
+    order = order_mindeg(go);
     h->order_used = DD_ORDER_MINDEG;
   } else if (opt.order == DD_ORDER_ND) {
-    order = order_nd(h->g);
+    order = order_nd(go);
     h->order_used = DD_ORDER_ND;
   } else {
-    auto md = order_mindeg(h->g);
-    auto nd = order_nd(h->g);
-    if (order_flops(h->g, nd) < order_flops(h->g, md)) {
+    auto md = order_mindeg(go);
+    auto nd = order_nd(go);
+    if (order_flops(go, nd) < order_flops(go, md)) {
       order = nd;
       h->order_used = DD_ORDER_ND;
     } else {
@@ -359,15 +402,34 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
       h->order_used = DD_ORDER_MINDEG;
     }
   }
+  for (int k = NE; k < N; ++k) order.push_back(k);  // kept blocks last, ascending id
   mark("ordering");
   h->S = symbolic_from_order(h->g, order);
+  if (n_schur > 0) {  // only eliminated positions are scheduled: drop the kept ones from the levels
+    Symbolic& Sm = h->S;
+    int nl = 0;
+    for (int t = 0; t < NE; ++t) nl = std::max(nl, Sm.level[t] + 1);
+    Sm.level_nodes.assign(nl, {});
+    for (int t = 0; t < NE; ++t) Sm.level_nodes[Sm.level[t]].push_back(t);
+    Sm.nlevels = nl;
+  }
   const Symbolic& S = h->S;
 
   mark("symbolic");
   // ---------------------------------------------------------------- layout
   const int64_t mu = h->cplx ? 4 : 1;
-  h->flops_factor = mu * S.flops_factor;
-  h->flops_solve = mu * S.flops_solve;
+  {  // algorithmic flops of the eliminated positions (all of them unless Schur mode)
+    double ff = 0, fs = 0;
+    for (int t = 0; t < NE; ++t) {
+      const double sv = (double)blk_size[S.order[t]];
+      double rv = 0;
+      for (int u : S.st[t]) rv += (double)blk_size[S.order[u]];
+      ff += sv * sv * sv / 3.0 + rv * sv * sv + rv * rv * sv;
+      fs += 2.0 * (sv * sv + 2.0 * rv * sv);
+    }
+    h->flops_factor = mu * ff;
+    h->flops_solve = mu * fs;
+  }
   h->nodes.resize(N);
   std::vector<int32_t> st_pos, st_row;
   int64_t ydof = 0, panel_off = 0;
@@ -395,11 +457,14 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
     nd.ydof = ydof;
     ydof += nd.sp;
     nd.odof = h->odof_blk[blk];
-    h->max_front = std::max<int64_t>(h->max_front, nd.s + r);
-    h->max_s = std::max(h->max_s, nd.s);
-    h->value_bytes += (double)(nd.s * (int64_t)nd.s + r * nd.s) * (h->cplx ? 16.0 : 8.0);
+    if (t < NE) {
+      h->max_front = std::max<int64_t>(h->max_front, nd.s + r);
+      h->max_s = std::max(h->max_s, nd.s);
+      h->value_bytes += (double)(nd.s * (int64_t)nd.s + r * nd.s) * (h->cplx ? 16.0 : 8.0);
+    }
   }
   h->n_pad = ydof;
+  h->r0 = NE < N ? h->nodes[NE].ydof : ydof;
   int64_t off = panel_off;
   for (int t = 0; t < N; ++t) {
     NodeDev& nd = h->nodes[t];
@@ -675,6 +740,19 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   std::vector<int64_t> odof(h->odof_blk.begin(), h->odof_blk.end() - 1);
   h->off_odof = B.put(odof);
   h->off_spsegs = B.put(h->spsegs);
+  if (n_schur > 0) {
+    h->schur_target.assign(sin->target, sin->target + n_schur);
+    h->schur_group.assign(sin->group, sin->group + n_schur);
+    h->n_aux = sin->n_aux;
+    h->aux_odof.assign(sin->n_aux, 0);
+    for (int64_t I = 1; I < sin->n_aux; ++I) h->aux_odof[I] = h->aux_odof[I - 1] + sin->aux_size[I - 1];
+    h->n_aux_dof = h->aux_odof[sin->n_aux - 1] + sin->aux_size[sin->n_aux - 1];
+    const int rc = build_schur_tables(h);
+    if (rc) {
+      delete h;
+      return rc;
+    }
+  }
   h->tables_bytes = align256(B.data.size());
 
   mark("blob");
@@ -710,6 +788,13 @@ int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr,
   return DD_OK;
 }
 
+extern "C" {
+
+int dd_aux_analyze(int64_t nblk, const int64_t* blk_size, const int64_t* colptr, const int32_t* rowidx,
+                   int32_t dtype, const dd_aux_options* opt, dd_aux_handle_t* out) {
+  return analyze_impl(nblk, blk_size, colptr, rowidx, dtype, opt, 0, nullptr, out);
+}
+
 int dd_aux_get_info(dd_aux_handle_t h, dd_aux_info* info) {
   if (!h) return fail(-1, "handle is NULL");
   if (!info) return fail(-2, "info is NULL");
@@ -728,6 +813,9 @@ int dd_aux_get_info(dd_aux_handle_t h, dd_aux_info* info) {
   info->work_bytes = h->work_bytes;
   info->dtype = h->dtype;
   info->order_used = h->order_used;
+  info->n_schur = h->n_schur;
+  info->n_groups = h->n_schur ? (int64_t)h->grp_ptr.size() - 1 : 0;
+  info->n_aux_dof = h->n_aux_dof;
   return DD_OK;
 }
 
@@ -792,6 +880,12 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     for (size_t q = 0; q < h->spsegs.size(); ++q) sp[q].voff = val_offset[h->spsegs[q].voff];
   }
   CUDA_TRY(cudaMemcpyAsync(F, h->blob.data.data(), h->blob.data.size(), cudaMemcpyHostToDevice, st));
+  if (h->n_schur > 0) {  // identity row maps of the kept (never pivoted) blocks
+    CUDA_TRY(cudaMemcpyAsync(F + h->off_gperm + (size_t)h->r0 * 4, h->kept_gperm.data(), h->kept_gperm.size() * 4,
+                             cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(F + h->off_ginv + (size_t)(h->n - (int64_t)h->kept_ginv.size()) * 4, h->kept_ginv.data(),
+                             h->kept_ginv.size() * 4, cudaMemcpyHostToDevice, st));
+  }
   // ---- K0 load list
   std::vector<LoadBlock> lbs;
   lbs.reserve(h->nnzb_in);
@@ -899,6 +993,8 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   // (options.use_graphs; SURVEY.md §8(a) a5 "graph-capture the whole level sequence")
   auto levels_body = [&](cudaStream_t st) -> int {
     CUDA_TRY(cudaMemsetAsync(k1.ipiv, 0, (size_t)h->n_pad * 4, st));
+    if (h->n_schur > 0)  // kept nodes are never factored: zero stats
+      CUDA_TRY(cudaMemsetAsync(F + h->off_stats, 0, (size_t)N * 8 * 8, st));
     CUDA_TRY(cudaMemsetAsync(totals_d, 0, 16 * sizeof(int64_t), st));
     if (k1.perturb_tau > 0) {  // reading L4 (opt-in): ||A||_inf of the caller's blocks before K1
       CUDA_TRY(cudaMemsetAsync(norm_d, 0, sizeof(unsigned long long), st));
@@ -1096,8 +1192,13 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
   return totals[7] ? DD_NONFINITE : (h->singular ? DD_ZERO_PIVOT : DD_OK);
 }
 
+enum { SW_FWD = 1, SW_D = 2, SW_BWD = 4, SW_ALL = 7 };
+
+// phases: SW_FWD forward sweep (levels ascending), SW_D the D^{-1} solve, SW_BWD backward sweep;
+// a Schur-mode handle's levels hold only its eliminated positions (kept rows are read / written
+// by the update kernels as struct rows, never solved)
 static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t yim, int64_t ldy, int nrhs,
-                       cudaStream_t st, double* part, double* T, const int* flag = nullptr) {
+                       cudaStream_t st, double* part, double* T, const int* flag = nullptr, int phases = SW_ALL) {
   // with a device flag the sweep may be skipped: its flops are not counted (conservative trace)
   const double fs = flag ? 0.0 : 1.0;
   const bool C = h->cplx;
@@ -1124,7 +1225,7 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
   a.ldT = pad8(std::max<int64_t>(h->nT, 2));
   a.Tim = C ? a.ldT * nrhs : 0;
   const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
-  for (int l = 0; l < (int)h->lv.size(); ++l) {
+  for (int l = 0; l < (int)h->lv.size() && (phases & SW_FWD); ++l) {
     const LevelRanges& R = h->lv[l];
     h->cur_level = l;
     SolveArgs b = a;
@@ -1142,13 +1243,13 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
     }
     LAUNCH_CHECK("k_fupd");
   }
-  {
+  if (phases & SW_D) {
     TraceScope ts(h, DD_PH_DSOLVE, 0.0, st);
     h->cur_level = -1;
-  launch_dsolve(C, a, st);
+    launch_dsolve(C, a, st);
   }
   LAUNCH_CHECK("k_dsolve");
-  for (int l = (int)h->lv.size() - 1; l >= 0; --l) {
+  for (int l = (int)h->lv.size() - 1; l >= 0 && (phases & SW_BWD); --l) {
     const LevelRanges& R = h->lv[l];
     h->cur_level = l;
     SolveArgs b = a;
@@ -1179,6 +1280,8 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
   if (!d_B) return fail(-5, "d_B is NULL");
   if (ldb < h->n) return fail(-6, "ldb < n");
   if (!d_work || ((uintptr_t)d_work & 255)) return fail(-7, "d_work is NULL or not 256-byte aligned");
+  if (h->n_schur > 0)
+    return fail(-1, "a Schur-mode (partial) factorization has no full solve: use dd_aux_condense / dd_aux_recover");
   if (!h->factored || h->factored_ptr != d_factor) return fail(DD_ERR_NOT_FACTORED, "d_factor holds no factorization of this handle");
   if (h->singular) return fail(DD_ERR_SINGULAR, "the factorization reported a zero pivot");
   const int refine = h->opt.refine_steps;
@@ -1527,6 +1630,314 @@ int dd_aux_get_level_trace(dd_aux_handle_t h, double* ms, double* flops) {
 int dd_aux_destroy(dd_aux_handle_t h) {
   delete h;
   return DD_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================ f3 / f2: Schur mode
+// Tables of a partial factorization (dd_aux_analyze_partial): export items, condensation gather
+// and recovery scatter lists, identity row maps of the kept blocks.
+static int build_schur_tables(dd_aux_handle_t h) {
+  const int N = h->S.nblk, NE = h->n_elim;
+  const int64_t NS = h->n_schur;
+  // groups = distinct schur_group values ascending; members by ascending target
+  std::vector<int32_t> idx(NS);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) {
+    return h->schur_group[a] != h->schur_group[b] ? h->schur_group[a] < h->schur_group[b]
+                                                  : h->schur_target[a] < h->schur_target[b];
+  });
+  h->grp_kept = idx;
+  h->grp_ptr.assign(1, 0);
+  h->grp_m.clear();
+  for (int64_t q = 0; q < NS; ++q) {
+    if (q > 0 && h->schur_group[idx[q]] == h->schur_group[idx[q - 1]] &&
+        h->schur_target[idx[q]] == h->schur_target[idx[q - 1]])
+      return fail(DD_ERR_PATTERN, "two kept blocks of group " + std::to_string(h->schur_group[idx[q]]) +
+                                      " have the same schur_target");
+    if (q > 0 && h->schur_group[idx[q]] != h->schur_group[idx[q - 1]]) h->grp_ptr.push_back(q);
+  }
+  h->grp_ptr.push_back(NS);
+  const int ng = (int)h->grp_ptr.size() - 1;
+  auto row_in = [&](int j, int i) -> int {  // row offset of position i inside panel j, -1 if absent
+    const NodeDev& nj = h->nodes[j];
+    int64_t ro = nj.sp;
+    for (int u : h->S.st[j]) {
+      if (u == i) return (int)ro;
+      ro += pad2(h->nodes[u].s);
+    }
+    return -1;
+  };
+  std::vector<SxItem> items;
+  std::vector<SxTile> tiles;
+  for (int g = 0; g < ng; ++g) {
+    int64_t m = 0;
+    std::vector<int64_t> off;
+    for (int64_t q = h->grp_ptr[g]; q < h->grp_ptr[g + 1]; ++q) {
+      off.push_back(m);
+      m += h->blk_size[NE + idx[q]];
+    }
+    h->grp_m.push_back(m);
+    for (int64_t qa = h->grp_ptr[g]; qa < h->grp_ptr[g + 1]; ++qa)
+      for (int64_t qb = h->grp_ptr[g]; qb < h->grp_ptr[g + 1]; ++qb) {
+        const int ta = h->S.pos[NE + idx[qa]], tb = h->S.pos[NE + idx[qb]];
+        SxItem it{};
+        it.rows = h->nodes[ta].s;
+        it.cols = h->nodes[tb].s;
+        it.group = g;
+        it.m = (int32_t)m;
+        it.dst = off[qa - h->grp_ptr[g]] + off[qb - h->grp_ptr[g]] * m;
+        if (ta == tb) {
+          it.mode = 2;
+          it.src = h->nodes[ta].panel;
+          it.ld = h->nodes[ta].ld;
+        } else {
+          const int lo = std::min(ta, tb), hi = std::max(ta, tb);
+          const int ro = row_in(lo, hi);
+          if (ro < 0) {
+            it.mode = 3;
+          } else {
+            it.mode = ta > tb ? 0 : 1;
+            it.src = h->nodes[lo].panel + ro;
+            it.ld = h->nodes[lo].ld;
+          }
+        }
+        const int id = (int)items.size();
+        items.push_back(it);
+        for (int r0 = 0; r0 < it.rows; r0 += 32)
+          for (int c0 = 0; c0 < it.cols; c0 += 32) tiles.push_back(SxTile{id, r0, c0, 0});
+      }
+  }
+  h->n_sx_tiles = (int)tiles.size();
+  // condensation gather: per auxiliary block, its kept copies in ascending position
+  std::vector<std::vector<int>> copies(h->n_aux);
+  for (int64_t k = 0; k < NS; ++k) copies[h->schur_target[k]].push_back(h->S.pos[NE + k]);
+  std::vector<SgItem> sg;
+  std::vector<int32_t> contrib;
+  for (int64_t I = 0; I < h->n_aux; ++I) {
+    if (copies[I].empty()) continue;
+    std::sort(copies[I].begin(), copies[I].end());
+    SgItem it{};
+    it.aux_row = h->aux_odof[I];
+    it.s = (int32_t)h->blk_size[NE + [&] {  // size of any copy
+      for (int64_t k = 0; k < NS; ++k)
+        if (h->schur_target[k] == I) return (int)k;
+      return 0;
+    }()];
+    it.c0 = (int32_t)contrib.size();
+    for (int t : copies[I]) contrib.push_back(t);
+    it.c1 = (int32_t)contrib.size();
+    sg.push_back(it);
+  }
+  h->n_sg_items = (int)sg.size();
+  // recovery scatter: per kept position, the auxiliary rows of its target
+  std::vector<SgItem> ss;
+  for (int64_t k = 0; k < NS; ++k) {
+    SgItem it{};
+    it.aux_row = h->aux_odof[h->schur_target[k]];
+    it.s = (int32_t)h->blk_size[NE + k];
+    it.c0 = h->S.pos[NE + k];
+    ss.push_back(it);
+  }
+  h->n_ss_items = (int)ss.size();
+  // identity row maps of the kept blocks: rows [r0, n_pad), original DoFs [odof(NE), n)
+  h->kept_gperm.clear();
+  h->kept_ginv.clear();
+  for (int t = NE; t < N; ++t) {
+    const NodeDev& nd = h->nodes[t];
+    for (int m = 0; m < nd.sp; ++m) h->kept_gperm.push_back(m < nd.s ? (int32_t)(nd.odof + m) : -1);
+  }
+  for (int64_t o = h->odof_blk[NE]; o < h->n; ++o) {
+    const int blk = (int)(std::upper_bound(h->odof_blk.begin(), h->odof_blk.end(), o) - h->odof_blk.begin()) - 1;
+    const NodeDev& nd = h->nodes[h->S.pos[blk]];
+    h->kept_ginv.push_back((int32_t)(nd.ydof + (o - nd.odof)));
+  }
+  Blob& B = h->blob;
+  h->off_sx_items = B.put(items);
+  h->off_sx_tiles = B.put(tiles);
+  h->off_sg_items = B.put(sg);
+  h->off_sg_contrib = B.put(contrib);
+  h->off_ss_items = B.put(ss);
+  h->off_soff = B.put(std::vector<int64_t>(ng, 0));
+  return DD_OK;
+}
+
+extern "C" {
+
+int dd_aux_analyze_partial(int64_t nblk, const int64_t* blk_size, const int64_t* colptr, const int32_t* rowidx,
+                           int32_t dtype, const dd_aux_options* opt, int64_t n_schur, const int32_t* schur_target,
+                           const int32_t* schur_group, int64_t n_aux, const int64_t* aux_blk_size,
+                           dd_aux_handle_t* out) {
+  if (!out) return fail(-12, "out is NULL");
+  if (nblk <= 0) return fail(-1, "nblk must be > 0");
+  if (!blk_size) return fail(-2, "blk_size is NULL");
+  if (n_schur < 1 || n_schur >= nblk) return fail(-7, "n_schur must be in [1, nblk)");
+  if (!schur_target) return fail(-8, "schur_target is NULL");
+  if (!schur_group) return fail(-9, "schur_group is NULL");
+  if (n_aux < 1) return fail(-10, "n_aux must be >= 1");
+  if (!aux_blk_size) return fail(-11, "aux_blk_size is NULL");
+  for (int64_t k = 0; k < n_schur; ++k) {
+    const int32_t I = schur_target[k];
+    if (I < 0 || I >= n_aux) return fail(-8, "schur_target out of range");
+    if (schur_group[k] < 0) return fail(-9, "schur_group must be >= 0");
+    if (aux_blk_size[I] != blk_size[nblk - n_schur + k])
+      return fail(-11, "kept block " + std::to_string(nblk - n_schur + k) + " and its target auxiliary block " +
+                           std::to_string(I) + " differ in size");
+  }
+  dd_aux_handle_t h = nullptr;
+  const SchurIn sin{schur_target, schur_group, n_aux, aux_blk_size};
+  const int rc = analyze_impl(nblk, blk_size, colptr, rowidx, dtype, opt, n_schur, &sin, &h);
+  if (rc) return rc;
+  *out = h;
+  return DD_OK;
+}
+
+int dd_aux_schur_cliques(dd_aux_handle_t h, int64_t* ngroups, int64_t* clq_ptr, int32_t* clq_blk) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (h->n_schur == 0) return fail(-1, "not a Schur-mode handle");
+  const int64_t ng = (int64_t)h->grp_ptr.size() - 1;
+  if (ngroups) *ngroups = ng;
+  if (clq_ptr)
+    for (int64_t g = 0; g <= ng; ++g) clq_ptr[g] = h->grp_ptr[g];
+  if (clq_blk)
+    for (int64_t q = 0; q < h->n_schur; ++q) clq_blk[q] = h->schur_target[h->grp_kept[q]];
+  return DD_OK;
+}
+
+int dd_aux_schur_export(dd_aux_handle_t h, const void* d_factor, void* d_S, const int64_t* S_offset, void* stream) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (h->n_schur == 0) return fail(-1, "not a Schur-mode handle");
+  if (!d_factor) return fail(-2, "d_factor is NULL");
+  if (!d_S) return fail(-3, "d_S is NULL");
+  if (!S_offset) return fail(-4, "S_offset is NULL");
+  if (!h->factored || h->factored_ptr != d_factor) return fail(DD_ERR_NOT_FACTORED, "not factored");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t ng = (int64_t)h->grp_ptr.size() - 1;
+  h->soff_host.assign(S_offset, S_offset + ng);  // kept alive until the next call (async upload)
+  uint8_t* F = (uint8_t*)const_cast<void*>(d_factor);
+  CUDA_TRY(cudaMemcpyAsync(F + h->off_soff, h->soff_host.data(), ng * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  SchurExportArgs a{(const SxItem*)(F + h->off_sx_items), (const SxTile*)(F + h->off_sx_tiles),
+                    (const double*)(F + h->off_arena), h->cplx ? h->nA : 0, (double*)d_S,
+                    (const int64_t*)(F + h->off_soff)};
+  {
+    TraceScope ts(h, DD_PH_SCHUR, 0.0, st);
+    launch_schur_export(h->cplx, a, h->n_sx_tiles, st);
+  }
+  LAUNCH_CHECK("k_schur_export");
+  return DD_OK;
+}
+
+}  // extern "C"
+
+// condense (mode 0) / recover (mode 1) of one chunk of <= SOLVE_MAX_COLS columns
+static int schur_sweep(dd_aux_handle_t h, int mode, const void* d_factor, int64_t nrhs, const void* d_F, int64_t ldf,
+                       void* d_V, int64_t ldv, void* d_X, int64_t ldx, void* d_work, cudaStream_t st) {
+  const bool C = h->cplx;
+  const int planes = C ? 2 : 1;
+  const uint8_t* F = (const uint8_t*)d_factor;
+  uint8_t* Wb = (uint8_t*)d_work;
+  const int64_t ldy = pad8(h->n_pad);
+  double* y = (double*)Wb;
+  const int64_t yim = C ? ldy * nrhs : 0;
+  double* Bsave = (double*)(Wb + align256((size_t)ldy * nrhs * planes * sizeof(double)));
+  double* berr_d = (double*)((uint8_t*)Bsave + align256((size_t)h->n * nrhs * planes * sizeof(double)));
+  int* flag_d = (int*)((uint8_t*)berr_d + align256((size_t)nrhs * sizeof(double)));
+  double* part = (double*)((uint8_t*)flag_d + 256);
+  double* Tbuf = (double*)((uint8_t*)part + align256(bupd_part_bytes(C, (int)nrhs)));
+  PermArgs pa{};
+  pa.gperm = (const int*)(F + h->off_gperm);
+  pa.nrows = h->n_pad;
+  pa.rowlim = h->r0;  // kept rows start at zero
+  pa.nrhs = (int)nrhs;
+  pa.y = y;
+  pa.yim = yim;
+  pa.ldy = ldy;
+  pa.src = (const double*)d_F;
+  pa.lds = ldf;
+  {
+    TraceScope ts(h, DD_PH_PERM, 0.0, st);
+    launch_perm_in(C, pa, st);
+  }
+  LAUNCH_CHECK("k_perm_in");
+  SchurVecArgs sv{};
+  sv.nd = (const NodeDev*)(F + h->off_nodes);
+  sv.contrib = (const int*)(F + h->off_sg_contrib);
+  sv.y = y;
+  sv.yim = yim;
+  sv.ldy = ldy;
+  sv.G = (double*)d_V;
+  sv.ldg = ldv;
+  sv.nrhs = (int)nrhs;
+  if (mode == 0) {  // condense: forward sweep, then G += kept rows (fixed order)
+    int rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf, nullptr, SW_FWD);
+    if (rc) return rc;
+    sv.items = (const SgItem*)(F + h->off_sg_items);
+    {
+      TraceScope ts(h, DD_PH_SCHUR, 0.0, st);
+      launch_schur_gather(C, sv, h->n_sg_items, st);
+    }
+    LAUNCH_CHECK("k_schur_gather");
+    return DD_OK;
+  }
+  // recover: forward sweep + D, kept rows <- x_b, backward sweep, x = P^T y
+  int rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf, nullptr, SW_FWD | SW_D);
+  if (rc) return rc;
+  sv.items = (const SgItem*)(F + h->off_ss_items);
+  {
+    TraceScope ts(h, DD_PH_SCHUR, 0.0, st);
+    launch_schur_scatter(C, sv, h->n_ss_items, st);
+  }
+  LAUNCH_CHECK("k_schur_scatter");
+  rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf, nullptr, SW_BWD);
+  if (rc) return rc;
+  pa.dst = (double*)d_X;
+  pa.ldd = ldx;
+  pa.accumulate = 0;
+  {
+    TraceScope ts(h, DD_PH_PERM, 0.0, st);
+    launch_perm_out(C, pa, st);
+  }
+  LAUNCH_CHECK("k_perm_out");
+  return DD_OK;
+}
+
+static int schur_call(dd_aux_handle_t h, int mode, const void* d_factor, int64_t nrhs, const void* d_F, int64_t ldf,
+                      void* d_V, int64_t ldv, void* d_X, int64_t ldx, void* d_work, void* stream) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (h->n_schur == 0) return fail(-1, "not a Schur-mode handle (dd_aux_analyze_partial)");
+  if (!d_factor) return fail(-2, "d_factor is NULL");
+  if (nrhs < 0) return fail(-3, "nrhs must be >= 0");
+  if (nrhs == 0) return DD_OK;
+  if (!d_F) return fail(-4, "d_F is NULL");
+  if (ldf < h->n) return fail(-5, "ldf < n");
+  if (!d_V) return fail(-6, mode ? "d_Xb is NULL" : "d_G is NULL");
+  if (ldv < h->n_aux_dof) return fail(-7, "leading dimension of the auxiliary block < n_aux DoFs");
+  if (mode == 1 && !d_X) return fail(-8, "d_X is NULL");
+  if (mode == 1 && ldx < h->n) return fail(-9, "ldx < n");
+  if (!d_work || ((uintptr_t)d_work & 255)) return fail(-10, "d_work is NULL or not 256-byte aligned");
+  if (!h->factored || h->factored_ptr != d_factor) return fail(DD_ERR_NOT_FACTORED, "not factored");
+  if (h->singular) return fail(DD_ERR_SINGULAR, "the partial factorization reported a zero pivot");
+  const size_t es = h->cplx ? 16 : 8;
+  for (int64_t c0 = 0; c0 < nrhs; c0 += SOLVE_MAX_COLS) {
+    const int64_t w = std::min(SOLVE_MAX_COLS, nrhs - c0);
+    const int rc = schur_sweep(h, mode, d_factor, w, (const uint8_t*)d_F + (size_t)c0 * ldf * es, ldf,
+                               (uint8_t*)d_V + (size_t)c0 * ldv * es, ldv,
+                               d_X ? (uint8_t*)d_X + (size_t)c0 * ldx * es : nullptr, ldx, d_work, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return DD_OK;
+}
+
+extern "C" {
+
+int dd_aux_condense(dd_aux_handle_t h, const void* d_factor, int64_t nrhs, const void* d_F, int64_t ldf, void* d_G,
+                    int64_t ldg, void* d_work, void* stream) {
+  return schur_call(h, 0, d_factor, nrhs, d_F, ldf, d_G, ldg, nullptr, 0, d_work, stream);
+}
+
+int dd_aux_recover(dd_aux_handle_t h, const void* d_factor, int64_t nrhs, const void* d_F, int64_t ldf,
+                   const void* d_Xb, int64_t ldxb, void* d_X, int64_t ldx, void* d_work, void* stream) {
+  return schur_call(h, 1, d_factor, nrhs, d_F, ldf, const_cast<void*>(d_Xb), ldxb, d_X, ldx, d_work, stream);
 }
 
 }  // extern "C"

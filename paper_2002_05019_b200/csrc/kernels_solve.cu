@@ -50,7 +50,7 @@ __global__ void k_perm_in(PermArgs a) {
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.nrows; g += (int64_t)gridDim.x * blockDim.x) {
     const int o = a.gperm[g];
     double re = 0.0, im = 0.0;
-    if (o >= 0) {
+    if (o >= 0 && (a.rowlim == 0 || g < a.rowlim)) {
       int64_t e = (int64_t)o + (int64_t)c * a.lds;
       if (C) {
         re = a.src[2 * e];

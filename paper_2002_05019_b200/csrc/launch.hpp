@@ -106,6 +106,7 @@ struct SolveArgs {
 struct PermArgs {
   const int* gperm;   // padded position row -> original DoF (-1 pad)
   int64_t nrows;      // padded n
+  int64_t rowlim;     // perm_in: rows >= rowlim are zeroed instead of gathered (0 = no limit)
   int nrhs;
   const double* src;  // interleaved (complex) or real, column-major, leading dim lds
   int64_t lds;
@@ -155,6 +156,46 @@ struct AsmArgs {
 };
 
 void launch_assemble(bool cplx, bool sym, const AsmArgs& a, int nitems, cudaStream_t st);
+
+// ---- f3/f2: partial (Schur-mode) factorization helpers (kernels_schur.cu)
+struct SxItem {        // one (member a, member b) sub-block of group g's dense Schur complement S_g
+  int64_t src;         // element offset (re plane) in the arena of the stored block's element (0, 0)
+  int64_t dst;         // element offset of S_g[ra, cb] inside S_g (ra + cb * m)
+  int32_t ld;          // leading dimension of the stored block (panel ld)
+  int32_t mode;        // 0: S = stored; 1: S = stored^T; 2: diagonal block (lower stored, mirrored); 3: zero
+  int32_t rows, cols;  // s_a, s_b
+  int32_t group, m;    // group index; m_g (leading dimension of S_g)
+};
+struct SxTile {        // 32 x 32 output tile of an item
+  int32_t item, r0, c0, pad;
+};
+struct SchurExportArgs {
+  const SxItem* items;
+  const SxTile* tiles;
+  const double* arena;
+  int64_t aim;
+  double* S;            // caller's output (interleaved complex or real)
+  const int64_t* soff;  // [ngroups] element offsets of S_g in S (uploaded per call)
+};
+struct SgItem {        // aux block I of the condensed right-hand side: its kept copies
+  int64_t aux_row;     // first row of I in the auxiliary DoF numbering
+  int32_t s;           // s_I
+  int32_t c0, c1;      // range in the contributor list (kept positions, ascending)
+  int32_t pad;
+};
+struct SchurVecArgs {
+  const NodeDev* nd;
+  const SgItem* items;   // gather: per aux block; scatter: per kept node (c0 = its position)
+  const int* contrib;    // kept positions
+  double* y;             // solve vector (position order, planar)
+  int64_t yim, ldy;
+  double* G;             // gather: caller's aux-ordered block (interleaved), += ; scatter: source
+  int64_t ldg;
+  int nrhs;
+};
+void launch_schur_export(bool cplx, const SchurExportArgs& a, int ntiles, cudaStream_t st);
+void launch_schur_gather(bool cplx, const SchurVecArgs& a, int nitems, cudaStream_t st);
+void launch_schur_scatter(bool cplx, const SchurVecArgs& a, int nitems, cudaStream_t st);
 int asm_chunk();
 
 void launch_load(bool cplx, const double* vals, const LoadBlock* lb, int nblocks, int64_t max_elems, double* arena,

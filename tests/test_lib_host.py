@@ -161,3 +161,40 @@ def test_interface_size_limit():
         assert ei.value.code == dd.DD_ERR_PATTERN and str(lim) in str(ei.value)
         h = dd.dd_aux_analyze([lim], [0, 1], [0], dtype=dt)
         dd.dd_aux_destroy(h)
+
+
+def test_schur_mode_host_tables():
+    """dd_aux_analyze_partial (f3): kept blocks last, eliminated part scheduled alone, cliques =
+    each subdomain's interfaces, flops / levels only over the eliminated positions."""
+    import paper_2002_05019_b200 as dd
+    from dd_inputs.fem import fem_dd, schur_block_problem
+    import oracle
+    m = fem_dd(2, 2, 2, 6, seed=0)
+    prob, ns, tgt, grp, auxs, info = schur_block_problem(m, leaf=16)
+    o = dd.dd_aux_default_options(dd.DD_ORDER_NATURAL)
+    h = dd.dd_aux_analyze_partial(prob.blk_size, prob.colptr, prob.rowidx, tgt, grp, auxs, dd.DD_REAL64, o)
+    inf = dd.dd_aux_get_info(h)
+    assert inf["n_schur"] == ns and inf["n_groups"] == m.nsub and inf["n_aux_dof"] == m.n_dual
+    assert dd.dd_aux_schur_cliques(h) == [m.sub_ifaces[p] for p in range(m.nsub)]
+    order = dd.dd_aux_get_order(h)
+    assert list(order[-ns:]) == list(range(prob.nblk - ns, prob.nblk))
+    sym = oracle.symbolic(prob.nblk, prob.colptr, prob.rowidx, list(order))
+    ne = prob.nblk - ns
+    fl = sum(float(prob.blk_size[k]) ** 3 / 3 + sum(float(prob.blk_size[i]) for i in sym["struct"][k]) *
+             float(prob.blk_size[k]) ** 2 + sum(float(prob.blk_size[i]) for i in sym["struct"][k]) ** 2 *
+             float(prob.blk_size[k]) for k in order[:ne])
+    assert inf["flops_factor"] == pytest.approx(fl, rel=1e-12)
+    parent, level, _ = dd.dd_aux_get_etree(h)
+    assert inf["n_levels"] == int(max(level[k] for k in order[:ne])) + 1
+    # subdomains are independent: no eliminated block's struct leaves its subdomain
+    nbp = info["nblk_per_sub"]
+    for k in order[:ne]:
+        p = k // nbp
+        for i in sym["struct"][k]:
+            assert (i < ne and i // nbp == p) or (i >= ne and grp[i - ne] == p)
+    # errors: size mismatch, bad target, n_schur out of range
+    with pytest.raises(dd.DDAuxError):
+        dd.dd_aux_analyze_partial(prob.blk_size, prob.colptr, prob.rowidx, tgt, grp, auxs + 1, dd.DD_REAL64, o)
+    with pytest.raises(dd.DDAuxError):
+        dd.dd_aux_analyze_partial(prob.blk_size, prob.colptr, prob.rowidx, tgt + 100, grp, auxs, dd.DD_REAL64, o)
+    dd.dd_aux_destroy(h)
