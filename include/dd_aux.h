@@ -132,6 +132,11 @@ int dd_aux_get_order(dd_aux_handle_t h, int32_t* order);
  * either pointer may be NULL.  nnz_struct (if non-NULL) receives sum_k |struct(k)|. */
 int dd_aux_get_etree(dd_aux_handle_t h, int32_t* parent, int32_t* level, int64_t* nnz_struct);
 
+/* struct(k) of every block k: the blocks adjacent to k when it is eliminated
+ * (after fill), as ORIGINAL block ids in elimination order.  Host out: st_ptr [nblk+1] (by block
+ * id), st_blk [nnz_struct]; either may be NULL (st_ptr alone gives the sizes). */
+int dd_aux_get_struct(dd_aux_handle_t h, int64_t* st_ptr, int32_t* st_blk);
+
 /* Bytes of d_work needed by dd_aux_solve for nrhs right-hand sides. */
 int dd_aux_solve_work_bytes(dd_aux_handle_t h, int64_t nrhs, size_t* bytes);
 
@@ -201,6 +206,12 @@ int dd_aux_assemble_work_bytes(dd_aux_handle_t h, int64_t nclq, const int64_t* c
 int dd_aux_assemble(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, const int32_t* clq_blk,
                     const void* d_S, const int64_t* S_offset, int32_t symmetrize, const int64_t* val_offset,
                     void* d_vals, void* d_work, void* stream);
+/* Same, accumulating: d_vals += the clique sum for every block some clique covers; blocks no
+ * clique covers keep their values (f4: the top separators' own blocks plus the Schur contributions
+ * of the subtrees factored on other GPUs).  symmetrize must be 0 (the cliques must be symmetric). */
+int dd_aux_assemble_acc(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, const int32_t* clq_blk,
+                        const void* d_S, const int64_t* S_offset, int32_t symmetrize, const int64_t* val_offset,
+                        void* d_vals, void* d_work, void* stream);
 /* Algorithmic (unique) HBM bytes of the last dd_aux_assemble: every output element written once,
  * every contributing S_p element read once (the mirrored S_p[J, I] too for the symmetric part of
  * an off-diagonal block). */
@@ -289,6 +300,13 @@ int dd_aux_condense(dd_aux_handle_t h, const void* d_factor, int64_t nrhs, const
  * kept rows = the copies of x_b; d_X may equal d_F).  Asynchronous. */
 int dd_aux_recover(dd_aux_handle_t h, const void* d_factor, int64_t nrhs, const void* d_F, int64_t ldf,
                    const void* d_Xb, int64_t ldxb, void* d_X, int64_t ldx, void* d_work, void* stream);
+
+/* Residual R = B - A X over the handle's ORIGINAL blocks d_vals (both triangles; the kernel of
+ * a8's refinement, K6), all n x nrhs column-major in the ORIGINAL DoF order.  Needs a factored
+ * d_factor (its row maps); d_work: dd_aux_solve_work_bytes(h, nrhs).  Works on Schur-mode handles
+ * (f4 refines across a partial handle per GPU plus the top handle).  Asynchronous. */
+int dd_aux_residual(dd_aux_handle_t h, const void* d_factor, const void* d_vals, int64_t nrhs, const void* d_B,
+                    int64_t ldb, const void* d_X, int64_t ldx, void* d_R, int64_t ldr, void* d_work, void* stream);
 
 int dd_aux_destroy(dd_aux_handle_t h);
 

@@ -23,7 +23,7 @@ __all__ = ["DD_REAL64", "DD_COMPLEX128", "DD_ORDER_AUTO", "DD_ORDER_ND", "DD_ORD
            "dd_aux_set_refine", "dd_aux_set_graphs", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_get_level_trace", "dd_aux_assemble_work_bytes", "dd_aux_assemble",
            "dd_aux_last_assemble_bytes", "cliques_to_csr", "AuxSolver", "LIB_PATH", "EXPORTED_SYMBOLS", "PHASES",
            "dd_aux_analyze_partial", "dd_aux_schur_cliques", "dd_aux_schur_export", "dd_aux_condense",
-           "dd_aux_recover", "SchurSolver"]
+           "dd_aux_recover", "SchurSolver", "dd_aux_get_struct", "dd_aux_assemble_acc", "dd_aux_residual"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdd_aux.so")
 
@@ -37,7 +37,8 @@ EXPORTED_SYMBOLS = ["dd_aux_default_options", "dd_aux_analyze", "dd_aux_get_info
                     "dd_aux_get_pivots", "dd_aux_set_refine", "dd_aux_set_graphs", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_get_level_trace", "dd_aux_destroy",
                     "dd_aux_last_error", "dd_aux_version", "dd_aux_assemble_work_bytes", "dd_aux_assemble",
                     "dd_aux_last_assemble_bytes", "dd_aux_analyze_partial", "dd_aux_schur_cliques",
-                    "dd_aux_schur_export", "dd_aux_condense", "dd_aux_recover"]
+                    "dd_aux_schur_export", "dd_aux_condense", "dd_aux_recover", "dd_aux_get_struct",
+                    "dd_aux_assemble_acc", "dd_aux_residual"]
 PHASES = ["load", "k1_diag_bk", "rowperm", "k2_panel", "k3_update", "stats", "perm", "fdiag", "fupd", "dsolve",
           "bupd", "bdiag", "spmv", "linv", "assemble", "schur"]
 
@@ -104,6 +105,9 @@ def _load():
         "dd_aux_analyze_partial": (ctypes.c_int, [i64, pi64, pi64, pi32, i32, ctypes.POINTER(dd_aux_options), i64,
                                                    pi32, pi32, i64, pi64, ctypes.POINTER(P)]),
         "dd_aux_schur_cliques": (ctypes.c_int, [P, pi64, pi64, pi32]),
+        "dd_aux_get_struct": (ctypes.c_int, [P, pi64, pi32]),
+        "dd_aux_residual": (ctypes.c_int, [P, P, P, i64, P, i64, P, i64, P, i64, P, P]),
+        "dd_aux_assemble_acc": (ctypes.c_int, [P, i64, pi64, pi32, P, pi64, i32, pi64, P, P, P]),
         "dd_aux_schur_export": (ctypes.c_int, [P, P, P, pi64, P]),
         "dd_aux_condense": (ctypes.c_int, [P, P, i64, P, i64, P, i64, P, P]),
         "dd_aux_recover": (ctypes.c_int, [P, P, i64, P, i64, P, i64, P, i64, P, P]),
@@ -215,6 +219,16 @@ def dd_aux_get_etree(h):
     return parent, level, int(nnz.value)
 
 
+def dd_aux_get_struct(h):
+    """{block id: [struct blocks in elimination order]} as (st_ptr, st_blk) arrays."""
+    n = dd_aux_get_info(h)["nblk"]
+    ptr = np.empty(n + 1, dtype=np.int64)
+    _check(_lib.dd_aux_get_struct(h, _np_ptr(ptr, ctypes.c_int64), None))
+    blk = np.empty(max(int(ptr[-1]), 1), dtype=np.int32)
+    _check(_lib.dd_aux_get_struct(h, None, _np_ptr(blk, ctypes.c_int32)))
+    return ptr, blk[:int(ptr[-1])]
+
+
 def dd_aux_solve_work_bytes(h, nrhs: int) -> int:
     b = ctypes.c_size_t()
     _check(_lib.dd_aux_solve_work_bytes(h, int(nrhs), ctypes.byref(b)))
@@ -314,6 +328,20 @@ def dd_aux_assemble(h, clq_ptr, clq_blk, d_S, S_offset, val_offset, d_vals, d_wo
     return _check(rc)
 
 
+def dd_aux_assemble_acc(h, clq_ptr, clq_blk, d_S, S_offset, val_offset, d_vals, d_work, symmetrize=False,
+                        stream=None):
+    """d_vals += sum of the cliques' contributions (blocks no clique covers are left as they are)."""
+    cp = np.ascontiguousarray(clq_ptr, dtype=np.int64)
+    cb = np.ascontiguousarray(clq_blk, dtype=np.int32)
+    so = np.ascontiguousarray(S_offset, dtype=np.int64)
+    vo = np.ascontiguousarray(val_offset, dtype=np.int64)
+    rc = _lib.dd_aux_assemble_acc(h, len(cp) - 1, _np_ptr(cp, ctypes.c_int64), _np_ptr(cb, ctypes.c_int32),
+                                  _dev_ptr(d_S), _np_ptr(so, ctypes.c_int64), int(bool(symmetrize)),
+                                  _np_ptr(vo, ctypes.c_int64), _dev_ptr(d_vals), _dev_ptr(d_work),
+                                  _stream_ptr(stream))
+    return _check(rc)
+
+
 def dd_aux_last_assemble_bytes(h) -> float:
     return float(_lib.dd_aux_last_assemble_bytes(h))
 
@@ -379,6 +407,16 @@ def dd_aux_recover(h, d_factor, d_F, d_Xb, d_X, d_work, stream=None):
     _, _, ldx = _cm(d_X)
     _check(_lib.dd_aux_recover(h, _dev_ptr(d_factor), int(nrhs), _dev_ptr(d_F), int(ldf), _dev_ptr(d_Xb), int(ldxb),
                                _dev_ptr(d_X), int(ldx), _dev_ptr(d_work), _stream_ptr(stream)))
+
+
+def dd_aux_residual(h, d_factor, d_vals, d_B, d_X, d_R, d_work, stream=None):
+    """R = B - A X over the handle's original blocks (column-major CUDA tensors)."""
+    _, nrhs, ldb = _cm(d_B)
+    _, _, ldx = _cm(d_X)
+    _, _, ldr = _cm(d_R)
+    _check(_lib.dd_aux_residual(h, _dev_ptr(d_factor), _dev_ptr(d_vals), int(nrhs), _dev_ptr(d_B), int(ldb),
+                                _dev_ptr(d_X), int(ldx), _dev_ptr(d_R), int(ldr), _dev_ptr(d_work),
+                                _stream_ptr(stream)))
 
 
 def dd_aux_destroy(h):

@@ -837,6 +837,22 @@ int dd_aux_get_etree(dd_aux_handle_t h, int32_t* parent, int32_t* level, int64_t
   return DD_OK;
 }
 
+int dd_aux_get_struct(dd_aux_handle_t h, int64_t* st_ptr, int32_t* st_blk) {
+  if (!h) return fail(-1, "handle is NULL");
+  const int N = h->S.nblk;
+  std::vector<int64_t> cnt(N + 1, 0);
+  for (int t = 0; t < N; ++t) cnt[h->S.order[t] + 1] = (int64_t)h->S.st[t].size();
+  for (int b = 0; b < N; ++b) cnt[b + 1] += cnt[b];
+  if (st_ptr)
+    for (int b = 0; b <= N; ++b) st_ptr[b] = cnt[b];
+  if (st_blk)
+    for (int t = 0; t < N; ++t) {
+      int64_t o = cnt[h->S.order[t]];
+      for (int u : h->S.st[t]) st_blk[o++] = h->S.order[u];
+    }
+  return DD_OK;
+}
+
 // The solve's column-indexed grids put the right-hand-side tile on gridDim.y (<= 65535): a call
 // with more columns runs in chunks of SOLVE_MAX_COLS (columns are independent, and every kernel's
 // per-column result is independent of how many columns are solved together, so chunking is
@@ -1476,9 +1492,28 @@ int dd_aux_assemble_work_bytes(dd_aux_handle_t h, int64_t nclq, const int64_t* c
   return DD_OK;
 }
 
+static int assemble_impl(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, const int32_t* clq_blk,
+                         const void* d_S, const int64_t* S_offset, int32_t symmetrize, const int64_t* val_offset,
+                         void* d_vals, void* d_work, void* stream, int accumulate);
+
 int dd_aux_assemble(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, const int32_t* clq_blk,
                     const void* d_S, const int64_t* S_offset, int32_t symmetrize, const int64_t* val_offset,
                     void* d_vals, void* d_work, void* stream) {
+  return assemble_impl(h, nclq, clq_ptr, clq_blk, d_S, S_offset, symmetrize, val_offset, d_vals, d_work, stream, 0);
+}
+
+int dd_aux_assemble_acc(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, const int32_t* clq_blk,
+                        const void* d_S, const int64_t* S_offset, int32_t symmetrize, const int64_t* val_offset,
+                        void* d_vals, void* d_work, void* stream) {
+  if (symmetrize) return fail(-7, "dd_aux_assemble_acc: symmetrize must be 0 (the cliques must be symmetric)");
+  return assemble_impl(h, nclq, clq_ptr, clq_blk, d_S, S_offset, 0, val_offset, d_vals, d_work, stream, 1);
+}
+
+}  // extern "C"
+
+static int assemble_impl(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, const int32_t* clq_blk,
+                         const void* d_S, const int64_t* S_offset, int32_t symmetrize, const int64_t* val_offset,
+                         void* d_vals, void* d_work, void* stream, int accumulate) {
   if (!h) return fail(-1, "handle is NULL");
   if (nclq > 0 && !d_S) return fail(-5, "d_S is NULL");
   if (nclq > 0 && !S_offset) return fail(-6, "S_offset is NULL");
@@ -1500,7 +1535,7 @@ int dd_aux_assemble(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, con
   if (!h->asm_cons.empty())
     CUDA_TRY(cudaMemcpyAsync(W + off_c, h->asm_cons.data(), h->asm_cons.size() * sizeof(AsmContrib),
                              cudaMemcpyHostToDevice, st));
-  AsmArgs a{(const AsmItem*)W, (const AsmContrib*)(W + off_c), (const double*)d_S, (double*)d_vals};
+  AsmArgs a{(const AsmItem*)W, (const AsmContrib*)(W + off_c), (const double*)d_S, (double*)d_vals, accumulate};
   {
     // algorithmic (unique) traffic: output written once + each contribution read once, plus the
     // mirrored block S_p[J, I] for the symmetric part of an off-diagonal block (a diagonal
@@ -1519,6 +1554,8 @@ int dd_aux_assemble(dd_aux_handle_t h, int64_t nclq, const int64_t* clq_ptr, con
   LAUNCH_CHECK("k_assemble");
   return DD_OK;
 }
+
+extern "C" {
 
 double dd_aux_last_assemble_bytes(dd_aux_handle_t h) { return h ? h->asm_bytes : 0.0; }
 
@@ -1938,6 +1975,78 @@ int dd_aux_condense(dd_aux_handle_t h, const void* d_factor, int64_t nrhs, const
 int dd_aux_recover(dd_aux_handle_t h, const void* d_factor, int64_t nrhs, const void* d_F, int64_t ldf,
                    const void* d_Xb, int64_t ldxb, void* d_X, int64_t ldx, void* d_work, void* stream) {
   return schur_call(h, 1, d_factor, nrhs, d_F, ldf, const_cast<void*>(d_Xb), ldxb, d_X, ldx, d_work, stream);
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// R = B - A X over the handle's ORIGINAL blocks (both triangles), original DoF order (a8's
+// residual, K6, exposed for callers that refine across several handles, e.g. f4).
+int dd_aux_residual(dd_aux_handle_t h, const void* d_factor, const void* d_vals, int64_t nrhs, const void* d_B,
+                    int64_t ldb, const void* d_X, int64_t ldx, void* d_R, int64_t ldr, void* d_work, void* stream) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (!d_factor) return fail(-2, "d_factor is NULL");
+  if (!d_vals) return fail(-3, "d_vals is NULL");
+  if (nrhs < 0) return fail(-4, "nrhs must be >= 0");
+  if (nrhs == 0) return DD_OK;
+  if (!d_B || ldb < h->n) return fail(-5, "d_B is NULL or ldb < n");
+  if (!d_X || ldx < h->n) return fail(-7, "d_X is NULL or ldx < n");
+  if (!d_R || ldr < h->n) return fail(-9, "d_R is NULL or ldr < n");
+  if (!d_work || ((uintptr_t)d_work & 255)) return fail(-11, "d_work is NULL or not 256-byte aligned");
+  if (!h->factored || h->factored_ptr != d_factor) return fail(DD_ERR_NOT_FACTORED, "not factored (row maps)");
+  if (nrhs > SOLVE_MAX_COLS) {
+    const size_t es = h->cplx ? 16 : 8;
+    for (int64_t c0 = 0; c0 < nrhs; c0 += SOLVE_MAX_COLS) {
+      const int rc = dd_aux_residual(h, d_factor, d_vals, std::min(SOLVE_MAX_COLS, nrhs - c0),
+                                     (const uint8_t*)d_B + (size_t)c0 * ldb * es, ldb,
+                                     (const uint8_t*)d_X + (size_t)c0 * ldx * es, ldx,
+                                     (uint8_t*)d_R + (size_t)c0 * ldr * es, ldr, d_work, stream);
+      if (rc) return rc;
+    }
+    return DD_OK;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool C = h->cplx;
+  const uint8_t* F = (const uint8_t*)d_factor;
+  const int64_t ldy = pad8(h->n_pad);
+  double* y = (double*)d_work;
+  const int64_t yim = C ? ldy * nrhs : 0;
+  SpmvArgs sa{};
+  sa.rows = (const SpRow*)(F + h->off_sprows);
+  sa.segs = (const SpSeg*)(F + h->off_spsegs);
+  sa.blk_size = (const int64_t*)(F + h->off_blksize);
+  sa.odof = (const int64_t*)(F + h->off_odof);
+  sa.vals = (const double*)d_vals;
+  sa.X = (const double*)d_X;
+  sa.ldx = ldx;
+  sa.Bsave = (const double*)d_B;
+  sa.ldb = ldb;
+  sa.ginv = (const int*)(F + h->off_ginv);
+  sa.y = y;
+  sa.yim = yim;
+  sa.ldy = ldy;
+  sa.nrhs = (int)nrhs;
+  {
+    TraceScope ts(h, DD_PH_SPMV, (C ? 8.0 : 2.0) * h->nnz_full * (double)nrhs, st);
+    launch_spmv(C, sa, h->n_sprows, st);
+  }
+  LAUNCH_CHECK("k_spmv");
+  PermArgs pa{};
+  pa.gperm = (const int*)(F + h->off_gperm);
+  pa.nrows = h->n_pad;
+  pa.nrhs = (int)nrhs;
+  pa.y = y;
+  pa.yim = yim;
+  pa.ldy = ldy;
+  pa.dst = (double*)d_R;
+  pa.ldd = ldr;
+  {
+    TraceScope ts(h, DD_PH_PERM, 0.0, st);
+    launch_perm_out(C, pa, st);
+  }
+  LAUNCH_CHECK("k_perm_out");
+  return DD_OK;
 }
 
 }  // extern "C"

@@ -60,10 +60,14 @@ __global__ void __launch_bounds__(AT * ATY) k_assemble(AsmArgs a) {
   // S_p element of the block is then read from HBM once (the pair S[r0, c0] / S[c0, r0] is read by
   // this CTA only)
   const bool mirror = SYM && it.pad;
+  if (a.accumulate && it.k0 == it.k1) return;  // accumulate mode: blocks no clique covers keep their values
   for (int r0 = mirror ? it.c0 : 0; r0 < it.rows; r0 += AT) {
     T acc[AT / ATY];
 #pragma unroll
-    for (int j = 0; j < AT / ATY; ++j) acc[j] = E::zero();
+    for (int j = 0; j < AT / ATY; ++j) {
+      const int row = r0 + tx, col = it.c0 + ty + ATY * j;  // accumulate (SYM = false only): start from the block
+      acc[j] = (a.accumulate && row < it.rows && col < it.cols) ? out[row + (int64_t)col * it.rows] : E::zero();
+    }
     for (int q = it.k0; q < it.k1; ++q) {
       const AsmContrib c = a.con[q];
       const T* Sp = S + c.soff;

@@ -153,6 +153,7 @@ struct AsmArgs {
   const AsmContrib* con;
   const double* S;     // interleaved complex or real
   double* vals;
+  int accumulate;      // 1: vals += sum (symmetrize off), uncovered blocks untouched
 };
 
 void launch_assemble(bool cplx, bool sym, const AsmArgs& a, int nitems, cudaStream_t st);
