@@ -659,7 +659,7 @@ def fem_arm(args, rank, world, local, dist):
         for ph, v in tr.items():
             if v["launches"]:
                 comb[f"{nm}:{ph}"] = v
-    dom = max(comb, key=lambda q: comb[q]["ms"])
+    dom = max((q for q in comb if q.startswith("sub:")), key=lambda q: comb[q]["ms"])  # the f3 kernels
     dk = comb[dom]
     achieved = dk["flops"] / (dk["ms"] * 1e-3) / 1e12 if dk["ms"] > 0 and dk["flops"] > 0 else None
     cpu = None

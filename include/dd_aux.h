@@ -308,6 +308,12 @@ int dd_aux_recover(dd_aux_handle_t h, const void* d_factor, int64_t nrhs, const 
 int dd_aux_residual(dd_aux_handle_t h, const void* d_factor, const void* d_vals, int64_t nrhs, const void* d_B,
                     int64_t ldb, const void* d_X, int64_t ldx, void* d_R, int64_t ldr, void* d_work, void* stream);
 
+/* Convergence report: per-column backward error ||b_j - A x_j||_inf /
+ * (||A||_inf ||x_j||_inf) (reading L6) of any X against the ORIGINAL blocks, computed on the device
+ * and copied to berr [nrhs] (host); synchronizes `stream`.  nrhs <= 32768. */
+int dd_aux_backward_error(dd_aux_handle_t h, const void* d_factor, const void* d_vals, int64_t nrhs, const void* d_B,
+                          int64_t ldb, const void* d_X, int64_t ldx, void* d_work, double* berr, void* stream);
+
 int dd_aux_destroy(dd_aux_handle_t h);
 
 const char* dd_aux_last_error(void);

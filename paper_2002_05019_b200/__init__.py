@@ -23,7 +23,8 @@ __all__ = ["DD_REAL64", "DD_COMPLEX128", "DD_ORDER_AUTO", "DD_ORDER_ND", "DD_ORD
            "dd_aux_set_refine", "dd_aux_set_graphs", "dd_aux_set_trace", "dd_aux_get_trace", "dd_aux_get_level_trace", "dd_aux_assemble_work_bytes", "dd_aux_assemble",
            "dd_aux_last_assemble_bytes", "cliques_to_csr", "AuxSolver", "LIB_PATH", "EXPORTED_SYMBOLS", "PHASES",
            "dd_aux_analyze_partial", "dd_aux_schur_cliques", "dd_aux_schur_export", "dd_aux_condense",
-           "dd_aux_recover", "SchurSolver", "dd_aux_get_struct", "dd_aux_assemble_acc", "dd_aux_residual"]
+           "dd_aux_recover", "SchurSolver", "dd_aux_get_struct", "dd_aux_assemble_acc", "dd_aux_residual",
+           "dd_aux_backward_error"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdd_aux.so")
 
@@ -38,7 +39,7 @@ EXPORTED_SYMBOLS = ["dd_aux_default_options", "dd_aux_analyze", "dd_aux_get_info
                     "dd_aux_last_error", "dd_aux_version", "dd_aux_assemble_work_bytes", "dd_aux_assemble",
                     "dd_aux_last_assemble_bytes", "dd_aux_analyze_partial", "dd_aux_schur_cliques",
                     "dd_aux_schur_export", "dd_aux_condense", "dd_aux_recover", "dd_aux_get_struct",
-                    "dd_aux_assemble_acc", "dd_aux_residual"]
+                    "dd_aux_assemble_acc", "dd_aux_residual", "dd_aux_backward_error"]
 PHASES = ["load", "k1_diag_bk", "rowperm", "k2_panel", "k3_update", "stats", "perm", "fdiag", "fupd", "dsolve",
           "bupd", "bdiag", "spmv", "linv", "assemble", "schur"]
 
@@ -107,6 +108,8 @@ def _load():
         "dd_aux_schur_cliques": (ctypes.c_int, [P, pi64, pi64, pi32]),
         "dd_aux_get_struct": (ctypes.c_int, [P, pi64, pi32]),
         "dd_aux_residual": (ctypes.c_int, [P, P, P, i64, P, i64, P, i64, P, i64, P, P]),
+        "dd_aux_backward_error": (ctypes.c_int, [P, P, P, i64, P, i64, P, i64, P, ctypes.POINTER(ctypes.c_double),
+                                                  P]),
         "dd_aux_assemble_acc": (ctypes.c_int, [P, i64, pi64, pi32, P, pi64, i32, pi64, P, P, P]),
         "dd_aux_schur_export": (ctypes.c_int, [P, P, P, pi64, P]),
         "dd_aux_condense": (ctypes.c_int, [P, P, i64, P, i64, P, i64, P, P]),
@@ -417,6 +420,17 @@ def dd_aux_residual(h, d_factor, d_vals, d_B, d_X, d_R, d_work, stream=None):
     _check(_lib.dd_aux_residual(h, _dev_ptr(d_factor), _dev_ptr(d_vals), int(nrhs), _dev_ptr(d_B), int(ldb),
                                 _dev_ptr(d_X), int(ldx), _dev_ptr(d_R), int(ldr), _dev_ptr(d_work),
                                 _stream_ptr(stream)))
+
+
+def dd_aux_backward_error(h, d_factor, d_vals, d_B, d_X, d_work, stream=None) -> np.ndarray:
+    """Per-column ||b - A x||_inf / (||A||_inf ||x||_inf) computed on the device (synchronizes)."""
+    _, nrhs, ldb = _cm(d_B)
+    _, _, ldx = _cm(d_X)
+    out = np.empty(nrhs, dtype=np.float64)
+    _check(_lib.dd_aux_backward_error(h, _dev_ptr(d_factor), _dev_ptr(d_vals), int(nrhs), _dev_ptr(d_B), int(ldb),
+                                      _dev_ptr(d_X), int(ldx), _dev_ptr(d_work), _np_ptr(out, ctypes.c_double),
+                                      _stream_ptr(stream)))
+    return out
 
 
 def dd_aux_destroy(h):

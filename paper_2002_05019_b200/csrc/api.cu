@@ -2050,3 +2050,62 @@ int dd_aux_residual(dd_aux_handle_t h, const void* d_factor, const void* d_vals,
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// Per-column backward error ||b - A x||_inf / (||A||_inf ||x||_inf) on the device (K6 residual,
+// ||A||_inf and k_berr; reading L6), copied to the host: a convergence report for any solve.
+int dd_aux_backward_error(dd_aux_handle_t h, const void* d_factor, const void* d_vals, int64_t nrhs, const void* d_B,
+                          int64_t ldb, const void* d_X, int64_t ldx, void* d_work, double* berr, void* stream) {
+  if (!h) return fail(-1, "handle is NULL");
+  if (!d_factor) return fail(-2, "d_factor is NULL");
+  if (!d_vals) return fail(-3, "d_vals is NULL");
+  if (nrhs < 0 || nrhs > SOLVE_MAX_COLS) return fail(-4, "nrhs must be in [0, 32768]");
+  if (nrhs == 0) return DD_OK;
+  if (!d_B || ldb < h->n) return fail(-5, "d_B is NULL or ldb < n");
+  if (!d_X || ldx < h->n) return fail(-7, "d_X is NULL or ldx < n");
+  if (!d_work || ((uintptr_t)d_work & 255)) return fail(-9, "d_work is NULL or not 256-byte aligned");
+  if (!berr) return fail(-10, "berr is NULL");
+  if (!h->factored || h->factored_ptr != d_factor) return fail(DD_ERR_NOT_FACTORED, "not factored (row maps)");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool C = h->cplx;
+  const int planes = C ? 2 : 1;
+  uint8_t* F = (uint8_t*)const_cast<void*>(d_factor);
+  uint8_t* Wb = (uint8_t*)d_work;
+  const int64_t ldy = pad8(h->n_pad);
+  double* y = (double*)Wb;
+  const int64_t yim = C ? ldy * nrhs : 0;
+  double* Bsave = (double*)(Wb + align256((size_t)ldy * nrhs * planes * sizeof(double)));
+  double* berr_d = (double*)((uint8_t*)Bsave + align256((size_t)h->n * nrhs * planes * sizeof(double)));
+  int* flag_d = (int*)((uint8_t*)berr_d + align256((size_t)nrhs * sizeof(double)));
+  unsigned long long* norm_d = (unsigned long long*)(F + h->off_norm);
+  SpmvArgs sa{};
+  sa.rows = (const SpRow*)(F + h->off_sprows);
+  sa.segs = (const SpSeg*)(F + h->off_spsegs);
+  sa.blk_size = (const int64_t*)(F + h->off_blksize);
+  sa.odof = (const int64_t*)(F + h->off_odof);
+  sa.vals = (const double*)d_vals;
+  sa.X = (const double*)d_X;
+  sa.ldx = ldx;
+  sa.Bsave = (const double*)d_B;
+  sa.ldb = ldb;
+  sa.ginv = (const int*)(F + h->off_ginv);
+  sa.y = y;
+  sa.yim = yim;
+  sa.ldy = ldy;
+  sa.nrhs = (int)nrhs;
+  launch_spmv(C, sa, h->n_sprows, st);
+  LAUNCH_CHECK("k_spmv");
+  CUDA_TRY(cudaMemsetAsync(norm_d, 0, sizeof(unsigned long long), st));
+  launch_norm_a(C, sa, h->n_sprows, norm_d, st);
+  LAUNCH_CHECK("k_norm_a");
+  CUDA_TRY(cudaMemsetAsync(flag_d, 0, sizeof(int), st));
+  launch_berr(C, y, yim, ldy, h->n_pad, (const double*)d_X, ldx, h->n, (int)nrhs, norm_d, 0.0, berr_d, flag_d, st);
+  LAUNCH_CHECK("k_berr");
+  h->norm_valid = false;
+  CUDA_TRY(cudaMemcpyAsync(berr, berr_d, (size_t)nrhs * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return DD_OK;
+}
+
+}  // extern "C"

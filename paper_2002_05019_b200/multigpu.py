@@ -381,7 +381,7 @@ class MultiGPUFactor:
         self._tdof = np.concatenate([[0], np.cumsum(P.top_sizes)]).astype(np.int64)
         self._ntd = int(self._tdof[-1])
         trows = torch.from_numpy(np.concatenate([np.arange(self.dof[g], self.dof[g + 1]) for g in P.top])).to(B.device)
-        bT = B.index_select(0, trows) if self.top is not None else None
+        bT = B.index_select(0, trows).t().contiguous().t() if self.top is not None else None
         Bp = {prt: self._local(prt, B) for prt in self.parts}
         xT, Xl = self._dd_solve(Bp, bT)
         for _ in range(refine_steps):
