@@ -314,6 +314,12 @@ int dd_aux_residual(dd_aux_handle_t h, const void* d_factor, const void* d_vals,
 int dd_aux_backward_error(dd_aux_handle_t h, const void* d_factor, const void* d_vals, int64_t nrhs, const void* d_B,
                           int64_t ldb, const void* d_X, int64_t ldx, void* d_work, double* berr, void* stream);
 
+/* Debug check (host only): every access the kernels derive from the handle's descriptor tables
+ * (panels, inverse tiles, W / K1 workspace, Schur-update targets and contributors, solve tiles,
+ * Schur-mode export / scatter items) lies inside its buffer and the arena regions are disjoint.
+ * DD_OK or DD_ERR_INTERNAL with the failed rule in dd_aux_last_error(). */
+int dd_aux_validate(dd_aux_handle_t h);
+
 int dd_aux_destroy(dd_aux_handle_t h);
 
 const char* dd_aux_last_error(void);

@@ -39,7 +39,8 @@ EXPORTED_SYMBOLS = ["dd_aux_default_options", "dd_aux_analyze", "dd_aux_get_info
                     "dd_aux_last_error", "dd_aux_version", "dd_aux_assemble_work_bytes", "dd_aux_assemble",
                     "dd_aux_last_assemble_bytes", "dd_aux_analyze_partial", "dd_aux_schur_cliques",
                     "dd_aux_schur_export", "dd_aux_condense", "dd_aux_recover", "dd_aux_get_struct",
-                    "dd_aux_assemble_acc", "dd_aux_residual", "dd_aux_backward_error"]
+                    "dd_aux_assemble_acc", "dd_aux_residual", "dd_aux_backward_error",
+                    "dd_aux_validate"]
 PHASES = ["load", "k1_diag_bk", "rowperm", "k2_panel", "k3_update", "stats", "perm", "fdiag", "fupd", "dsolve",
           "bupd", "bdiag", "spmv", "linv", "assemble", "schur"]
 
@@ -108,6 +109,7 @@ def _load():
         "dd_aux_schur_cliques": (ctypes.c_int, [P, pi64, pi64, pi32]),
         "dd_aux_get_struct": (ctypes.c_int, [P, pi64, pi32]),
         "dd_aux_residual": (ctypes.c_int, [P, P, P, i64, P, i64, P, i64, P, i64, P, P]),
+        "dd_aux_validate": (ctypes.c_int, [P]),
         "dd_aux_backward_error": (ctypes.c_int, [P, P, P, i64, P, i64, P, i64, P, ctypes.POINTER(ctypes.c_double),
                                                   P]),
         "dd_aux_assemble_acc": (ctypes.c_int, [P, i64, pi64, pi32, P, pi64, i32, pi64, P, P, P]),
@@ -431,6 +433,11 @@ def dd_aux_backward_error(h, d_factor, d_vals, d_B, d_X, d_work, stream=None) ->
                                       _dev_ptr(d_X), int(ldx), _dev_ptr(d_work), _np_ptr(out, ctypes.c_double),
                                       _stream_ptr(stream)))
     return out
+
+
+def dd_aux_validate(h):
+    """Host-side bounds check of every descriptor table (raises DDAuxError naming the rule)."""
+    _check(_lib.dd_aux_validate(h))
 
 
 def dd_aux_destroy(h):

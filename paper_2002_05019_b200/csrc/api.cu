@@ -2109,3 +2109,98 @@ int dd_aux_backward_error(dd_aux_handle_t h, const void* d_factor, const void* d
 }
 
 }  // extern "C"
+
+// ============================================================================ table validation
+// compute-sanitizer is closed on the GPU pool, so every descriptor the kernels index through is
+// checked on the host instead: each access a kernel derives from a table entry must fall inside
+// its buffer (arena, W / K1 workspace, solve rows).  Integer work only; used by the CPU test suite
+// on many random patterns and in Schur mode.
+template <class T>
+static const T* blob_at(dd_aux_handle_t h, size_t off) {
+  return (const T*)(h->blob.data.data() + off);
+}
+
+extern "C" int dd_aux_validate(dd_aux_handle_t h) {
+  if (!h) return fail(-1, "handle is NULL");
+  const int N = h->S.nblk;
+  auto bad = [&](const std::string& m) { return fail(DD_ERR_INTERNAL, "validate: " + m); };
+  // panels, inverse tiles, full inverses: in bounds and disjoint
+  std::vector<std::pair<int64_t, int64_t>> reg;
+  for (int t = 0; t < N; ++t) {
+    const NodeDev& nd = h->nodes[t];
+    if (nd.s <= 0 || nd.sp < nd.s || nd.ld < nd.sp + nd.rp || nd.ld % 8) return bad("panel shape of node " + std::to_string(t));
+    reg.push_back({nd.panel, nd.panel + (int64_t)nd.ld * nd.s});
+    reg.push_back({nd.linv, nd.linv + (int64_t)((nd.s + TB - 1) / TB) * TB * TB});
+    reg.push_back({nd.inv, nd.inv + (int64_t)nd.ldi * nd.s});
+    if (nd.ydof + nd.sp > h->n_pad) return bad("ydof of node " + std::to_string(t));
+    int64_t ro = nd.sp;
+    for (int q = 0; q < nd.nst; ++q) {
+      const int u = h->S.st[t][q];
+      if (u <= t || u >= N) return bad("struct order of node " + std::to_string(t));
+      ro += pad2(h->nodes[u].s);
+    }
+    if (ro != nd.sp + nd.rp) return bad("struct rows of node " + std::to_string(t));
+  }
+  reg.push_back({h->d_off, h->d_off + h->n_pad});
+  reg.push_back({h->e_off, h->e_off + h->n_pad});
+  std::sort(reg.begin(), reg.end());
+  for (size_t q = 0; q < reg.size(); ++q) {
+    if (reg[q].first < 0 || reg[q].second > h->nA) return bad("arena region out of bounds");
+    if (q && reg[q].first < reg[q - 1].second) return bad("arena regions overlap");
+  }
+  // per-level workspace (W, K1 scratch)
+  for (const auto& L : h->S.level_nodes)
+    for (int t : L) {
+      const NodeDev& nd = h->nodes[t];
+      if (nd.w + (int64_t)nd.ldw * nd.s > h->nW || nd.ldw < nd.rp) return bad("W of node " + std::to_string(t));
+      if (nd.k1w + (int64_t)nd.sp * K1NB_MAX > h->nK1) return bad("K1 scratch of node " + std::to_string(t));
+    }
+  // Schur update targets / contributors
+  const UpdTarget* tg = blob_at<UpdTarget>(h, h->off_targets);
+  const UpdContrib* uc = blob_at<UpdContrib>(h, h->off_contribs);
+  const size_t ntg = (h->off_contribs - h->off_targets) / sizeof(UpdTarget);
+  for (const LevelRanges& R : h->lv) {
+    if (R.t1 < R.t0 || (size_t)R.t1 > ntg) return bad("target range");
+    for (int q = R.t0; q < R.t1; ++q) {
+      const UpdTarget& T = tg[q];
+      if (T.j < 0 || T.j >= N) return bad("target panel");
+      const NodeDev& nj = h->nodes[T.j];
+      if (T.N != nj.s || T.ro + T.M > nj.ld || (T.diag && (T.ro != 0 || T.M != T.N))) return bad("target rows");
+      for (int c = T.c0; c < T.c1; ++c) {
+        const NodeDev& nk = h->nodes[uc[c].k];
+        if (uc[c].k < 0 || uc[c].k >= T.j) return bad("contributor not eliminated before its target panel");
+        if (uc[c].arow < 0 || uc[c].arow + T.M > nk.rp) return bad("contributor W rows");
+        if (uc[c].brow < nk.sp || uc[c].brow + T.N > nk.ld) return bad("contributor L rows");
+      }
+    }
+  }
+  // forward-solve targets
+  const SolveTarget* ft = blob_at<SolveTarget>(h, h->off_ftargets);
+  const SolveContrib* fc = blob_at<SolveContrib>(h, h->off_fcontribs);
+  for (const LevelRanges& R : h->lv)
+    for (int q = R.f0; q < R.f1; ++q) {
+      const NodeDev& ni = h->nodes[ft[q].i];
+      if (ft[q].tm * solve_bm(h->cplx) >= ni.s) return bad("forward tile");
+      for (int c = ft[q].c0; c < ft[q].c1; ++c)
+        if (fc[c].ro + ni.s > h->nodes[fc[c].k].ld) return bad("forward contributor rows");
+    }
+  // Schur mode: export items within the arena, gather/scatter rows within the solve vector
+  if (h->n_schur > 0) {
+    const SxItem* it = blob_at<SxItem>(h, h->off_sx_items);
+    const size_t nit = (h->off_sx_tiles - h->off_sx_items) / sizeof(SxItem);
+    for (size_t q = 0; q < nit; ++q) {
+      if (it[q].mode == 3) continue;
+      const int64_t last = it[q].mode == 1 ? it[q].src + (it[q].cols - 1) + (int64_t)(it[q].rows - 1) * it[q].ld
+                                           : it[q].src + (it[q].rows - 1) + (int64_t)(it[q].cols - 1) * it[q].ld;
+      if (it[q].src < 0 || last >= h->nA) return bad("export item out of the arena");
+      if (it[q].dst + (it[q].rows - 1) + (int64_t)(it[q].cols - 1) * it[q].m >= (int64_t)it[q].m * it[q].m)
+        return bad("export item out of its S_g");
+    }
+    const SgItem* ss = blob_at<SgItem>(h, h->off_ss_items);
+    for (int q = 0; q < h->n_ss_items; ++q) {
+      const NodeDev& nd = h->nodes[ss[q].c0];
+      if (ss[q].c0 < h->n_elim || nd.s != ss[q].s || ss[q].aux_row + ss[q].s > h->n_aux_dof) return bad("scatter item");
+    }
+  }
+  return DD_OK;
+}

@@ -198,3 +198,36 @@ def test_schur_mode_host_tables():
     with pytest.raises(dd.DDAuxError):
         dd.dd_aux_analyze_partial(prob.blk_size, prob.colptr, prob.rowidx, tgt + 100, grp, auxs, dd.DD_REAL64, o)
     dd.dd_aux_destroy(h)
+
+
+def test_table_validation_random_patterns():
+    """compute-sanitizer is closed on the GPU pool: instead every descriptor table the kernels index
+    through is bounds-checked on the host (dd_aux_validate) over random block patterns (1-40 DoF
+    blocks, 2-30 blocks, every order), the BASELINE patterns, and Schur-mode handles."""
+    import paper_2002_05019_b200 as dd
+    from dd_inputs.fem import fem_dd, schur_block_problem
+    rng = np.random.default_rng(123)
+    for trial in range(150):
+        nblk = int(rng.integers(2, 31))
+        sizes = rng.integers(1, 41, nblk)
+        dens = rng.uniform(0.05, 1.0)
+        edges = [[u, v] for u in range(nblk) for v in range(u) if rng.random() < dens]
+        cp, ri = dd_inputs.block_pattern_from_cliques(nblk, edges)
+        order = [dd.DD_ORDER_AUTO, dd.DD_ORDER_ND, dd.DD_ORDER_MINDEG, dd.DD_ORDER_NATURAL][trial % 4]
+        h = dd.dd_aux_analyze(sizes, cp, ri, dd.DD_COMPLEX128 if trial % 3 == 0 else dd.DD_REAL64,
+                              dd.dd_aux_default_options(order))
+        dd.dd_aux_validate(h)
+        dd.dd_aux_destroy(h)
+    for name, kw in [("cfg1", {}), ("cfg2", dict(grid=(4, 4, 3))), ("cfg3", {})]:
+        c = dd_inputs.CONFIGS[name]
+        g = kw.get("grid", c["grid"])
+        pairs, bs, cl, cp, ri, vo, tot = dd_inputs._topology(*g, c["sizes"], np.random.default_rng(0), c["topology"])
+        h = dd.dd_aux_analyze(bs, cp, ri, dd.DD_COMPLEX128 if c["complex_"] else dd.DD_REAL64)
+        dd.dd_aux_validate(h)
+        dd.dd_aux_destroy(h)
+    m = fem_dd(3, 2, 2, 8, seed=1)
+    prob, ns, tgt, grp, auxs, info = schur_block_problem(m, leaf=24)
+    h = dd.dd_aux_analyze_partial(prob.blk_size, prob.colptr, prob.rowidx, tgt, grp, auxs, dd.DD_REAL64,
+                                  dd.dd_aux_default_options(dd.DD_ORDER_AUTO))
+    dd.dd_aux_validate(h)
+    dd.dd_aux_destroy(h)
