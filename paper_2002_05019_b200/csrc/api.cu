@@ -1027,7 +1027,9 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
     K2Args k2{maxL_d, (const Tile*)(F + h->off_k2items), (const Strip*)(F + h->off_strips), dnodes, arena, aim, work,
               wim, k1.perm, k1.ipiv, h->d_off, h->e_off};
     K3Args k3{(const UpdTarget*)(F + h->off_targets), (const int64_t*)(F + h->off_tiles), 0, 0,
-              (const UpdContrib*)(F + h->off_contribs), dnodes, arena, aim, work, wim};
+              (const UpdContrib*)(F + h->off_contribs), dnodes, arena, aim, work, wim, 0,
+              (unsigned long long*)(totals_d + 9)};
+    static const bool k3p = getenv("DD_AUX_K3PERSIST") && atoi(getenv("DD_AUX_K3PERSIST"));  // A/B
     const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
     // ---- a2-a5: level-scheduled factorization with a one-level lookahead.
     // Main stream st: K3a(l) [targets in panels of level l+1] -> K3b(l) [the rest].
@@ -1113,7 +1115,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
       const int64_t tiles_a2 = R.tiles_a - R.tiles_a1;
       if (R.tiles_a1 > 0) {
         TraceScope ts(h, DD_PH_K3, (tiles_a2 > 0 || R.tiles_b > 0) ? 0.0 : R.fl_k3, st);
-        launch_k3(C, h->k3cfg, a3, (int)R.tiles_a1, st);
+        launch_k3(C, h->k3cfg, a3, (int)R.tiles_a1, st, k3p);
       }
       LAUNCH_CHECK("k3_update");
       CUDA_TRY(cudaEventRecord(h->evA[l], st));
@@ -1130,7 +1132,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
       h->cur_level = l;
       if (tiles_a2 > 0) {
         TraceScope ts(h, DD_PH_K3, R.tiles_b > 0 ? 0.0 : R.fl_k3, st);
-        launch_k3(C, h->k3cfg, a3, (int)tiles_a2, st);
+        launch_k3(C, h->k3cfg, a3, (int)tiles_a2, st, k3p);
       }
       LAUNCH_CHECK("k3_update");
       CUDA_TRY(cudaEventRecord(h->evA2[l], st));
@@ -1146,7 +1148,7 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
       h->cur_level = l;
       if (R.tiles_b > 0) {
         TraceScope ts(h, DD_PH_K3, R.fl_k3, st);
-        launch_k3(C, h->k3cfg, a3, (int)R.tiles_b, st);
+        launch_k3(C, h->k3cfg, a3, (int)R.tiles_b, st, k3p);
       }
       LAUNCH_CHECK("k3_update");
     }

@@ -1286,14 +1286,14 @@ struct K3Cfg<true, 15> {  // complex 64x32 3M VEC, 5 CTAs per SM
 };
 #endif
 
+// One output tile of the Schur update (the body of both K3 launch forms).
 template <bool C, int CFG>
-__global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_update(K3Args a) {
+__device__ __forceinline__ void k3_tile(const K3Args& a, int64_t blk, double* smem) {
   using Cf = K3Cfg<C, CFG>;
   using G = typename Cf::G;
   constexpr int BM = Cf::BM, BN = Cf::BN;
-  extern __shared__ __align__(16) double smem[];
   // implicit tiles: find this CTA's target (last t with tprefix[t] <= gid) and its (tm, tn)
-  const int64_t gid = a.tile0 + blockIdx.x;
+  const int64_t gid = a.tile0 + blk;
   int lo = 0, hi = a.ntargets - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -1354,6 +1354,29 @@ __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_upd
   G::prefetch_tile_l2(Cb, nj.ld, a.aim, mlim, nlim);
   G::run(segfn, tg.c1 - tg.c0, T.tm * BM, T.tn * BN, tg.M, tg.N, a.wim, a.aim, smem, acc, mask);
   G::template store_tile<1>(acc, smem, Cb, nj.ld, a.aim, mlim, nlim);
+}
+
+template <bool C, int CFG>
+__global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_update(K3Args a) {
+  extern __shared__ __align__(16) double smem[];
+  k3_tile<C, CFG>(a, blockIdx.x, smem);
+}
+
+// Persistent form (A/B, DD_AUX_K3PERSIST=1): one CTA per resident slot, tiles taken from a
+// dynamic counter in launch (cost-descending) order, so no CTA is launched per tile and the
+// largest-K tiles start first (LPT-like load balance across the SMs).
+template <bool C, int CFG>
+__global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_update_persist(K3Args a) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ long long s_tile;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = (long long)atomicAdd(a.counter, 1ull);
+    __syncthreads();
+    const long long t = s_tile;
+    __syncthreads();
+    if (t >= a.ntiles) return;
+    k3_tile<C, CFG>(a, t, smem);
+  }
 }
 
 // ============================================================================ K2 panel TRSM
@@ -1654,20 +1677,43 @@ int k3_bn(bool cplx, int cfg) {
 }
 
 template <bool C, int CFG>
-static void launch_k3_t(const K3Args& a, int ntiles, cudaStream_t st) {
+static void launch_k3_t(const K3Args& a, int ntiles, cudaStream_t st, bool persistent) {
   using Cf = K3Cfg<C, CFG>;
+  if (persistent) {
+    static int slots = 0;
+    if (!slots) {
+      set_smem(k3_update_persist<C, CFG>, Cf::G::SMEM_BYTES);
+      int per = 0, dev = 0, nsm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k3_update_persist<C, CFG>, Cf::NT, Cf::G::SMEM_BYTES);
+      slots = std::max(1, per) * nsm;
+    }
+    K3Args b = a;
+    b.ntiles = ntiles;
+    cudaMemsetAsync(b.counter, 0, sizeof(unsigned long long), st);
+    k3_update_persist<C, CFG><<<std::min(ntiles, slots), Cf::NT, Cf::G::SMEM_BYTES, st>>>(b);
+    return;
+  }
   set_smem(k3_update<C, CFG>, Cf::G::SMEM_BYTES);
   k3_update<C, CFG><<<ntiles, Cf::NT, Cf::G::SMEM_BYTES, st>>>(a);
 }
 
 template <int CFG>
-static void launch_k3_c(bool cplx, const K3Args& a, int ntiles, cudaStream_t st) {
-  if (cplx) launch_k3_t<true, CFG>(a, ntiles, st);
-  else launch_k3_t<false, CFG>(a, ntiles, st);
+static void launch_k3_c(bool cplx, const K3Args& a, int ntiles, cudaStream_t st, bool persistent = false) {
+  if (cplx) launch_k3_t<true, CFG>(a, ntiles, st, persistent);
+  else launch_k3_t<false, CFG>(a, ntiles, st, persistent);
 }
 
-void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st) {
+void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st, bool persistent) {
   if (ntiles == 0) return;
+  persistent = persistent && a.counter != nullptr;
+  if (cfg == 9 || cfg == 10 || cfg == 13) {  // the default-build configurations (persistent-capable)
+    if (cfg == 9) launch_k3_c<9>(cplx, a, ntiles, st, persistent);
+    else if (cfg == 10) launch_k3_c<10>(cplx, a, ntiles, st, persistent);
+    else launch_k3_c<13>(cplx, a, ntiles, st, persistent);
+    return;
+  }
   switch (cfg) {
 #ifdef DD_AUX_AB
     case 0: launch_k3_c<0>(cplx, a, ntiles, st); break;

@@ -72,6 +72,8 @@ struct K3Args {
   int64_t aim;
   const double* work;
   int64_t wim;
+  int64_t ntiles;             // persistent variant: tiles of this launch
+  unsigned long long* counter;  // persistent variant: dynamic tile counter (zeroed before the launch)
 };
 
 struct LinvArgs {      // full inverse of each unit-lower L_tt from its TB x TB tile inverses
@@ -211,7 +213,7 @@ void launch_rowperm(bool cplx, const RowpermArgs& a, int nlist, int max_s, cudaS
 void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, int max_s, cudaStream_t st);
 int k3_bm(bool cplx, int cfg);
 int k3_bn(bool cplx, int cfg);
-void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st);
+void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st, bool persistent = false);
 // totals: [npos, nneg, nzero, n2x2, nswaps, first zero/non-finite pivot (1 + original DoF, in
 // elimination order; 0 = none), nperturbed, nonfinite]
 void launch_k4(const int64_t* node_stats, int nnodes, const int* gperm, int64_t* out, cudaStream_t st);
