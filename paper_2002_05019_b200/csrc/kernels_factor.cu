@@ -96,7 +96,21 @@ __device__ __forceinline__ double modulus(cz v) {
   else return fabs(v.r);
 }
 
+#ifndef DDK_REDUX
+#define DDK_REDUX 0
+#endif
 __device__ __forceinline__ void warp_argmax(double& v, int& i) {
+#if DDK_REDUX
+  // (value desc, index asc) with three warp redux.sync ops: magnitudes are >= 0 (or -1 = no
+  // candidate), so the IEEE bit pattern of a non-negative double orders like its value
+  const bool cand = v >= 0.0;
+  const unsigned hi = cand ? (unsigned)__double2hiint(v) : 0u, lo = cand ? (unsigned)__double2loint(v) : 0u;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  const unsigned mi = __reduce_min_sync(0xffffffffu, (cand && hi == mh && lo == ml) ? (unsigned)i : 0xffffffffu);
+  v = (mh | ml) || mi != 0xffffffffu ? __hiloint2double((int)mh, (int)ml) : -1.0;
+  i = mi == 0xffffffffu ? INT_MAX : (int)mi;
+#else
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     double v2 = __shfl_xor_sync(0xffffffffu, v, o);
@@ -106,6 +120,7 @@ __device__ __forceinline__ void warp_argmax(double& v, int& i) {
       i = i2;
     }
   }
+#endif
 }
 
 // block-wide (max value, smallest index on ties): IDAMAX semantics (reading L3).  One barrier:
@@ -127,6 +142,9 @@ __device__ __forceinline__ void block_argmax(double& v, int& i, double (*shv)[NT
   constexpr int NW = NT1 / 32;
   v = sv[lane % NW];
   i = si[lane % NW];
+#if DDK_REDUX
+  warp_argmax(v, i);
+#else
 #pragma unroll
   for (int o = NW / 2; o; o >>= 1) {
     double v2 = __shfl_xor_sync(0xffffffffu, v, o);
@@ -136,6 +154,7 @@ __device__ __forceinline__ void block_argmax(double& v, int& i, double (*shv)[NT
       i = i2;
     }
   }
+#endif
 }
 
 // Common tail of both K1 variants: TB x TB inverse diagonal tiles of L, the global permutation
