@@ -97,7 +97,7 @@ __device__ __forceinline__ double modulus(cz v) {
 }
 
 #ifndef DDK_REDUX
-#define DDK_REDUX 0
+#define DDK_REDUX 1  // measured: cfg1 K1 30.1 -> 28.5 ms (factor 37.1 -> 35.9 ms) against the shuffle tree
 #endif
 __device__ __forceinline__ void warp_argmax(double& v, int& i) {
 #if DDK_REDUX
@@ -465,10 +465,29 @@ __global__ void __launch_bounds__(NT1) k1_diag_bk(K1Args a) {
       if (kp != kkk) {
         swapped = true;
         __syncthreads();
-        // move the non-updated column kkk of the trailing block to position kp (dlasyf)
-        if (tid == 0) st<C>(A, Ael(kp, kp), aim, ld<C>(A, Ael(kkk, kkk), aim));
-        for (int j = kkk + 1 + tid; j < kp; j += NT1) st<C>(A, Ael(kp, j), aim, ld<C>(A, Ael(j, kkk), aim));
-        for (int j = kp + 1 + tid; j < s; j += NT1) st<C>(A, Ael(j, kp), aim, ld<C>(A, Ael(j, kkk), aim));
+        // move the non-updated column kkk of the trailing block to position kp (dlasyf).  The column
+        // is already in registers (Ak = column k, the prefetched An = column k+1), so each row owner
+        // stores its own element: no global round trip on the interchange path
+        if constexpr (PF) {
+          if (pf || kstep == 1) {
+#pragma unroll
+            for (int q = 0; q < K1_MAXQ; ++q) {
+              const int i = tid + q * NT1;
+              const cz cv = kstep == 1 ? Ak[q] : An[PF ? q : 0];
+              if (i == kkk) st<C>(A, Ael(kp, kp), aim, cv);
+              else if (i > kkk && i < kp) st<C>(A, Ael(kp, i), aim, cv);
+              else if (i > kp && i < s) st<C>(A, Ael(i, kp), aim, cv);
+            }
+          } else {
+            if (tid == 0) st<C>(A, Ael(kp, kp), aim, ld<C>(A, Ael(kkk, kkk), aim));
+            for (int j = kkk + 1 + tid; j < kp; j += NT1) st<C>(A, Ael(kp, j), aim, ld<C>(A, Ael(j, kkk), aim));
+            for (int j = kp + 1 + tid; j < s; j += NT1) st<C>(A, Ael(j, kp), aim, ld<C>(A, Ael(j, kkk), aim));
+          }
+        } else {
+          if (tid == 0) st<C>(A, Ael(kp, kp), aim, ld<C>(A, Ael(kkk, kkk), aim));
+          for (int j = kkk + 1 + tid; j < kp; j += NT1) st<C>(A, Ael(kp, j), aim, ld<C>(A, Ael(j, kkk), aim));
+          for (int j = kp + 1 + tid; j < s; j += NT1) st<C>(A, Ael(j, kp), aim, ld<C>(A, Ael(j, kkk), aim));
+        }
         // rows kkk, kp of the panel's L columns (shared copy) -- earlier panels: deferred
         for (int m = tid; m < kk; m += NT1) {
           double t0 = Lpr[LP(kkk, m)];
