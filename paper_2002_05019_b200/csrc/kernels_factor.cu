@@ -1323,6 +1323,38 @@ struct K3Cfg<true, 15> {  // complex 64x32 3M VEC, 5 CTAs per SM
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 5;
 };
 #endif
+#ifdef DD_AUX_AB
+template <>
+struct K3Cfg<false, 16> {  // real 64x64, BK = 32, 2 stages, RECT (3 CTAs/SM): half the stage barriers per flop
+  using G = Gemm<64, 64, 32, 2, 2, 2, false, false, false, false, false, false, true>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 3;
+};
+template <>
+struct K3Cfg<true, 16> {
+  using G = Gemm<64, 32, 32, 2, 2, 2, true, false, false, true, false, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 3;
+};
+template <>
+struct K3Cfg<false, 17> {  // real 128x64, 4 warps of 64x32 (16 DMMAs per 12 fragment loads), 3 stages, RECT
+  using G = Gemm<128, 64, 16, 2, 2, 3, false, false, false, false, false, false, true>;
+  static constexpr int NT = 128, BM = 128, BN = 64, MINB = 2;
+};
+template <>
+struct K3Cfg<true, 17> {
+  using G = Gemm<64, 64, 16, 2, 2, 2, true, false, false, true, false, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 2;
+};
+template <>
+struct K3Cfg<false, 18> {  // real 64x128 (warps 2x2 of 32x64), 3 stages, RECT
+  using G = Gemm<64, 128, 16, 2, 2, 3, false, false, false, false, false, false, true>;
+  static constexpr int NT = 128, BM = 64, BN = 128, MINB = 2;
+};
+template <>
+struct K3Cfg<true, 18> {
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, true, true>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
+};
+#endif
 
 // One output tile of the Schur update (the body of both K3 launch forms).
 template <bool C, int CFG>
@@ -1665,6 +1697,9 @@ int k3_bm(bool cplx, int cfg) {
 #endif
 #ifdef DD_AUX_AB
     case 15: return bm_of<15>(cplx);
+    case 16: return bm_of<16>(cplx);
+    case 17: return bm_of<17>(cplx);
+    case 18: return bm_of<18>(cplx);
 #endif
     default: return bm_of<13>(cplx);
   }
@@ -1709,6 +1744,9 @@ int k3_bn(bool cplx, int cfg) {
 #endif
 #ifdef DD_AUX_AB
     case 15: return bn_of<15>(cplx);
+    case 16: return bn_of<16>(cplx);
+    case 17: return bn_of<17>(cplx);
+    case 18: return bn_of<18>(cplx);
 #endif
     default: return bn_of<13>(cplx);
   }
@@ -1791,6 +1829,9 @@ void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st,
 #endif
 #ifdef DD_AUX_AB
     case 15: launch_k3_c<15>(cplx, a, ntiles, st); break;
+    case 16: launch_k3_c<16>(cplx, a, ntiles, st); break;
+    case 17: launch_k3_c<17>(cplx, a, ntiles, st); break;
+    case 18: launch_k3_c<18>(cplx, a, ntiles, st); break;
 #endif
     default: launch_k3_c<13>(cplx, a, ntiles, st); break;
   }
@@ -1829,6 +1870,11 @@ void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, int
 #endif
 #ifdef DD_AUX_AB
       case 1: cplx ? launch_k2_t<true, 1>(a, nitems, max_s, st) : launch_k2_t<false, 1>(a, nitems, max_s, st); break;
+#endif
+#ifdef DD_AUX_AB
+      case 16: cplx ? launch_k2_t<true, 16>(a, nitems, max_s, st) : launch_k2_t<false, 16>(a, nitems, max_s, st); break;
+      case 17: cplx ? launch_k2_t<true, 17>(a, nitems, max_s, st) : launch_k2_t<false, 17>(a, nitems, max_s, st); break;
+      case 18: cplx ? launch_k2_t<true, 18>(a, nitems, max_s, st) : launch_k2_t<false, 18>(a, nitems, max_s, st); break;
 #endif
       default: cplx ? launch_k2_t<true, 13>(a, nitems, max_s, st) : launch_k2_t<false, 13>(a, nitems, max_s, st); break;
     }

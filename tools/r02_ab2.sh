@@ -1,0 +1,7 @@
+#!/bin/bash
+# round 2 A/B: K3 tile shapes on cfg2 (AB build), default config 13 on the same box
+A="--config cfg2 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+DD_AUX_DEFS="DD_AUX_AB" python dd_build.py > /dev/null
+for c in 13 16 17 18; do DD_AUX_K3CFG=$c timeout 900 python bench.py $A > gpurun_out/ab2_cfg2_k$c.log 2>&1; done
+DD_AUX_K3CFG=17 timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "scaled or corpus" > gpurun_out/ab2_parity_k17.log 2>&1; echo rc=$? >> gpurun_out/ab2_parity_k17.log
+python dd_build.py > /dev/null
