@@ -290,15 +290,23 @@ class MultiGPUFactor:
         import torch
         P = self.plan
         exports = {}
+        self.timings = {"parts_ms": {}, "export_bytes": {}}
+        ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
         for prt, ss in self.parts.items():
             pp = P.parts[prt]
             pv = gather_values(d_vals, val_offset, self.bs, self.colptr, self.rowidx, pp.src, pp.val_offset,
                                pp.blk_size, pp.colptr, pp.rowidx, pp.nvals)
+            e0, e1 = ev(), ev()
+            e0.record()
             rc, _ = ss.factor(pv, pp.val_offset)
             if rc != DD_OK:
                 raise RuntimeError(f"part {prt}: partial factorization rc={rc}")
             ss._pv = pv
             dS, Soff = ss.export()
+            e1.record()
+            torch.cuda.synchronize()
+            self.timings["parts_ms"][prt] = e0.elapsed_time(e1)
+            self.timings["export_bytes"][prt] = dS.numel() * dS.element_size()
             exports[prt] = (dS, Soff, ss.cliques())
         if self.dist is not None:       # NCCL point-to-point: every rank's S buffer to rank 0
             if self.rank != 0:
@@ -320,6 +328,8 @@ class MultiGPUFactor:
         tv = gather_values(d_vals, val_offset, self.bs, self.colptr, self.rowidx, P.top_src, P.top_val_offset,
                            P.top_sizes, P.top_colptr, P.top_rowidx, P.top_nvals)
         self._tv_orig = tv.clone()  # the top blocks' own values (global refinement residual)
+        e0, e1 = ev(), ev()
+        e0.record()
         for prt in sorted(exports):
             dS, Soff, cl = exports[prt]
             if not cl:
@@ -331,6 +341,9 @@ class MultiGPUFactor:
             torch.cuda.synchronize()
         self._tv = tv
         rc, fi = self.top.factor(tv, P.top_val_offset)
+        e1.record()
+        torch.cuda.synchronize()
+        self.timings["top_ms"] = e0.elapsed_time(e1)  # assemble_acc of every part's S + top factor
         return rc
 
     # -------------------------------------------------------------------------------- solve
