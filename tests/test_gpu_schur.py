@@ -130,3 +130,69 @@ def test_full_dd_pipeline_on_gpu(cplx, grid, a, leaf):
     assert berr.max() <= 1e-12, berr.max()
     aux.close()
     ss.close()
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_schur_mode_random_patterns_one_group(cplx, seed):
+    """Schur mode on random block-sparse matrices (sizes 1-40, kept blocks of different sizes, kept
+    blocks coupled to each other and to everything): with ONE group the export is the whole Schur
+    complement onto the kept blocks, D_kk - D_ke D_ee^{-1} D_ek (the plain definition, numpy)."""
+    import torch
+    import paper_2002_05019_b200 as dd
+    from dd_inputs import Problem, block_pattern_from_cliques, dense_expand
+    rng = np.random.default_rng(100 + seed + 10 * cplx)
+    nblk = int(rng.integers(5, 12))
+    ns = int(rng.integers(1, 4))
+    sizes = rng.integers(1, 41, nblk)
+    edges = [[u, v] for u in range(nblk) for v in range(u) if rng.random() < 0.5]
+    colptr, rowidx = block_pattern_from_cliques(nblk, edges)
+    off, tot = [], 0
+    for j in range(nblk):
+        for q in range(colptr[j], colptr[j + 1]):
+            off.append(tot)
+            tot += int(sizes[rowidx[q]]) * int(sizes[j])
+    vals = rng.standard_normal(tot) + (1j * rng.standard_normal(tot) if cplx else 0)
+    p = Problem(np.asarray(sizes, dtype=np.int64), colptr, rowidx, vals, np.asarray(off, dtype=np.int64), [])
+    tgt = np.arange(ns, dtype=np.int32)
+    grp = np.zeros(ns, dtype=np.int32)
+    auxs = np.asarray(sizes[nblk - ns:], dtype=np.int64)
+    ss = dd.SchurSolver(p.blk_size, p.colptr, p.rowidx, tgt, grp, auxs, complex_=cplx, order=dd.DD_ORDER_AUTO)
+    ss._auxs = auxs
+    rc, _ = ss.factor(torch.from_numpy(p.values).cuda(), p.val_offset)
+    assert rc == dd.DD_OK
+    dd.dd_aux_validate(ss.h)
+    dS, Soff = ss.export()
+    torch.cuda.synchronize()
+    m = int(auxs.sum())
+    S = dS.cpu().numpy()[:m * m].reshape(m, m).T
+    D = dense_expand(p)
+    ne = int(sizes[:nblk - ns].sum())
+    Sref = D[ne:, ne:] - D[ne:, :ne] @ np.linalg.solve(D[:ne, :ne], D[:ne, ne:])
+    # forward error of a Schur complement ~ u * cond(D_ee) * |D|: allow 1e-12 * cond * max|D| (~4500 u)
+    assert np.abs(S - Sref).max() <= 1e-12 * np.linalg.cond(D[:ne, :ne]) * np.abs(D).max()
+
+
+def test_residual_and_backward_error_apis():
+    """dd_aux_residual / dd_aux_backward_error against the oracle's block matvec and berr."""
+    import torch
+    import paper_2002_05019_b200 as dd
+    from dd_inputs import random_rhs
+    from oracle.block_ldlt import matvec_blocks, residual_berr
+    for name, grid, sz in (("cfg1", (2, 2, 2), 50), ("cfg3", (2, 2, 2), 30)):
+        p = dd_inputs.config(name, grid=grid, sizes=sz)
+        s = dd.AuxSolver(p.blk_size, p.colptr, p.rowidx, complex_=p.is_complex)
+        vals = torch.from_numpy(p.values).cuda()
+        s.factor(vals, p.val_offset)
+        B = random_rhs(p.n, 5, p.is_complex, 1)
+        X = random_rhs(p.n, 5, p.is_complex, 2)
+        Bd, Xd = to_dev_colmajor(B, torch), to_dev_colmajor(X, torch)
+        R = torch.empty_like(Bd.t().contiguous()).t()
+        w = s._work(dd.dd_aux_solve_work_bytes(s.h, 5))
+        dd.dd_aux_residual(s.h, s.factor_buf, vals, Bd, Xd, R, w)
+        torch.cuda.synchronize()
+        Rref = B - matvec_blocks(p, X)
+        assert np.abs(R.cpu().numpy() - Rref).max() <= 1e-12 * np.abs(Rref).max()
+        be = dd.dd_aux_backward_error(s.h, s.factor_buf, vals, Bd, Xd, w)
+        np.testing.assert_allclose(be, residual_berr(p, X, B), rtol=1e-10)
+        s.close()
