@@ -548,7 +548,8 @@ def fem_arm(args, rank, world, local, dist):
     nrhs = args.nrhs or fc["nrhs"]
     t0 = time.time()
     m = fem_dd(*fc["grid"], fc["a"], complex_=fc["complex_"], seed=args.seed + rank, nrhs=nrhs)
-    prob, ns, tgt, grp, auxs, info = schur_block_problem(m, leaf=fc["leaf"])
+    leaf = int(os.environ.get("DD_FEM_LEAF", fc["leaf"]))  # supernode (ND leaf) size: the ordering input
+    prob, ns, tgt, grp, auxs, info = schur_block_problem(m, leaf=leaf)
     gen_s = time.time() - t0
     cplx = fc["complex_"]
     tdt = torch.complex128 if cplx else torch.float64
@@ -688,7 +689,7 @@ def fem_arm(args, rank, world, local, dist):
         "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128" if cplx else "f64", "data": "synthetic",
         "config": {"workload": fc["txt"], "n_arrowhead": int(A.shape[0]), "n_sub_handle": prob.n,
-                   "nblk": prob.nblk, "n_schur": ns, "leaf": fc["leaf"], "nrhs": nrhs,
+                   "nblk": prob.nblk, "n_schur": ns, "leaf": leaf, "nrhs": nrhs,
                    "levels": ss.info["n_levels"], "aux_n": m.n_dual},
         "f3_ms": f3_ms, "f3_tflops": fl3 / (f3_ms * 1e-3) / 1e12, "f3_frac_of_fp64_peak": fl3 / (f3_ms * 1e-3) / 1e12 / peak_tf,
         "f1_plus_aux_factor_ms": aux_ms, "condense_plus_aux_solve_ms": cond_ms, "f2_recover_ms": rec_ms,

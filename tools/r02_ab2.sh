@@ -5,3 +5,5 @@ DD_AUX_DEFS="DD_AUX_AB" python dd_build.py > /dev/null
 for c in 13 16 17 18; do DD_AUX_K3CFG=$c timeout 900 python bench.py $A > gpurun_out/ab2_cfg2_k$c.log 2>&1; done
 DD_AUX_K3CFG=17 timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "scaled or corpus" > gpurun_out/ab2_parity_k17.log 2>&1; echo rc=$? >> gpurun_out/ab2_parity_k17.log
 python dd_build.py > /dev/null
+# f3 supernode (ND leaf) size A/B on fem1
+for L in 64 256 512; do DD_FEM_LEAF=$L timeout 600 python bench.py --config fem1 --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/ab2_fem1_leaf$L.log 2>&1; done
