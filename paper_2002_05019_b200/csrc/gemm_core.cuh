@@ -343,7 +343,10 @@ struct Gemm {
     const int g = lane >> 2, tg = lane & 3;
 #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
-      if (ks > 0 && ks >= nks) break;  // warp-uniform
+#ifndef DDK_KSTEP_BREAK
+#define DDK_KSTEP_BREAK 1
+#endif
+      if (DDK_KSTEP_BREAK && ks > 0 && ks >= nks) break;  // warp-uniform
       const int k = ks * 4 + tg;
       double ar[MI][2], br[NI];
       double ai[CPLX ? MI : 1][2], bi[CPLX ? NI : 1];

@@ -1432,6 +1432,7 @@ __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_upd
   k3_tile<C, CFG>(a, blockIdx.x, smem);
 }
 
+#ifdef DD_AUX_AB
 // Persistent form (A/B, DD_AUX_K3PERSIST=1): one CTA per resident slot, tiles taken from a
 // dynamic counter in launch (cost-descending) order, so no CTA is launched per tile and the
 // largest-K tiles start first (LPT-like load balance across the SMs).
@@ -1448,6 +1449,7 @@ __global__ void __launch_bounds__(K3Cfg<C, CFG>::NT, K3Cfg<C, CFG>::MINB) k3_upd
     k3_tile<C, CFG>(a, t, smem);
   }
 }
+#endif  // DD_AUX_AB
 
 // ============================================================================ K2 panel TRSM
 // W_t = (A_struct,t P_t^T) L_tt^{-T} as ONE tiled DMMA GEMM per level using the full inverse
@@ -1755,6 +1757,7 @@ int k3_bn(bool cplx, int cfg) {
 template <bool C, int CFG>
 static void launch_k3_t(const K3Args& a, int ntiles, cudaStream_t st, bool persistent) {
   using Cf = K3Cfg<C, CFG>;
+#ifdef DD_AUX_AB
   if (persistent) {
     static int slots = 0;
     if (!slots) {
@@ -1771,6 +1774,9 @@ static void launch_k3_t(const K3Args& a, int ntiles, cudaStream_t st, bool persi
     k3_update_persist<C, CFG><<<std::min(ntiles, slots), Cf::NT, Cf::G::SMEM_BYTES, st>>>(b);
     return;
   }
+#else
+  (void)persistent;  // measured slower: A/B builds only
+#endif
   set_smem(k3_update<C, CFG>, Cf::G::SMEM_BYTES);
   k3_update<C, CFG><<<ntiles, Cf::NT, Cf::G::SMEM_BYTES, st>>>(a);
 }

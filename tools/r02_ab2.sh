@@ -7,3 +7,10 @@ DD_AUX_K3CFG=17 timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "
 python dd_build.py > /dev/null
 # f3 supernode (ND leaf) size A/B on fem1
 for L in 64 256 512; do DD_FEM_LEAF=$L timeout 600 python bench.py --config fem1 --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/ab2_fem1_leaf$L.log 2>&1; done
+# K3 engine: no per-k-step early exit (lets the compiler software-pipeline fragment loads across k-steps)
+A="--steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+DD_AUX_DEFS="DDK_KSTEP_BREAK=0" python dd_build.py > /dev/null
+timeout 900 python bench.py --config cfg2 $A > gpurun_out/ab2_cfg2_nobreak.log 2>&1
+timeout 900 python bench.py --config cfg3 $A > gpurun_out/ab2_cfg3_nobreak.log 2>&1
+python dd_build.py > /dev/null
+timeout 900 python bench.py --config cfg3 $A > gpurun_out/ab2_cfg3_base.log 2>&1
