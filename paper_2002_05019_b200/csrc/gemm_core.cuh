@@ -341,15 +341,18 @@ struct Gemm {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = warp % WARPS_M, wn = warp / WARPS_M;
     const int g = lane >> 2, tg = lane & 3;
-#pragma unroll
-    for (int ks = 0; ks < BK / 4; ++ks) {
-#ifndef DDK_KSTEP_BREAK
-#define DDK_KSTEP_BREAK 1
-#endif
-      if (DDK_KSTEP_BREAK && ks > 0 && ks >= nks) break;  // warp-uniform
-      const int k = ks * 4 + tg;
+    struct Frag {
       double ar[MI][2], br[NI];
       double ai[CPLX ? MI : 1][2], bi[CPLX ? NI : 1];
+    };
+    auto load = [&](int ks, Frag& f) {
+      const int k = ks * 4 + tg;
+      auto& ar = f.ar;
+      auto& br = f.br;
+      auto& ai = f.ai;
+      auto& bi = f.bi;
+      (void)ai;
+      (void)bi;
       if constexpr (VEC) {
 #pragma unroll
         for (int a = 0; a < NA; ++a) {
@@ -396,6 +399,14 @@ struct Gemm {
           if constexpr (CPLX) bi[b] = Bs[B_TILE + o];
         }
       }
+    };
+    auto issue = [&](Frag& f) {
+      auto& ar = f.ar;
+      auto& br = f.br;
+      auto& ai = f.ai;
+      auto& bi = f.bi;
+      (void)ai;
+      (void)bi;
       // Issue order: every product class over all (a, b) before the next class, so two
       // DMMAs into the same accumulator are MI*NI instructions apart (no dependency stall).
       if constexpr (C3M) {
@@ -452,6 +463,32 @@ struct Gemm {
             if ((mask >> (a * NI + b)) & 1u) dmma16x8x4(acc.i[a][b], ai[a][0], ai[a][1], br[b]);
       }
       }  // 4M / real
+    };
+#ifndef DDK_KSTEP_BREAK
+#define DDK_KSTEP_BREAK 1
+#endif
+#ifndef DDK_FRAG_DB
+#define DDK_FRAG_DB 0
+#endif
+    if constexpr (DDK_FRAG_DB != 0) {
+      // register double-buffered fragments: the loads of k-step ks+1 are issued before the DMMAs
+      // of k-step ks (the k-tail skip is kept: an empty k-step loads and issues nothing)
+      Frag fr[2];
+      load(0, fr[0]);
+#pragma unroll
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        if (ks > 0 && ks >= nks) break;  // warp-uniform
+        if (ks + 1 < BK / 4 && ks + 1 < nks) load(ks + 1, fr[(ks + 1) & 1]);
+        issue(fr[ks & 1]);
+      }
+    } else {
+#pragma unroll
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        if (DDK_KSTEP_BREAK && ks > 0 && ks >= nks) break;  // warp-uniform
+        Frag f;
+        load(ks, f);
+        issue(f);
+      }
     }
   }
 
