@@ -231,3 +231,24 @@ def test_table_validation_random_patterns():
                                   dd.dd_aux_default_options(dd.DD_ORDER_AUTO))
     dd.dd_aux_validate(h)
     dd.dd_aux_destroy(h)
+
+
+def test_schur_mode_argument_errors():
+    """dd_aux_analyze_partial rejects bad Schur descriptions (LAPACK-style argument codes)."""
+    import paper_2002_05019_b200 as dd
+    sizes = np.array([3, 4, 5, 6], dtype=np.int64)
+    cp, ri = dd_inputs.block_pattern_from_cliques(4, [[0, 1, 2, 3]])
+    o = dd.dd_aux_default_options(dd.DD_ORDER_NATURAL)
+    ok = dict(schur_target=[0, 1], schur_group=[0, 0], aux_blk_size=[5, 6])
+    h = dd.dd_aux_analyze_partial(sizes, cp, ri, **ok, opt=o)
+    assert dd.dd_aux_get_info(h)["n_schur"] == 2
+    dd.dd_aux_validate(h)
+    dd.dd_aux_destroy(h)
+    bad = [dict(schur_target=[], schur_group=[], aux_blk_size=[5]),                  # n_schur = 0
+           dict(schur_target=[0, 1, 2, 3], schur_group=[0] * 4, aux_blk_size=sizes),  # n_schur = nblk
+           dict(schur_target=[0, 0], schur_group=[0, 0], aux_blk_size=[5]),           # same target twice in a group
+           dict(schur_target=[0, 1], schur_group=[0, -1], aux_blk_size=[5, 6]),       # negative group
+           dict(schur_target=[1, 0], schur_group=[0, 1], aux_blk_size=[5, 6])]        # size mismatch
+    for kw in bad:
+        with pytest.raises(dd.DDAuxError):
+            dd.dd_aux_analyze_partial(sizes, cp, ri, **kw, opt=o)
