@@ -871,6 +871,7 @@ int dd_aux_solve_work_bytes(dd_aux_handle_t h, int64_t nrhs, size_t* bytes) {
   w += align256((size_t)nrhs * sizeof(double)) + 256;                    // per-column berr + flag
   w += align256(bupd_part_bytes(h->cplx, (int)nrhs));                    // backward split-K partials
   w += align256((size_t)pad8(std::max<int64_t>(h->nT, 2)) * nrhs * planes * sizeof(double));  // level buffer T
+  w += align256(bupd_cnt_bytes(h->cplx, (int)nrhs));                                            // split-K counters
   *bytes = w;
   return DD_OK;
 }
@@ -1216,7 +1217,8 @@ enum { SW_FWD = 1, SW_D = 2, SW_BWD = 4, SW_ALL = 7 };
 // a Schur-mode handle's levels hold only its eliminated positions (kept rows are read / written
 // by the update kernels as struct rows, never solved)
 static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t yim, int64_t ldy, int nrhs,
-                       cudaStream_t st, double* part, double* T, const int* flag = nullptr, int phases = SW_ALL) {
+                       cudaStream_t st, double* part, double* T, const int* flag = nullptr, int phases = SW_ALL,
+                       int* cnt = nullptr) {
   // with a device flag the sweep may be skipped: its flops are not counted (conservative trace)
   const double fs = flag ? 0.0 : 1.0;
   const bool C = h->cplx;
@@ -1240,6 +1242,7 @@ static int solve_sweep(dd_aux_handle_t h, const uint8_t* F, double* y, int64_t y
   a.flag = flag;
   a.dtiles = (const DTile*)(F + h->off_dtiles);
   a.T = T;
+  a.cnt = cnt;
   a.ldT = pad8(std::max<int64_t>(h->nT, 2));
   a.Tim = C ? a.ldT * nrhs : 0;
   const int* lvlnodes = (const int*)(F + h->off_lvlnodes);
@@ -1350,7 +1353,11 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
     int* flag_d = (int*)((uint8_t*)berr_d + align256((size_t)nrhs * sizeof(double)));
     double* part = (double*)((uint8_t*)flag_d + 256);
     double* Tbuf = (double*)((uint8_t*)part + align256(bupd_part_bytes(C, (int)nrhs)));
-    int rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf);
+    int* cnt = (int*)((uint8_t*)Tbuf + align256((size_t)pad8(std::max<int64_t>(h->nT, 2)) * nrhs * planes * sizeof(double)));
+    static const bool fold = !(getenv("DD_AUX_BUPD_FOLD") && atoi(getenv("DD_AUX_BUPD_FOLD")) == 0);  // A/B
+    if (fold) CUDA_TRY(cudaMemsetAsync(cnt, 0, bupd_cnt_bytes(C, (int)nrhs), st));
+    else cnt = nullptr;
+    int rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf, nullptr, SW_ALL, cnt);
     if (rc) return rc;
     pa.dst = (double*)d_B;
     pa.ldd = ldb;
@@ -1396,7 +1403,7 @@ int dd_aux_solve(dd_aux_handle_t h, const void* d_factor, const void* d_vals, in
         LAUNCH_CHECK("k_berr");
         flag = flag_d;
       }
-      rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf, flag);
+      rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf, flag, SW_ALL, cnt);
       if (rc) return rc;
       pa.accumulate = 1;
       pa.flag = flag;
@@ -1883,6 +1890,8 @@ static int schur_sweep(dd_aux_handle_t h, int mode, const void* d_factor, int64_
   int* flag_d = (int*)((uint8_t*)berr_d + align256((size_t)nrhs * sizeof(double)));
   double* part = (double*)((uint8_t*)flag_d + 256);
   double* Tbuf = (double*)((uint8_t*)part + align256(bupd_part_bytes(C, (int)nrhs)));
+  int* cnt = (int*)((uint8_t*)Tbuf + align256((size_t)pad8(std::max<int64_t>(h->nT, 2)) * nrhs * planes * sizeof(double)));
+  CUDA_TRY(cudaMemsetAsync(cnt, 0, bupd_cnt_bytes(C, (int)nrhs), st));
   PermArgs pa{};
   pa.gperm = (const int*)(F + h->off_gperm);
   pa.nrows = h->n_pad;
@@ -1927,7 +1936,7 @@ static int schur_sweep(dd_aux_handle_t h, int mode, const void* d_factor, int64_
     launch_schur_scatter(C, sv, h->n_ss_items, st);
   }
   LAUNCH_CHECK("k_schur_scatter");
-  rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf, nullptr, SW_BWD);
+  rc = solve_sweep(h, F, y, yim, ldy, (int)nrhs, st, part, Tbuf, nullptr, SW_BWD, cnt);
   if (rc) return rc;
   pa.dst = (double*)d_X;
   pa.ldd = ldx;

@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(128) k_fupd(SolveArgs a) {
 // CL (thread-block cluster of the G chunk CTAs of one tile, G <= 8): the partial tiles are reduced
 // through distributed shared memory in the same fixed order g = 0..G-1 (bitwise the same result
 // as the two-kernel partial-buffer path, without its HBM round trip and second launch).
-template <bool C, bool M3, bool CL>
+template <bool C, bool M3, bool CL, bool FOLD = false>
 __global__ void __launch_bounds__(128) k_bupd(SolveArgs a, int G, double* part, int64_t pim) {
   if (a.flag && *a.flag == 0) return;
   using G_ = typename SolveG<C, M3>::BU;
@@ -246,6 +246,33 @@ __global__ void __launch_bounds__(128) k_bupd(SolveArgs a, int G, double* part, 
         if (C) P[e + pim] = vi;
       }
     });
+    if constexpr (FOLD) {
+      // the last of the G chunk CTAs of this (tile, rhs tile) to finish reduces the partials in the
+      // fixed order g = 0..G-1 (bitwise the sums of k_bupd_reduce, without its second launch)
+      __shared__ int s_last;
+      __threadfence();
+      __syncthreads();
+      int* cnt = a.cnt + (int64_t)tile * gridDim.y + blockIdx.y;
+      if (threadIdx.x == 0) s_last = atomicAdd(cnt, 1) == G - 1;
+      __syncthreads();
+      if (!s_last) return;
+      __threadfence();
+      for (int e = threadIdx.x; e < SUBM * SBN; e += blockDim.x) {
+        const int r = e % SUBM, c = e / SUBM;
+        if (m0 + r >= nt.s || n0 + c >= a.nrhs) continue;
+        const int64_t pe = (int64_t)r + (int64_t)(n0 + c) * SUBM;
+        double sr = 0.0, si = 0.0;
+        for (int h = 0; h < G; ++h) {
+          const double* Q = part + (int64_t)(tile * G + h) * SUBM * a.nrhs;
+          sr += __ldcg(Q + pe);
+          if (C) si += __ldcg(Q + pe + pim);
+        }
+        const int64_t o = nt.ydof + (int64_t)(m0 + r) + (int64_t)(n0 + c) * a.ldy;
+        a.y[o] -= sr;
+        if (C) a.y[o + a.yim] -= si;
+      }
+      if (threadIdx.x == 0) *cnt = 0;  // ready for the next launch
+    }
   }
 }
 
@@ -613,6 +640,10 @@ static void set_smem(K kern, size_t bytes) {
 
 int solve_bm(bool) { return SUBM; }
 size_t bupd_part_bytes(bool cplx, int nrhs) { return (size_t)BUPD_MAX_PARTS * SUBM * nrhs * (cplx ? 2 : 1) * 8; }
+size_t bupd_cnt_bytes(bool cplx, int nrhs) {  // one arrival counter per (split tile, rhs tile)
+  (void)cplx;
+  return (size_t)BUPD_MAX_PARTS * ((nrhs + SolveN<true>::value - 1) / SolveN<true>::value) * sizeof(int);
+}
 int spmv_bm() { return SPM; }
 
 static dim3 rows_grid(int64_t nrows, int nrhs) {
@@ -714,6 +745,11 @@ static void bupd_t(const SolveArgs& a, int ntiles, int G, double* part, int64_t 
 #else
   (void)cluster;
 #endif
+  if (G > 1 && a.cnt) {  // split-K with the in-kernel (last-arriver) reduction
+    set_smem(k_bupd<C, M3, false, true>, GB::SMEM_BYTES);
+    k_bupd<C, M3, false, true><<<grid, 128, GB::SMEM_BYTES, st>>>(a, G, part, pim);
+    return;
+  }
   set_smem(k_bupd<C, M3, false>, GB::SMEM_BYTES);
   k_bupd<C, M3, false><<<grid, 128, GB::SMEM_BYTES, st>>>(a, G, part, pim);
 }
@@ -735,7 +771,7 @@ void launch_bupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, int max_rp,
   if (!cplx) bupd_t<false, false>(a, ntiles, G, part, pim, cluster, st);
   else if (m3) bupd_t<true, true>(a, ntiles, G, part, pim, cluster, st);
   else bupd_t<true, false>(a, ntiles, G, part, pim, cluster, st);
-  if (G > 1 && !cluster) {
+  if (G > 1 && !cluster && !a.cnt) {
     dim3 g2(ntiles, std::min(64, (SUBM * a.nrhs + 255) / 256));
     if (cplx) k_bupd_reduce<true><<<g2, 256, 0, st>>>(a, G, part, pim);
     else k_bupd_reduce<false><<<g2, 256, 0, st>>>(a, G, part, pim);

@@ -103,6 +103,7 @@ struct SolveArgs {
   const DTile* dtiles;          // diagonal-solve tiles of the level (node, 64-row tile, T offset)
   double* T;                    // level buffer for the diagonal solves (planar), ld ldT
   int64_t Tim, ldT;
+  int* cnt;                     // backward split-K arrival counters (zero between launches), or null
 };
 
 struct PermArgs {
@@ -231,6 +232,7 @@ void launch_dsolve(bool cplx, const SolveArgs& a, cudaStream_t st);
 // max_rp: largest padded struct-row count of the level's nodes (bounds the split-K factor)
 void launch_bupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, int max_rp, double* part, cudaStream_t st);
 size_t bupd_part_bytes(bool cplx, int nrhs);
+size_t bupd_cnt_bytes(bool cplx, int nrhs);
 int spmv_bm();
 // ||A||_inf of the caller's original blocks (max row sum of moduli) -> *out (bits of a double)
 void launch_norm_a(bool cplx, const SpmvArgs& a, int nrow_tiles, unsigned long long* out, cudaStream_t st);

@@ -14,3 +14,9 @@ timeout 900 python bench.py --config cfg2 $A > gpurun_out/ab2_cfg2_nobreak.log 2
 timeout 900 python bench.py --config cfg3 $A > gpurun_out/ab2_cfg3_nobreak.log 2>&1
 python dd_build.py > /dev/null
 timeout 900 python bench.py --config cfg3 $A > gpurun_out/ab2_cfg3_base.log 2>&1
+# solve: backward split-K reduction folded into k_bupd (default) vs the separate reduce kernel
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "multi_rhs or scaled or graphs or padded" > gpurun_out/ab2_fold_tests.log 2>&1; echo rc=$? >> gpurun_out/ab2_fold_tests.log
+A="--steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+DD_AUX_BUPD_FOLD=0 timeout 900 python bench.py --config cfg3 $A > gpurun_out/ab2_cfg3_nofold.log 2>&1
+DD_AUX_BUPD_FOLD=0 timeout 900 python bench.py --config cfg2 $A > gpurun_out/ab2_cfg2_nofold.log 2>&1
+timeout 900 python bench.py --config cfg2 $A > gpurun_out/ab2_cfg2_fold.log 2>&1
