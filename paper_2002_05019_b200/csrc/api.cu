@@ -147,7 +147,7 @@ struct dd_aux_handle_s {
   std::vector<int64_t> grp_ptr;    // groups (distinct schur_group, ascending): members in clq_blk order
   std::vector<int32_t> grp_kept;   // kept indices sorted by (group, target)
   std::vector<int64_t> grp_m;      // m_g
-  std::vector<int32_t> kept_gperm, kept_ginv;  // identity maps of the kept rows (uploaded per factor)
+  std::vector<int32_t> kept_gperm, kept_ginv, kept_perm;  // identity maps of the kept rows (uploaded per factor)
   size_t off_sx_items = 0, off_sx_tiles = 0, off_sg_items = 0, off_sg_contrib = 0, off_ss_items = 0,
          off_soff = 0;
   int n_sx_tiles = 0, n_sg_items = 0, n_ss_items = 0;
@@ -902,6 +902,8 @@ int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offs
                              cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(F + h->off_ginv + (size_t)(h->n - (int64_t)h->kept_ginv.size()) * 4, h->kept_ginv.data(),
                              h->kept_ginv.size() * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(F + h->off_perm + (size_t)h->r0 * 4, h->kept_perm.data(), h->kept_perm.size() * 4,
+                             cudaMemcpyHostToDevice, st));
   }
   // ---- K0 load list
   std::vector<LoadBlock> lbs;
@@ -1789,9 +1791,13 @@ static int build_schur_tables(dd_aux_handle_t h) {
   // identity row maps of the kept blocks: rows [r0, n_pad), original DoFs [odof(NE), n)
   h->kept_gperm.clear();
   h->kept_ginv.clear();
+  h->kept_perm.clear();
   for (int t = NE; t < N; ++t) {
     const NodeDev& nd = h->nodes[t];
-    for (int m = 0; m < nd.sp; ++m) h->kept_gperm.push_back(m < nd.s ? (int32_t)(nd.odof + m) : -1);
+    for (int m = 0; m < nd.sp; ++m) {
+      h->kept_gperm.push_back(m < nd.s ? (int32_t)(nd.odof + m) : -1);
+      h->kept_perm.push_back(m);
+    }
   }
   for (int64_t o = h->odof_blk[NE]; o < h->n; ++o) {
     const int blk = (int)(std::upper_bound(h->odof_blk.begin(), h->odof_blk.end(), o) - h->odof_blk.begin()) - 1;
