@@ -140,6 +140,17 @@ def plan_subtrees(blk_size, colptr, rowidx, nparts, *, order_opt=DD_ORDER_AUTO, 
         top.append(k)
         top_fl += fl[k]
         roots.extend(children[k])
+    # a subtree whose root has no outside neighbours (a whole connected component) has nothing to
+    # condense onto T: its root joins T too, so every part's kept set is non-empty
+    while True:
+        lone = [k for k in roots if st_ptr[k + 1] == st_ptr[k]]
+        if not lone:
+            break
+        for k in lone:
+            roots.remove(k)
+            top.append(k)
+            top_fl += fl[k]
+            roots.extend(children[k])
     loads, own = lpt(roots)
     top = sorted(top, key=lambda k: pos[k])
     top_pos = {k: i for i, k in enumerate(top)}
@@ -275,6 +286,8 @@ class MultiGPUFactor:
         self.parts = {}
         for prt in mine:
             pp = self.plan.parts[prt]
+            if len(pp.elim) == 0:  # more ranks than subtrees: this part has nothing to factor
+                continue
             ss = SchurSolver(pp.blk_size, pp.colptr, pp.rowidx, pp.schur_target, pp.schur_group, self.plan.top_sizes,
                              complex_=complex_, order=DD_ORDER_NATURAL, device=device)
             ss._auxs = self.plan.top_sizes
@@ -310,15 +323,22 @@ class MultiGPUFactor:
             exports[prt] = (dS, Soff, ss.cliques())
         if self.dist is not None:       # NCCL point-to-point: every rank's S buffer to rank 0
             if self.rank != 0:
-                dS = exports[self.rank][0]
+                dS = exports[self.rank][0] if self.rank in exports else torch.zeros(0, dtype=torch.complex128 if
+                                                                                     self.cplx else torch.float64,
+                                                                                     device=self.device)
                 self.dist.send(torch.tensor([dS.numel()], dtype=torch.int64, device=dS.device), dst=0)
-                self.dist.send(dS, dst=0)
+                if dS.numel():
+                    self.dist.send(dS, dst=0)
             else:
                 for src in range(1, self.nparts):
                     n = torch.zeros(1, dtype=torch.int64, device=self.device)
                     self.dist.recv(n, src=src)
-                    buf = torch.empty(int(n.item()), dtype=exports[0][0].dtype, device=self.device)
-                    self.dist.recv(buf, src=src)
+                    buf = torch.empty(int(n.item()), dtype=torch.complex128 if self.cplx else torch.float64,
+                                      device=self.device)
+                    if buf.numel():
+                        self.dist.recv(buf, src=src)
+                    else:
+                        continue
                     cl = [P.cliques[si] for si in P.parts[src].groups]
                     ms = [int(P.top_sizes[c].sum()) for c in cl]
                     soff = np.concatenate([[0], np.cumsum([m * m for m in ms])[:-1]]).astype(np.int64)
@@ -434,6 +454,8 @@ class MultiGPUFactor:
                 self.dist.send(Xl[prt][:ne].t().contiguous(), dst=0)
         if self.dist is not None and self.rank == 0:
             for src in range(1, self.nparts):
+                if len(self.plan.parts[src].elim) == 0:
+                    continue
                 rows, ne, nk = self._rows(src)
                 buf = torch.empty((B.shape[1], len(rows)), dtype=B.dtype, device=B.device)
                 self.dist.recv(buf, src=src)

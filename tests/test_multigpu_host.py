@@ -150,3 +150,30 @@ def test_gloo_world2_reduce_protocol():
     for pr in procs:
         pr.join(timeout=60)
     assert res[0] is not None and res[0] <= 1e-10, res
+
+
+def test_plan_random_patterns_and_validate():
+    """plan_subtrees on random block graphs and orders: every non-top block in exactly one part, T
+    ancestor-closed, every part's Schur-mode handle passes the library's table validation."""
+    rng = np.random.default_rng(7)
+    for trial in range(20):
+        nblk = int(rng.integers(6, 40))
+        sizes = rng.integers(1, 30, nblk)
+        edges = [[u, v] for u in range(nblk) for v in range(u) if rng.random() < rng.uniform(0.05, 0.4)]
+        cp, ri = dd_inputs.block_pattern_from_cliques(nblk, edges)
+        nparts = int(rng.integers(2, 5))
+        plan = plan_subtrees(sizes, cp, ri, nparts)
+        owned = np.concatenate([pp.elim for pp in plan.parts] + [plan.top])
+        assert sorted(owned.tolist()) == list(range(nblk))
+        for pp in plan.parts:
+            if len(pp.elim) == 0:
+                continue
+            assert len(pp.schur_target) > 0   # every subtree condenses onto T (lone components join T)
+            h = dd.dd_aux_analyze_partial(pp.blk_size, pp.colptr, pp.rowidx, pp.schur_target, pp.schur_group,
+                                          plan.top_sizes, dd.DD_REAL64, dd.dd_aux_default_options(dd.DD_ORDER_NATURAL))
+            dd.dd_aux_validate(h)
+            dd.dd_aux_destroy(h)
+        if len(plan.top):
+            h = dd.dd_aux_analyze(plan.top_sizes, plan.top_colptr, plan.top_rowidx)
+            dd.dd_aux_validate(h)
+            dd.dd_aux_destroy(h)
