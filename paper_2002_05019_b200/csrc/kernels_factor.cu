@@ -1354,6 +1354,16 @@ struct K3Cfg<true, 18> {
   using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, true, true>;
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
+template <>
+struct K3Cfg<false, 19> {  // = 13
+  using G = Gemm<64, 64, 16, 2, 2, 2, false, false, false, false, false, false, true>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
+};
+template <>
+struct K3Cfg<true, 19> {  // complex 64x32 3M VEC (= 9) at 3 CTAs/SM: 168 registers, no spills
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, true, true>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 3;
+};
 #endif
 
 // One output tile of the Schur update (the body of both K3 launch forms).
@@ -1702,6 +1712,7 @@ int k3_bm(bool cplx, int cfg) {
     case 16: return bm_of<16>(cplx);
     case 17: return bm_of<17>(cplx);
     case 18: return bm_of<18>(cplx);
+    case 19: return bm_of<19>(cplx);
 #endif
     default: return bm_of<13>(cplx);
   }
@@ -1749,6 +1760,7 @@ int k3_bn(bool cplx, int cfg) {
     case 16: return bn_of<16>(cplx);
     case 17: return bn_of<17>(cplx);
     case 18: return bn_of<18>(cplx);
+    case 19: return bn_of<19>(cplx);
 #endif
     default: return bn_of<13>(cplx);
   }
@@ -1838,6 +1850,7 @@ void launch_k3(bool cplx, int cfg, const K3Args& a, int ntiles, cudaStream_t st,
     case 16: launch_k3_c<16>(cplx, a, ntiles, st); break;
     case 17: launch_k3_c<17>(cplx, a, ntiles, st); break;
     case 18: launch_k3_c<18>(cplx, a, ntiles, st); break;
+    case 19: launch_k3_c<19>(cplx, a, ntiles, st); break;
 #endif
     default: launch_k3_c<13>(cplx, a, ntiles, st); break;
   }
@@ -1881,6 +1894,7 @@ void launch_k2(bool cplx, int cfg, const K2Args& a, int nitems, int nstrips, int
       case 16: cplx ? launch_k2_t<true, 16>(a, nitems, max_s, st) : launch_k2_t<false, 16>(a, nitems, max_s, st); break;
       case 17: cplx ? launch_k2_t<true, 17>(a, nitems, max_s, st) : launch_k2_t<false, 17>(a, nitems, max_s, st); break;
       case 18: cplx ? launch_k2_t<true, 18>(a, nitems, max_s, st) : launch_k2_t<false, 18>(a, nitems, max_s, st); break;
+      case 19: cplx ? launch_k2_t<true, 19>(a, nitems, max_s, st) : launch_k2_t<false, 19>(a, nitems, max_s, st); break;
 #endif
       default: cplx ? launch_k2_t<true, 13>(a, nitems, max_s, st) : launch_k2_t<false, 13>(a, nitems, max_s, st); break;
     }
