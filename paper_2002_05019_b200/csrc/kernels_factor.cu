@@ -1375,10 +1375,32 @@ __device__ __forceinline__ void k3_tile(const K3Args& a, int64_t blk, double* sm
   // implicit tiles: find this CTA's target (last t with tprefix[t] <= gid) and its (tm, tn)
   const int64_t gid = a.tile0 + blk;
   int lo = 0, hi = a.ntargets - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a.tprefix[mid] <= gid) lo = mid;
-    else hi = mid - 1;
+#ifndef DDK_K3_SEARCH32
+#define DDK_K3_SEARCH32 1
+#endif
+  if (DDK_K3_SEARCH32) {
+    // 32-ary search: each round every lane probes one of 32 evenly spaced candidates at once (one
+    // dependent global latency per round instead of one per halving); every warp finds the same t
+    const int lane = threadIdx.x & 31;
+    while (lo < hi) {
+      const int step = (hi - lo + 31) >> 5;  // >= 1
+      const int pidx = lo + 1 + lane * step;
+      const bool ok = pidx <= hi && a.tprefix[pidx] <= gid;
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      if (m == 0u) {
+        hi = lo;
+      } else {
+        const int j = 31 - __clz(m);  // the last candidate with tprefix <= gid (tprefix ascending)
+        lo = lo + 1 + j * step;
+        hi = min(hi, lo + step - 1);
+      }
+    }
+  } else {
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.tprefix[mid] <= gid) lo = mid;
+      else hi = mid - 1;
+    }
   }
   const UpdTarget tg = a.targets[lo];
   Tile T;
