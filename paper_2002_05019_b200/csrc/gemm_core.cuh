@@ -38,6 +38,15 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+// fixed 16-byte copy to a shared-window address, skipped when !pred (the destination keeps its
+// old contents: only for rows / columns whose results are never stored)
+__device__ __forceinline__ void cp_async16_if(unsigned saddr, const void* gmem, int pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
+      " @p cp.async.cg.shared.global [%0], [%1], 16;\n}\n" ::"r"(saddr),
+      "l"(gmem), "r"(pred)
+      : "memory");
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
@@ -86,7 +95,8 @@ __device__ __forceinline__ double dneg(double x) {  // sign flip on the integer 
 // adjacent in shared memory: one 16-byte LDS each instead of two 8-byte ones (bank-conflict free
 // with the ld = 4 (mod 16) padding).  The accumulator mapping (for_each, masks) follows.
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool CPLX, bool A_KM, bool B_KN,
-          bool C3M = false, bool FINE = true, bool VEC = false, bool RECT = false, bool MBAR = false>
+          bool C3M = false, bool FINE = true, bool VEC = false, bool RECT = false, bool MBAR = false,
+          bool FAST = true>
 struct Gemm {
   static constexpr int NTHR = WARPS_M * WARPS_N * 32;
   static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
@@ -297,6 +307,157 @@ struct Gemm {
     }
   }
 
+  // ---- Fast loader (MK x NK operands, no column gather).  load_stage recomputes every chunk's
+  // source address and bounds from scratch (~26 SASS instructions and a 6-deep dependent chain
+  // per cp.async: more issue slots per stage than the DMMAs themselves).  A thread's chunks of a
+  // stage all share one row offset and sit a fixed number of k-columns apart, so inside a segment
+  // the thread keeps ONE running pointer per operand (pa, pb): a full stage costs one 64-bit add
+  // per chunk.  The row predicate (bytes) is constant per tile; only a segment's last partial
+  // stage (pk + BK > K) and gathered segments go through load_stage.  The chunks of the next
+  // stage are issued in BK/4 parts between the k-steps of the current stage (part(ks)), so no
+  // warp spends a long DMMA-free stretch issuing copies.
+#ifndef DDK_FASTLD
+#define DDK_FASTLD 1
+#endif
+  static constexpr int KSTEPS = BK / 4;
+  // the copies of a stage go out in the first SPREAD k-steps (KSTEPS = evenly over the stage)
+#ifndef DDK_FASTLD_SPREAD
+#define DDK_FASTLD_SPREAD 0
+#endif
+  static constexpr int SPREAD = (DDK_FASTLD_SPREAD > 0 && DDK_FASTLD_SPREAD < KSTEPS) ? DDK_FASTLD_SPREAD : KSTEPS;
+  // One operand's copy pattern.  RC (row-contiguous: A "MK" / B "NK"): a thread's chunks share one
+  // row pair and sit KS k-columns apart, the running pointer walks through them and through the
+  // stages.  KC (k-contiguous: A "KM" / B "KN"): a thread's chunks share one k pair and sit RS
+  // rows apart (pointer p0 + j * RS * ld, one row-predicate bit per chunk); a stage advances p0
+  // by BK elements.
+  template <int R, int LD, bool KC>
+  struct Pat {
+    static constexpr int GRP = KC ? BK / 2 : R / 2;          // threads along the contiguous direction
+    static constexpr int STEP = NTHR / (GRP > 0 ? GRP : 1);  // k columns (RC) or rows (KC) between chunks
+    static constexpr int CH = (KC ? R : BK) / (STEP > 0 ? STEP : 1);
+    static constexpr bool OK = GRP > 0 && NTHR % GRP == 0 && (KC ? R : BK) % STEP == 0 && CH >= 1 && CH <= 32;
+    __device__ static int off(int tid) {  // offset of the thread's first chunk inside the operand's stage tile
+      const int c = (tid % GRP) * 2, o = tid / GRP;
+      return KC ? o * LD + c : o * LD + c;
+    }
+    static constexpr int DSTEP = STEP * LD;  // smem distance between a thread's successive chunks
+  };
+  using PA = Pat<BM, A_LD, A_KM>;
+  using PB = Pat<BN, B_LD, B_KN>;
+  static constexpr bool FASTLD = DDK_FASTLD && FAST && !MBAR && PA::OK && PB::OK;
+  struct FastLd {
+    const double* pa;  // this thread's first A chunk of the next full stage
+    const double* pb;
+    int64_t ia, ib;    // element stride between the thread's successive chunks
+    unsigned ba, bb;   // row predicate(s): RC one flag, KC bit j = chunk j's row lies inside the operand
+    unsigned sa, sb;   // shared-window address of this thread's first A / B chunk in stage slot 0
+  };
+  // Rows m >= M of A (columns n >= N of B) are NOT zero-filled here, and a last odd row is copied
+  // as a full 16-byte chunk: row m of the product depends on row m of A only, rows >= M are never
+  // stored, and the extra element lies inside the operand's (even) leading dimension.  Zero fill
+  // matters along K only, which the generic loader handles (partial last stage of a segment).
+  template <class P, bool KC>
+  __device__ static unsigned fast_pred(int r0, int lim) {
+    const int tid = threadIdx.x;
+    if constexpr (!KC) {
+      return (unsigned)(r0 + (tid % P::GRP) * 2 < lim);
+    } else {
+      unsigned m = 0;
+#pragma unroll
+      for (int j = 0; j < P::CH; ++j) m |= (unsigned)(r0 + tid / P::GRP + j * P::STEP < lim) << j;
+      return m;
+    }
+  }
+  __device__ static void fast_tile(FastLd& f, double* smem, int m0, int n0, int M, int N) {
+    f.ba = fast_pred<PA, A_KM>(m0, M);
+    f.bb = fast_pred<PB, B_KN>(n0, N);
+    f.sa = smem_u32(smem + PA::off(threadIdx.x));
+    f.sb = smem_u32(smem + NPL * A_TILE + PB::off(threadIdx.x));
+  }
+  // pointer to the thread's first chunk at k offset 0 of a segment + the chunk stride
+  template <class P, bool KC>
+  __device__ static void fast_ptr(const double*& p, int64_t& inc, unsigned pred, const double* base, int64_t ld,
+                                  int r0) {
+    const int tid = threadIdx.x;
+    const int c = (tid % P::GRP) * 2, o = tid / P::GRP;
+    if constexpr (!KC) {
+      p = pred ? base + (r0 + c) + (int64_t)o * ld : base;
+      inc = pred ? (int64_t)P::STEP * ld : 0;
+    } else {
+      p = base + c + (int64_t)(r0 + o) * ld;  // chunks whose row is outside are predicated off
+      inc = (int64_t)P::STEP * ld;
+    }
+  }
+  __device__ static void fast_seg(FastLd& f, const Seg& sg, int m0, int n0) {
+    fast_ptr<PA, A_KM>(f.pa, f.ia, f.ba, sg.a, sg.lda, m0);
+    fast_ptr<PB, B_KN>(f.pb, f.ib, f.bb, sg.b, sg.ldb, n0);
+  }
+  template <class P, bool KC, int KS, int TILE>
+  __device__ static void fast_op(const double*& p, int64_t inc, unsigned pred, unsigned sdst, int64_t im) {
+#pragma unroll
+    for (int j = 0; j < P::CH; ++j)
+      if (j * SPREAD / P::CH == KS) {
+        const unsigned d = sdst + (unsigned)(j * P::DSTEP * sizeof(double));
+        if constexpr (!KC) {
+          cp_async16_if(d, p, pred);
+          if constexpr (CPLX) cp_async16_if(d + (unsigned)(TILE * sizeof(double)), p + im, pred);
+          p += inc;
+        } else {
+          const double* q = p + j * inc;
+          cp_async16_if(d, q, (pred >> j) & 1u);
+          if constexpr (CPLX) cp_async16_if(d + (unsigned)(TILE * sizeof(double)), q + im, (pred >> j) & 1u);
+        }
+      }
+    if constexpr (KC && KS == SPREAD - 1) p += BK;
+  }
+  // part KS (of KSTEPS) of a full stage's copies into stage slot `slot`
+  template <int KS>
+  __device__ static void fast_part(FastLd& f, int slot, int64_t aim, int64_t bim) {
+    const unsigned so = (unsigned)slot * (unsigned)(STAGE * sizeof(double));
+    fast_op<PA, A_KM, KS, A_TILE>(f.pa, f.ia, f.ba, f.sa + so, aim);
+    fast_op<PB, B_KN, KS, B_TILE>(f.pb, f.ib, f.bb, f.sb + so, bim);
+  }
+  // What the copy engine of run() does during one compute stage: mode 0 nothing, 1 a full stage
+  // through the running pointers (in parts, between the k-steps), 2 the generic loader (all of
+  // it ahead of the compute stage: one inlined copy, not one per compute body).
+  struct StageLd {
+    int mode, slot;
+    double* st;
+    FastLd* f;
+    const Seg* sg;
+    int kofs, m0, n0, M, N;
+    int64_t aim, bim;
+    template <int KS>
+    __device__ __forceinline__ void part() const {
+      if (mode == 1) fast_part<KS>(*f, slot, aim, bim);
+    }
+    __device__ __forceinline__ void generic() const {  // mode 2: ahead of the compute stage
+      if (mode == 2) load_stage(st, *sg, kofs, m0, n0, M, N, aim, bim);
+    }
+    __device__ __forceinline__ void part_rt(int ks) const {  // ks is a constant after unrolling
+      switch (ks) {
+        case 0: part<0>(); break;
+        case 1: if constexpr (KSTEPS > 1) part<1 % KSTEPS>(); break;
+        case 2: if constexpr (KSTEPS > 2) part<2 % KSTEPS>(); break;
+        case 3: if constexpr (KSTEPS > 3) part<3 % KSTEPS>(); break;
+        case 4: if constexpr (KSTEPS > 4) part<4 % KSTEPS>(); break;
+        case 5: if constexpr (KSTEPS > 5) part<5 % KSTEPS>(); break;
+        case 6: if constexpr (KSTEPS > 6) part<6 % KSTEPS>(); break;
+        case 7: if constexpr (KSTEPS > 7) part<7 % KSTEPS>(); break;
+      }
+    }
+    __device__ __forceinline__ void all() const {
+      part<0>();
+      if constexpr (KSTEPS > 1) part<1 % KSTEPS>();
+      if constexpr (KSTEPS > 2) part<2 % KSTEPS>();
+      if constexpr (KSTEPS > 3) part<3 % KSTEPS>();
+      if constexpr (KSTEPS > 4) part<4 % KSTEPS>();
+      if constexpr (KSTEPS > 5) part<5 % KSTEPS>();
+      if constexpr (KSTEPS > 6) part<6 % KSTEPS>();
+      if constexpr (KSTEPS > 7) part<7 % KSTEPS>();
+    }
+  };
+
   // Bit (a*NI + b) set = this warp's 16x8 sub-tile (a, b) intersects the valid region: rows
   // < mlim, cols < nlim and, when diag_off != NO_DIAG, not strictly above the diagonal
   // col - row == diag_off (diagonal target blocks store only their lower triangle).  Masked
@@ -333,8 +494,10 @@ struct Gemm {
   // Sub-tiles a < NA, b < NB of the warp tile; PRED: per-mma predicate from mask (FINE mode).
   // nks: k-steps of 4 holding data in this stage (a segment's last stage may be partly
   // zero-filled: its empty k-steps issue no DMMA)
-  template <int NA, int NB, bool PRED>
-  __device__ static void compute_body(const double* st, Acc& acc, unsigned mask, int nks = BK / 4) {
+  // LD: the copies of the next stage (ld) are issued in parts between the k-steps
+  template <int NA, int NB, bool PRED, bool LD = false>
+  __device__ static void compute_body(const double* st, Acc& acc, unsigned mask, int nks = BK / 4,
+                                      const StageLd* ld = nullptr) {
     if constexpr (!PRED) mask = ~0u;  // constant: the per-mma predicates fold away
     const double* As = st;
     const double* Bs = st + NPL * A_TILE;
@@ -470,7 +633,16 @@ struct Gemm {
 #ifndef DDK_FRAG_DB
 #define DDK_FRAG_DB 0
 #endif
-    if constexpr (DDK_FRAG_DB != 0) {
+    if constexpr (LD) {
+#pragma unroll
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        const bool live = ks == 0 || ks < nks;  // warp-uniform; an empty k-step loads and issues nothing
+        Frag f;
+        if (live) load(ks, f);
+        ld->part_rt(ks);
+        if (live) issue(f);
+      }
+    } else if constexpr (DDK_FRAG_DB != 0) {
       // register double-buffered fragments: the loads of k-step ks+1 are issued before the DMMAs
       // of k-step ks (the k-tail skip is kept: an empty k-step loads and issues nothing)
       Frag fr[2];
@@ -492,25 +664,33 @@ struct Gemm {
     }
   }
 
-  __device__ static void compute_stage(const double* st, Acc& acc, unsigned mask = ~0u, int nks = BK / 4) {
+  template <bool LD = false>
+  __device__ static void compute_stage(const double* st, Acc& acc, unsigned mask = ~0u, int nks = BK / 4,
+                                       const StageLd* ld = nullptr) {
     if constexpr (RECT) {
-      if (mask == 0u) return;  // warp-uniform
+      if (mask == 0u) {  // warp-uniform
+        if constexpr (LD) ld->all();
+        return;
+      }
       const int na = (mask >> 4) & 15, ncg = (mask >> 8) & 15;
       constexpr int BPG = VEC ? 2 : 1;  // sub-tiles per column group
-      if (na == MI && ncg == NCG) return compute_body<MI, NI, false>(st, acc, ~0u, nks);
+      if (na == MI && ncg == NCG) return compute_body<MI, NI, false, LD>(st, acc, ~0u, nks, ld);
       if constexpr (MI >= 2) {
-        if (na == 1 && ncg == NCG) return compute_body<1, NI, false>(st, acc, ~0u, nks);
+        if (na == 1 && ncg == NCG) return compute_body<1, NI, false, LD>(st, acc, ~0u, nks, ld);
       }
       if constexpr (NCG >= 2) {
-        if (na == MI && ncg == 1) return compute_body<MI, BPG, false>(st, acc, ~0u, nks);
-        if (na == 1 && ncg == 1) return compute_body<1, BPG, false>(st, acc, ~0u, nks);
+        if (na == MI && ncg == 1) return compute_body<MI, BPG, false, LD>(st, acc, ~0u, nks, ld);
+        if (na == 1 && ncg == 1) return compute_body<1, BPG, false, LD>(st, acc, ~0u, nks, ld);
       }
-      return compute_body<MI, NI, false>(st, acc, ~0u, nks);  // other shapes: full warp tile
+      return compute_body<MI, NI, false, LD>(st, acc, ~0u, nks, ld);  // other shapes: full warp tile
     } else if constexpr (!FINE) {
-      if (mask == 0u) return;  // warp-uniform
-      compute_body<MI, NI, false>(st, acc, ~0u, nks);
+      if (mask == 0u) {  // warp-uniform
+        if constexpr (LD) ld->all();
+        return;
+      }
+      compute_body<MI, NI, false, LD>(st, acc, ~0u, nks, ld);
     } else {
-      compute_body<MI, NI, true>(st, acc, mask, nks);
+      compute_body<MI, NI, true, LD>(st, acc, mask, nks, ld);
     }
   }
 
@@ -551,6 +731,58 @@ struct Gemm {
       const int kv = DDK_KSKIP ? min(BK, cur.K - pk) : BK;
       kvpack = (kvpack & ~(15u << (4 * slot))) | ((unsigned)((kv + 3) / 4) << (4 * slot));
     };
+    if constexpr (FASTLD) {
+      FastLd f;
+      fast_tile(f, smem, m0, n0, M, N);
+      if (pseg < nseg) fast_seg(f, cur, m0, n0);
+      StageLd sl;
+      sl.f = &f;
+      sl.sg = &cur;
+      sl.m0 = m0, sl.n0 = n0, sl.M = M, sl.N = N, sl.aim = aim, sl.bim = bim;
+      // choose how the next stage is copied (before the copies), then step to the stage after it
+      auto plan = [&]() {
+        sl.mode = 0;
+        if (pseg < nseg) {
+          sl.mode = (cur.acol == nullptr && pk + BK <= cur.K) ? 1 : 2;
+          sl.slot = issued % STAGES;
+          sl.st = smem + sl.slot * STAGE;
+          sl.kofs = pk;
+          note_k(issued % STAGES);
+        }
+      };
+      auto step = [&]() {
+        if (sl.mode) {
+          const int was = pseg;
+          advance();
+          ++issued;
+          if (pseg != was && pseg < nseg) fast_seg(f, cur, m0, n0);
+        }
+      };
+#pragma unroll 1
+      for (int s = 0; s < STAGES - 1; ++s) {
+        plan();
+        sl.generic();
+        sl.all();
+        step();
+        cp_async_commit();
+      }
+      int done = 0;
+#pragma unroll 1
+      while (done < issued) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        plan();
+        sl.generic();
+        const int slot = done % STAGES;
+        compute_stage<true>(smem + slot * STAGE, acc, mask, (int)((kvpack >> (4 * slot)) & 15u), &sl);
+        step();
+        cp_async_commit();
+        ++done;
+      }
+      cp_async_wait<0>();
+      __syncthreads();
+      return;
+    }
 #pragma unroll 1
     for (int s = 0; s < STAGES - 1; ++s) {
       if (pseg < nseg) {

@@ -1239,8 +1239,8 @@ struct K3Cfg<false, 9> {  // real 64x64, coarse masking, vectorised (16-byte) fr
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
 };
 template <>
-struct K3Cfg<true, 9> {  // complex 64x32 3M, vectorised fragment loads
-  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, true, true>;
+struct K3Cfg<true, 9> {  // complex 64x32 3M, vectorised fragment loads (generic loader: the fast one spills at 128 registers)
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, true, true, false, false, false>;
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
 template <>
@@ -1290,7 +1290,7 @@ struct K3Cfg<false, 13> {  // real 64x64, RECT, 2 stages (34 KB smem; dense micr
 };
 template <>
 struct K3Cfg<true, 13> {  // complex 64x32 3M, 2 stages, coarse masking (no per-mma predicates)
-  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, false, false, false>;
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, false, false, false, false, false>;
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
 

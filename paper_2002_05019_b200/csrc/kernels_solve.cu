@@ -102,7 +102,7 @@ __global__ void k_copy(const double* __restrict__ src, int64_t lds, double* __re
 // inverse (k_linv): CTA (node, 64-row tile) x (64-rhs tile), K restricted to the triangle;
 // results go to the level buffer T, then k_dcopy moves them back into y (no in-place hazard).
 template <bool C, bool BWD, bool M3>
-__global__ void __launch_bounds__(128) k_diag_g(SolveArgs a) {
+__global__ void __launch_bounds__(128, M3 ? 3 : 4) k_diag_g(SolveArgs a) {
   if (a.flag && *a.flag == 0) return;
   using G = typename std::conditional<BWD, typename SolveG<C, M3>::BU, typename SolveG<C, M3>::FU>::type;
   constexpr int SBN = SolveN<C>::value;
@@ -142,7 +142,7 @@ __global__ void k_dcopy(SolveArgs a, int ntiles) {
 
 // ---------------------------------------------------------------------------- level updates
 template <bool C, bool M3>
-__global__ void __launch_bounds__(128) k_fupd(SolveArgs a) {
+__global__ void __launch_bounds__(128, M3 ? 3 : 4) k_fupd(SolveArgs a) {
   if (a.flag && *a.flag == 0) return;
   using G = typename SolveG<C, M3>::FU;
   constexpr int SBN = SolveN<C>::value;
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(128) k_fupd(SolveArgs a) {
 // through distributed shared memory in the same fixed order g = 0..G-1 (bitwise the same result
 // as the two-kernel partial-buffer path, without its HBM round trip and second launch).
 template <bool C, bool M3, bool CL, bool FOLD = false>
-__global__ void __launch_bounds__(128) k_bupd(SolveArgs a, int G, double* part, int64_t pim) {
+__global__ void __launch_bounds__(128, M3 ? 3 : 4) k_bupd(SolveArgs a, int G, double* part, int64_t pim) {
   if (a.flag && *a.flag == 0) return;
   using G_ = typename SolveG<C, M3>::BU;
   constexpr int SBN = SolveN<C>::value;

@@ -101,6 +101,8 @@ int main() {
   run<Gemm<64, 32, 16, 2, 2, 2, true, false, false>, true, 64, 32>("cplx 64x32 K=512", 8192, 512, 512);
   // mbarrier pipeline (no CTA barrier per stage) vs __syncthreads pipeline, K3 real regime
   run<Gemm<64, 64, 16, 2, 2, 2, false, false, false, false, false, false, true>, false, 64, 64>("real 64x64 RECT 2st K=576", 8192, 576, 576);
+  run<Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false, false, true>, false, 64, 64>("real 64x64 RECT 3st K=576", 8192, 576, 576);
+  run<Gemm<64, 64, 16, 2, 2, 2, false, false, false, false, false, false, true>, false, 64, 64>("real 64x64 RECT 2st K=8192", 8192, 8192, 512);
   run<Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false, false, true, true>, false, 64, 64>("real 64x64 RECT 3st MBAR K=576", 8192, 576, 576);
   run<Gemm<64, 64, 16, 2, 2, 4, false, false, false, false, false, false, true, true>, false, 64, 64>("real 64x64 RECT 4st MBAR K=576", 8192, 576, 576);
   run<Gemm<64, 64, 16, 2, 2, 3, false, false, false, false, false, false, true, true>, false, 64, 64>("real 64x64 RECT 3st MBAR K=8192", 8192, 8192, 512);
