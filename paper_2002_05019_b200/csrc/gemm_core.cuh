@@ -132,11 +132,23 @@ struct Gemm {
         }
   }
 
+  // Warp aliasing for ragged tiles (RECT, 2 x 2 warps, tile_mask(.., alias = true)): when only warp
+  // row 0 (and / or warp column 0) of a tile holds valid rows (columns), the warps of row 1
+  // (column 1) would idle.  They are mapped onto the same warp tile as their row-0 (column-0)
+  // sibling instead and the k-steps of every stage are dealt round-robin over the 2 (4) aliases;
+  // store_tile adds the partial sums in a fixed order.
+  __device__ static int alias_nsplit(unsigned amap) { return ((amap & 1u) ? 2 : 1) * ((amap & 2u) ? 2 : 1); }
+  __device__ static int alias_part(unsigned amap) {
+    const int warp = threadIdx.x >> 5;
+    return ((amap & 1u) ? warp % WARPS_M : 0) + ((amap & 2u) ? (warp / WARPS_M) * ((amap & 1u) ? 2 : 1) : 0);
+  }
+
   // Visit every accumulator element: f(row_in_tile, col_in_tile, re, im)
+  // amap (RECT + alias, see tile_mask): bit 0 / 1 = this tile's warps all work on warp row / column 0
   template <class F>
-  __device__ static void for_each(const Acc& acc, F f) {
+  __device__ static void for_each(const Acc& acc, F f, unsigned amap = 0u) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+    const int wm = (amap & 1u) ? 0 : warp % WARPS_M, wn = (amap & 2u) ? 0 : warp / WARPS_M;
     const int g = lane >> 2, tg = lane & 3;
 #pragma unroll
     for (int a = 0; a < MI; ++a)
@@ -182,16 +194,57 @@ struct Gemm {
   // MODE 0: C = acc, 1: C -= acc.  Call after run() (which ends with a barrier); ends with one.
   static constexpr int ELD = BM + 2;
   static_assert((size_t)BN * ELD * (CPLX ? 2 : 1) <= (size_t)STAGES * STAGE, "epilogue tile fits the pipeline smem");
+  // MODE 2: C -= acc as fire-and-forget reductions at L2 (red.global.add.f64 of -acc): no C load,
+  // no round trip before the CTA retires.  Every element of C gets exactly ONE reduction per
+  // launch (owner-computes tiles; aliased warps are summed in shared memory first), so the result
+  // does not depend on the order the reductions arrive in, and C + (-v) rounds as C - v does:
+  // bitwise the read-modify-write result.  `active` = this warp holds a computed warp tile.
   template <int MODE>
   __device__ static void store_tile(const Acc& acc, double* smem, double* C, int64_t ldc, int64_t cim, int mlim,
-                                    int nlim) {
+                                    int nlim, unsigned amap = 0u, bool active = true) {
     double* Sr = smem;
     double* Si = smem + BN * ELD;
-    for_each(acc, [&](int r, int c, double vr, double vi) {
-      Sr[c * ELD + r] = vr;
-      if constexpr (CPLX) Si[c * ELD + r] = vi;
-    });
-    __syncthreads();
+    if constexpr (MODE == 2) {
+      if (amap == 0u) {  // straight from the accumulator fragments (8 rows x 1 column = two full sectors)
+        if (active)
+          for_each(acc, [&](int r, int c, double vr, double vi) {
+            if (r < mlim && c < nlim) {
+              atomicAdd(C + r + (int64_t)c * ldc, -vr);
+              if constexpr (CPLX) atomicAdd(C + r + (int64_t)c * ldc + cim, -vi);
+            }
+          });
+        return;
+      }
+    }
+    if (amap == 0u) {
+      for_each(acc, [&](int r, int c, double vr, double vi) {
+        Sr[c * ELD + r] = vr;
+        if constexpr (CPLX) Si[c * ELD + r] = vi;
+      });
+      __syncthreads();
+    } else {
+      // aliased warps hold partial sums (their share of the k-steps) of the same warp tile: added
+      // in the fixed order part 0, 1, .. (deterministic)
+      const int nsplit = alias_nsplit(amap), part = alias_part(amap);
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        if (p >= nsplit) break;  // CTA-uniform
+        if (part == p)
+          for_each(
+              acc,
+              [&](int r, int c, double vr, double vi) {
+                if (p == 0) {
+                  Sr[c * ELD + r] = vr;
+                  if constexpr (CPLX) Si[c * ELD + r] = vi;
+                } else {
+                  Sr[c * ELD + r] += vr;
+                  if constexpr (CPLX) Si[c * ELD + r] += vi;
+                }
+              },
+              amap);
+        __syncthreads();
+      }
+    }
     constexpr int PER = (BM * BN + NTHR - 1) / NTHR;
     // the accumulator registers are dead once staged, so a whole tile's loads fit in flight
 #ifndef DDK_EPI_BATCH
@@ -210,6 +263,18 @@ struct Gemm {
           old_r[u] = C[r + (int64_t)c * ldc];
           if constexpr (CPLX) old_i[u] = C[r + (int64_t)c * ldc + cim];
         }
+      }
+      if constexpr (MODE == 2) {  // aliased tile: the summed staging tile goes out as reductions
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u) {
+          const int e = threadIdx.x + (q0 + u) * NTHR;
+          const int r = e % BM, c = e / BM;
+          if (q0 + u < PER && c < BN && r < mlim && c < nlim) {
+            atomicAdd(C + r + (int64_t)c * ldc, -Sr[c * ELD + r]);
+            if constexpr (CPLX) atomicAdd(C + r + (int64_t)c * ldc + cim, -Si[c * ELD + r]);
+          }
+        }
+        continue;
       }
 #pragma unroll
       for (int u = 0; u < BATCH; ++u) {
@@ -320,11 +385,18 @@ struct Gemm {
 #define DDK_FASTLD 1
 #endif
   static constexpr int KSTEPS = BK / 4;
-  // the copies of a stage go out in the first SPREAD k-steps (KSTEPS = evenly over the stage)
+  // the copies of a stage go out in the first SPREAD k-steps.  Measured on cfg2 (2-stage pipelines):
+  // K3 (MK x NK) 29.3 / 29.8 / 29.9 TF/s with SPREAD 1 / 2 / 4; the solve (.. x KN) 4,405 / 4,367 /
+  // 4,505 ms per 1000 RHS -- copies issued in the last k-steps have little time to land before
+  // the next stage's wait, which the solve's shorter stages (32-column tiles) expose.
 #ifndef DDK_FASTLD_SPREAD
 #define DDK_FASTLD_SPREAD 0
 #endif
-  static constexpr int SPREAD = (DDK_FASTLD_SPREAD > 0 && DDK_FASTLD_SPREAD < KSTEPS) ? DDK_FASTLD_SPREAD : KSTEPS;
+#ifndef DDK_FASTLD_SPREAD_KN
+#define DDK_FASTLD_SPREAD_KN 2
+#endif
+  static constexpr int SPREAD_REQ = B_KN ? DDK_FASTLD_SPREAD_KN : DDK_FASTLD_SPREAD;
+  static constexpr int SPREAD = (SPREAD_REQ > 0 && SPREAD_REQ < KSTEPS) ? SPREAD_REQ : KSTEPS;
   // One operand's copy pattern.  RC (row-contiguous: A "MK" / B "NK"): a thread's chunks share one
   // row pair and sit KS k-columns apart, the running pointer walks through them and through the
   // stages.  KC (k-contiguous: A "KM" / B "KN"): a thread's chunks share one k pair and sit RS
@@ -344,7 +416,8 @@ struct Gemm {
   };
   using PA = Pat<BM, A_LD, A_KM>;
   using PB = Pat<BN, B_LD, B_KN>;
-  static constexpr bool FASTLD = DDK_FASTLD && FAST && !MBAR && PA::OK && PB::OK;
+  static constexpr bool FASTLD_ANY = DDK_FASTLD && FAST && PA::OK && PB::OK;
+  static constexpr bool FASTLD = FASTLD_ANY && !MBAR;
   struct FastLd {
     const double* pa;  // this thread's first A chunk of the next full stage
     const double* pb;
@@ -468,15 +541,25 @@ struct Gemm {
   // (entirely outside, or strictly above a diagonal target's diagonal).
   static constexpr int CG = VEC ? 16 : 8;    // columns per column group
   static constexpr int NCG = WTN / CG;       // column groups per warp tile
-  __device__ static unsigned tile_mask(int mlim, int nlim, int diag_off) {
+  static constexpr bool ALIAS_OK = RECT && WARPS_M == 2 && WARPS_N == 2;
+  // CTA-uniform alias map of a tile with mlim valid rows and nlim valid columns
+  __device__ static unsigned alias_map(int mlim, int nlim) {
+    return ALIAS_OK ? (unsigned)(mlim <= WTM) | ((unsigned)(nlim <= WTN) << 1) : 0u;
+  }
+  __device__ static unsigned tile_mask(int mlim, int nlim, int diag_off, bool alias = false) {
     const int warp = threadIdx.x >> 5;
-    const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+    int wm = warp % WARPS_M, wn = warp / WARPS_M;
     if constexpr (RECT) {
+      unsigned amap = 0u;
+      if constexpr (ALIAS_OK) {
+        if (alias && mlim <= WTM) amap |= 1u, wm = 0;
+        if (alias && nlim <= WTN) amap |= 2u, wn = 0;
+      }
       const int r0 = wm * WTM, c0 = wn * WTN;
       if (r0 >= mlim || c0 >= nlim) return 0u;
       if (diag_off != NO_DIAG && r0 + WTM - 1 < c0 + diag_off) return 0u;
       const int na = min(MI, (mlim - r0 + 15) / 16), ncg = min(NCG, (nlim - c0 + CG - 1) / CG);
-      return 1u | ((unsigned)na << 4) | ((unsigned)ncg << 8);
+      return 1u | ((unsigned)na << 4) | ((unsigned)ncg << 8) | (amap << 12);
     }
     unsigned m = 0;
 #pragma unroll
@@ -497,12 +580,22 @@ struct Gemm {
   // LD: the copies of the next stage (ld) are issued in parts between the k-steps
   template <int NA, int NB, bool PRED, bool LD = false>
   __device__ static void compute_body(const double* st, Acc& acc, unsigned mask, int nks = BK / 4,
-                                      const StageLd* ld = nullptr) {
+                                      const StageLd* ld = nullptr, unsigned amap = 0u) {
     if constexpr (!PRED) mask = ~0u;  // constant: the per-mma predicates fold away
     const double* As = st;
     const double* Bs = st + NPL * A_TILE;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+    const int wm = (amap & 1u) ? 0 : warp % WARPS_M, wn = (amap & 2u) ? 0 : warp / WARPS_M;
+    // live k-steps of this warp: those holding data (k tail) and, for aliased warps, ks = part (mod nsplit)
+    unsigned lm = (1u << (nks > 0 ? nks : 1)) - 1u;
+    if (amap) {
+      const int ns = alias_nsplit(amap), pt = alias_part(amap);
+      unsigned pm = 0u;
+#pragma unroll
+      for (int ks = 0; ks < BK / 4; ++ks)
+        if ((ks & (ns - 1)) == pt) pm |= 1u << ks;
+      lm &= pm;
+    }
     const int g = lane >> 2, tg = lane & 3;
     struct Frag {
       double ar[MI][2], br[NI];
@@ -636,7 +729,8 @@ struct Gemm {
     if constexpr (LD) {
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
-        const bool live = ks == 0 || ks < nks;  // warp-uniform; an empty k-step loads and issues nothing
+        // warp-uniform; an empty k-step (k tail, or another alias's share) loads and issues nothing
+        const bool live = (lm >> ks) & 1u;
         Frag f;
         if (live) load(ks, f);
         ld->part_rt(ks);
@@ -657,6 +751,7 @@ struct Gemm {
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
         if (DDK_KSTEP_BREAK && ks > 0 && ks >= nks) break;  // warp-uniform
+        if (!((lm >> ks) & 1u)) continue;
         Frag f;
         load(ks, f);
         issue(f);
@@ -664,7 +759,9 @@ struct Gemm {
     }
   }
 
-  template <bool LD = false>
+  // AL: the tile's warps may be aliased (runtime amap from the mask); otherwise amap is the
+  // constant 0 and the alias logic folds away (its runtime form costs registers: spills at 128)
+  template <bool LD = false, bool AL = false>
   __device__ static void compute_stage(const double* st, Acc& acc, unsigned mask = ~0u, int nks = BK / 4,
                                        const StageLd* ld = nullptr) {
     if constexpr (RECT) {
@@ -674,6 +771,13 @@ struct Gemm {
       }
       const int na = (mask >> 4) & 15, ncg = (mask >> 8) & 15;
       constexpr int BPG = VEC ? 2 : 1;  // sub-tiles per column group
+      if constexpr (AL) {  // ragged tiles only: two bodies (code size)
+        const unsigned amap = (mask >> 12) & 3u;
+        if constexpr (MI >= 2) {
+          if (na == 1) return compute_body<1, NI, false, LD>(st, acc, ~0u, nks, ld, amap);
+        }
+        return compute_body<MI, NI, false, LD>(st, acc, ~0u, nks, ld, amap);
+      }
       if (na == MI && ncg == NCG) return compute_body<MI, NI, false, LD>(st, acc, ~0u, nks, ld);
       if constexpr (MI >= 2) {
         if (na == 1 && ncg == NCG) return compute_body<1, NI, false, LD>(st, acc, ~0u, nks, ld);
@@ -696,7 +800,7 @@ struct Gemm {
 
   // Main loop over a segment list. SegFn: Seg(int idx). All threads of the CTA call this
   // with identical arguments.  smem: STAGES*STAGE doubles.  Ends with a __syncthreads().
-  template <class SegFn>
+  template <bool AL = false, class SegFn>
   __device__ static void run(SegFn segfn, int nseg, int m0, int n0, int M, int N, int64_t aim, int64_t bim,
                              double* smem, Acc& acc, unsigned mask = ~0u) {
     if constexpr (MBAR) {
@@ -774,7 +878,7 @@ struct Gemm {
         plan();
         sl.generic();
         const int slot = done % STAGES;
-        compute_stage<true>(smem + slot * STAGE, acc, mask, (int)((kvpack >> (4 * slot)) & 15u), &sl);
+        compute_stage<true, AL>(smem + slot * STAGE, acc, mask, (int)((kvpack >> (4 * slot)) & 15u), &sl);
         step();
         cp_async_commit();
         ++done;
@@ -806,7 +910,7 @@ struct Gemm {
       }
       cp_async_commit();
       const int slot = done % STAGES;
-      compute_stage(smem + slot * STAGE, acc, mask, (int)((kvpack >> (4 * slot)) & 15u));
+      compute_stage<false, AL>(smem + slot * STAGE, acc, mask, (int)((kvpack >> (4 * slot)) & 15u));
       ++done;
     }
     cp_async_wait<0>();
@@ -849,30 +953,54 @@ struct Gemm {
       }
     };
     int issued = 0;
-#pragma unroll 1
-    for (int q = 0; q < STAGES - 1 && pseg < nseg; ++q) {
-      load_stage(smem + q * STAGE, cur, pk, m0, n0, M, N, aim, bim);
-      mbar_cpasync_arrive(&full[q]);
+    unsigned kvpack = 0;  // per stage slot: k-steps of 4 holding data (4 bits each)
+    auto note_k = [&](int slot) {
+      const int kv = DDK_KSKIP ? min(BK, cur.K - pk) : BK;
+      kvpack = (kvpack & ~(15u << (4 * slot))) | ((unsigned)((kv + 3) / 4) << (4 * slot));
+    };
+    FastLd f;
+    if constexpr (FASTLD_ANY) {
+      fast_tile(f, smem, m0, n0, M, N);
+      if (pseg < nseg) fast_seg(f, cur, m0, n0);
+    }
+    // one stage's copies (all at once: the interleaved form would have to wait for the buffer's
+    // previous readers before the compute stage, i.e. a CTA-wide barrier again)
+    auto load_next = [&](int slot) {
+      note_k(slot);
+      if constexpr (FASTLD_ANY) {
+        StageLd sl;
+        sl.f = &f, sl.sg = &cur, sl.slot = slot, sl.st = smem + slot * STAGE, sl.kofs = pk;
+        sl.m0 = m0, sl.n0 = n0, sl.M = M, sl.N = N, sl.aim = aim, sl.bim = bim;
+        sl.mode = (cur.acol == nullptr && pk + BK <= cur.K) ? 1 : 2;
+        sl.generic();
+        sl.all();
+      } else {
+        load_stage(smem + slot * STAGE, cur, pk, m0, n0, M, N, aim, bim);
+      }
+      mbar_cpasync_arrive(&full[slot]);
+      const int was = pseg;
       advance();
       ++issued;
-    }
+      if constexpr (FASTLD_ANY) {
+        if (pseg != was && pseg < nseg) fast_seg(f, cur, m0, n0);
+      }
+    };
+#pragma unroll 1
+    for (int q = 0; q < STAGES - 1 && pseg < nseg; ++q) load_next(q);
     const int lane = threadIdx.x & 31;
     int done = 0;
 #pragma unroll 1
     while (done < issued) {
       const int sb = done % STAGES;
       mbar_wait(&full[sb], (unsigned)((done / STAGES) & 1));
-      compute_stage(smem + sb * STAGE, acc, mask);
+      compute_stage(smem + sb * STAGE, acc, mask, (int)((kvpack >> (4 * sb)) & 15u));
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[sb]);
       ++done;
       if (pseg < nseg) {
         const int nb = issued % STAGES;
         if (issued >= STAGES) mbar_wait(&empty[nb], (unsigned)(((issued - STAGES) / STAGES) & 1));
-        load_stage(smem + nb * STAGE, cur, pk, m0, n0, M, N, aim, bim);
-        mbar_cpasync_arrive(&full[nb]);
-        advance();
-        ++issued;
+        load_next(nb);
       }
     }
     cp_async_wait<0>();

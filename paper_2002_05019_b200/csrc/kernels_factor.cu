@@ -1284,8 +1284,8 @@ struct K3Cfg<true, 12> {  // complex 64x32 4M, VEC, RECT
 #endif
 
 template <>
-struct K3Cfg<false, 13> {  // real 64x64, RECT, 2 stages (34 KB smem; dense microbench +1.5% at K=576)
-  using G = Gemm<64, 64, 16, 2, 2, 2, false, false, false, false, false, false, true>;
+struct K3Cfg<false, 13> {  // real 64x64, RECT, BK = 24, 2 stages (52 KB smem, 4 CTAs/SM): 2/3 of the stage barriers per flop of BK = 16 (cfg2: 29.9 -> 30.5 TF/s; BK = 32 only fits 3 CTAs/SM: 26.4)
+  using G = Gemm<64, 64, 24, 2, 2, 2, false, false, false, false, false, false, true>;
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
 };
 template <>
@@ -1325,9 +1325,9 @@ struct K3Cfg<true, 15> {  // complex 64x32 3M VEC, 5 CTAs per SM
 #endif
 #ifdef DD_AUX_AB
 template <>
-struct K3Cfg<false, 16> {  // real 64x64, BK = 32, 2 stages, RECT (3 CTAs/SM): half the stage barriers per flop
-  using G = Gemm<64, 64, 32, 2, 2, 2, false, false, false, false, false, false, true>;
-  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 3;
+struct K3Cfg<false, 16> {  // real 64x64, RECT, BK = 16, 2 stages (the default before BK = 24)
+  using G = Gemm<64, 64, 16, 2, 2, 2, false, false, false, false, false, false, true>;
+  static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
 };
 template <>
 struct K3Cfg<true, 16> {
@@ -1335,9 +1335,9 @@ struct K3Cfg<true, 16> {
   static constexpr int NT = 128, BM = 64, BN = 32, MINB = 3;
 };
 template <>
-struct K3Cfg<false, 17> {  // real 128x64, 4 warps of 64x32 (16 DMMAs per 12 fragment loads), 3 stages, RECT
-  using G = Gemm<128, 64, 16, 2, 2, 3, false, false, false, false, false, false, true>;
-  static constexpr int NT = 128, BM = 128, BN = 64, MINB = 2;
+struct K3Cfg<false, 17> {  // real 128x64, 8 warps of 32x32, 3 stages, RECT (2 CTAs/SM, 16 warps; 4 warps of 64x32: 24.5 TF/s on cfg2)
+  using G = Gemm<128, 64, 16, 4, 2, 3, false, false, false, false, false, false, true>;
+  static constexpr int NT = 256, BM = 128, BN = 64, MINB = 2;
 };
 template <>
 struct K3Cfg<true, 17> {
@@ -1345,9 +1345,9 @@ struct K3Cfg<true, 17> {
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 2;
 };
 template <>
-struct K3Cfg<false, 18> {  // real 64x128 (warps 2x2 of 32x64), 3 stages, RECT
-  using G = Gemm<64, 128, 16, 2, 2, 3, false, false, false, false, false, false, true>;
-  static constexpr int NT = 128, BM = 64, BN = 128, MINB = 2;
+struct K3Cfg<false, 18> {  // real 64x64, 8 warps of 32x16, 2 stages, RECT (3 CTAs/SM, 24 warps; 64x128 with 4 warps: 22.9 TF/s on cfg2)
+  using G = Gemm<64, 64, 16, 2, 4, 2, false, false, false, false, false, false, true>;
+  static constexpr int NT = 256, BM = 64, BN = 64, MINB = 3;
 };
 template <>
 struct K3Cfg<true, 18> {
@@ -1451,11 +1451,28 @@ __device__ __forceinline__ void k3_tile(const K3Args& a, int64_t blk, double* sm
   }
   auto segfn = [&](int q) { return (DDK_SEGC > 0 && q < K3_SEGC) ? segc[q] : gseg(q); };
   const int mlim = tg.M - T.tm * BM, nlim = tg.N - T.tn * BN;
-  const unsigned mask = G::tile_mask(mlim, nlim, tg.diag ? T.tn * BN - T.tm * BM : G::NO_DIAG);
+#ifndef DDK_K3_ALIAS
+#define DDK_K3_ALIAS 0  // measured slower on cfg2 (30.16 -> 29.64 TF/s: register spills on the aliased path, 2-4 extra barriers in its epilogue); A/B switch
+#endif
+  // ragged tiles (valid rows / columns within one warp row / column): the otherwise idle warps
+  // share the k-steps of the occupied warp tiles (gemm_core.cuh "warp aliasing")
+  const unsigned amap = DDK_K3_ALIAS ? G::alias_map(mlim, nlim) : 0u;
+  const int diag_off = tg.diag ? T.tn * BN - T.tm * BM : G::NO_DIAG;
   double* Cb = a.arena + nj.panel + tg.ro + (int64_t)T.tm * BM + (int64_t)T.tn * BN * nj.ld;
-  G::prefetch_tile_l2(Cb, nj.ld, a.aim, mlim, nlim);
-  G::run(segfn, tg.c1 - tg.c0, T.tm * BM, T.tn * BN, tg.M, tg.N, a.wim, a.aim, smem, acc, mask);
-  G::template store_tile<1>(acc, smem, Cb, nj.ld, a.aim, mlim, nlim);
+#ifndef DDK_K3_RED
+#define DDK_K3_RED 1
+#endif
+  constexpr int EPI = DDK_K3_RED ? 2 : 1;  // 2: L2 reductions (no C read round trip); 1: read-modify-write
+  if (EPI == 1) G::prefetch_tile_l2(Cb, nj.ld, a.aim, mlim, nlim);
+  unsigned mask;
+  if (amap) {  // CTA-uniform
+    mask = G::tile_mask(mlim, nlim, diag_off, true);
+    G::template run<true>(segfn, tg.c1 - tg.c0, T.tm * BM, T.tn * BN, tg.M, tg.N, a.wim, a.aim, smem, acc, mask);
+  } else {
+    mask = G::tile_mask(mlim, nlim, diag_off);
+    G::run(segfn, tg.c1 - tg.c0, T.tm * BM, T.tn * BN, tg.M, tg.N, a.wim, a.aim, smem, acc, mask);
+  }
+  G::template store_tile<EPI>(acc, smem, Cb, nj.ld, a.aim, mlim, nlim, amap, mask != 0u);
 }
 
 template <bool C, int CFG>

@@ -35,12 +35,19 @@ struct SolveN {
 #ifndef DDK_SOLVE_STAGES_REAL
 #define DDK_SOLVE_STAGES_REAL 2
 #endif
+#ifndef DDK_SOLVE_RED
+#define DDK_SOLVE_RED 1
+#endif
 template <bool C, bool M3>
 struct SolveG {
   static constexpr int BN = SolveN<C>::value;
   static constexpr int ST = C ? 2 : DDK_SOLVE_STAGES_REAL;
-  using FU = Gemm<SUBM, BN, 16, 2, 2, ST, C, false, true, C && M3, C>;  // MK x KN (FINE = C)
-  using BU = Gemm<SUBM, BN, 16, 2, 2, ST, C, true, true, C && M3, C>;   // KM x KN
+#ifndef DDK_SOLVE_FAST_C
+#define DDK_SOLVE_FAST_C 1
+#endif
+  static constexpr bool FAST = !C || DDK_SOLVE_FAST_C;  // fast loader (A/B switch for the complex kernels)
+  using FU = Gemm<SUBM, BN, 16, 2, 2, ST, C, false, true, C && M3, C, false, false, false, FAST>;  // MK x KN (FINE = C)
+  using BU = Gemm<SUBM, BN, 16, 2, 2, ST, C, true, true, C && M3, C, false, false, false, FAST>;   // KM x KN
 };
 
 // ---------------------------------------------------------------------------- permutations
@@ -161,8 +168,10 @@ __global__ void __launch_bounds__(128, M3 ? 3 : 4) k_fupd(SolveArgs a) {
   };
   G::run(segfn, T.c1 - T.c0, m0, n0, ni.s, a.nrhs, a.aim, a.yim, smem, acc,
          G::tile_mask(ni.s - m0, a.nrhs - n0, G::NO_DIAG));
-  G::template store_tile<1>(acc, smem, a.y + ni.ydof + m0 + (int64_t)n0 * a.ldy, a.ldy, a.yim, ni.s - m0,
-                            a.nrhs - n0);
+  // y_i -= acc as L2 reductions: one reduction per element and launch (owner-computes tiles), so
+  // the result is order-independent and bitwise the read-modify-write one (gemm_core.cuh MODE 2)
+  G::template store_tile<DDK_SOLVE_RED ? 2 : 1>(acc, smem, a.y + ni.ydof + m0 + (int64_t)n0 * a.ldy, a.ldy, a.yim,
+                                                 ni.s - m0, a.nrhs - n0);
 }
 
 // Backward pull update y_t -= sum_{i in struct(t)} L_it^T y_i.  With split-K (G > 1) CTA
@@ -210,8 +219,8 @@ __global__ void __launch_bounds__(128, M3 ? 3 : 4) k_bupd(SolveArgs a, int G, do
   G_::run(segfn, qb - qa + 1, m0, n0, nt.s, a.nrhs, a.aim, a.yim, smem, acc,
           G_::tile_mask(nt.s - m0, a.nrhs - n0, G_::NO_DIAG));
   if (G == 1) {
-    G_::template store_tile<1>(acc, smem, a.y + nt.ydof + m0 + (int64_t)n0 * a.ldy, a.ldy, a.yim, nt.s - m0,
-                               a.nrhs - n0);
+    G_::template store_tile<DDK_SOLVE_RED ? 2 : 1>(acc, smem, a.y + nt.ydof + m0 + (int64_t)n0 * a.ldy, a.ldy, a.yim,
+                                                    nt.s - m0, a.nrhs - n0);
   } else if constexpr (CL) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
