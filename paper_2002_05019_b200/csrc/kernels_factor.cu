@@ -1239,9 +1239,9 @@ struct K3Cfg<false, 9> {  // real 64x64, coarse masking, vectorised (16-byte) fr
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
 };
 template <>
-struct K3Cfg<true, 9> {  // complex 64x32 3M, vectorised fragment loads (generic loader: the fast one spills at 128 registers)
-  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, true, true, false, false, false>;
-  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
+struct K3Cfg<true, 9> {  // complex 64x32 3M, vectorised fragment loads, fast loader at 3 CTAs/SM (162 registers, no spills; at 4 CTAs/SM the fast loader spills: 21 TF/s; generic loader at 4 CTAs/SM: 38.5 vs 40.0 effective TF/s on cfg3)
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, true, true>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 3;
 };
 template <>
 struct K3Cfg<false, 10> {  // real 64x64, per-sub-tile masking, vectorised fragment loads
@@ -1360,9 +1360,9 @@ struct K3Cfg<false, 19> {  // = 13
   static constexpr int NT = 128, BM = 64, BN = 64, MINB = 4;
 };
 template <>
-struct K3Cfg<true, 19> {  // complex 64x32 3M VEC (= 9) at 3 CTAs/SM: 168 registers, no spills
-  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, true, true>;
-  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 3;
+struct K3Cfg<true, 19> {  // complex 64x32 3M VEC, generic loader, 4 CTAs/SM (the default before the fast loader at 3 CTAs/SM)
+  using G = Gemm<64, 32, 16, 2, 2, 2, true, false, false, true, true, true, false, false, false>;
+  static constexpr int NT = 128, BM = 64, BN = 32, MINB = 4;
 };
 #endif
 

@@ -271,10 +271,20 @@ __global__ void __launch_bounds__(128, M3 ? 3 : 4) k_bupd(SolveArgs a, int G, do
         if (m0 + r >= nt.s || n0 + c >= a.nrhs) continue;
         const int64_t pe = (int64_t)r + (int64_t)(n0 + c) * SUBM;
         double sr = 0.0, si = 0.0;
-        for (int h = 0; h < G; ++h) {
-          const double* Q = part + (int64_t)(tile * G + h) * SUBM * a.nrhs;
-          sr += __ldcg(Q + pe);
-          if (C) si += __ldcg(Q + pe + pim);
+        for (int h0 = 0; h0 < G; h0 += 8) {  // 8 partials in flight, added in the order h = 0..G-1
+          double vr[8], vi[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const double* Q = part + (int64_t)(tile * G + min(h0 + u, G - 1)) * SUBM * a.nrhs;
+            vr[u] = __ldcg(Q + pe);
+            vi[u] = C ? __ldcg(Q + pe + pim) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (h0 + u < G) {
+              sr += vr[u];
+              if (C) si += vi[u];
+            }
         }
         const int64_t o = nt.ydof + (int64_t)(m0 + r) + (int64_t)(n0 + c) * a.ldy;
         a.y[o] -= sr;
@@ -777,10 +787,20 @@ void launch_bupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, int max_rp,
   int G = part ? bupd_split(cplx, ntiles, a.nrhs, max_rp) : 1;
   if (cluster) G = std::min(G, 8);
   const int64_t pim = (int64_t)BUPD_MAX_PARTS * SUBM * a.nrhs;
-  if (!cplx) bupd_t<false, false>(a, ntiles, G, part, pim, cluster, st);
-  else if (m3) bupd_t<true, true>(a, ntiles, G, part, pim, cluster, st);
-  else bupd_t<true, false>(a, ntiles, G, part, pim, cluster, st);
-  if (G > 1 && !cluster && !a.cnt) {
+  // The in-kernel (last-arriver) reduction is ONE CTA per (tile, rhs tile) reading G partial
+  // tiles: with many chunks and few tiles (the top levels; cfg1 everywhere) the separate reduce
+  // kernel spreads the same fixed-order sums over the whole GPU instead (cfg1 backward update
+  // 5.5 -> 2.7 ms per batch).  Both forms add the partials in the order g = 0..G-1: bitwise equal.
+#ifndef DDK_BUPD_FOLD_MAXG
+#define DDK_BUPD_FOLD_MAXG 8
+#endif
+  SolveArgs b = a;
+  if (G > DDK_BUPD_FOLD_MAXG) b.cnt = nullptr;
+  const SolveArgs& a_ = b;
+  if (!cplx) bupd_t<false, false>(a_, ntiles, G, part, pim, cluster, st);
+  else if (m3) bupd_t<true, true>(a_, ntiles, G, part, pim, cluster, st);
+  else bupd_t<true, false>(a_, ntiles, G, part, pim, cluster, st);
+  if (G > 1 && !cluster && !a_.cnt) {
     dim3 g2(ntiles, std::min(64, (SUBM * a.nrhs + 255) / 256));
     if (cplx) k_bupd_reduce<true><<<g2, 256, 0, st>>>(a, G, part, pim);
     else k_bupd_reduce<false><<<g2, 256, 0, st>>>(a, G, part, pim);
