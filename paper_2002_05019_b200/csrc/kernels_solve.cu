@@ -788,11 +788,13 @@ void launch_bupd(bool cplx, bool m3, const SolveArgs& a, int ntiles, int max_rp,
   if (cluster) G = std::min(G, 8);
   const int64_t pim = (int64_t)BUPD_MAX_PARTS * SUBM * a.nrhs;
   // The in-kernel (last-arriver) reduction is ONE CTA per (tile, rhs tile) reading G partial
-  // tiles: with many chunks and few tiles (the top levels; cfg1 everywhere) the separate reduce
-  // kernel spreads the same fixed-order sums over the whole GPU instead (cfg1 backward update
-  // 5.5 -> 2.7 ms per batch).  Both forms add the partials in the order g = 0..G-1: bitwise equal.
+  // tiles; the separate reduce kernel spreads the same fixed-order sums over the whole GPU.
+  // Measured (solve ms per 1000 RHS, fold for G <= 0 / 4 / 8 / 32): cfg1 143 / 145 / 147 / 185,
+  // cfg2 4,234 / 4,238 / 4,253 / 4,352, cfg3 3,504 / 3,539 / 3,551 / 3,599 -- the separate kernel
+  // wins everywhere, so the fold is off (DDK_BUPD_FOLD_MAXG = 0; A/B switch).  Both forms add the
+  // partials in the order g = 0..G-1: bitwise equal.
 #ifndef DDK_BUPD_FOLD_MAXG
-#define DDK_BUPD_FOLD_MAXG 8
+#define DDK_BUPD_FOLD_MAXG 0
 #endif
   SolveArgs b = a;
   if (G > DDK_BUPD_FOLD_MAXG) b.cnt = nullptr;
