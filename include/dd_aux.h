@@ -156,7 +156,11 @@ int dd_aux_solve_work_bytes(dd_aux_handle_t h, int64_t nrhs, size_t* bytes);
  * Returns DD_OK, DD_ZERO_PIVOT (D singular), DD_NONFINITE (NaN/Inf met in a pivot column; the
  * factor is unusable), or an error.  With options.perturb an exactly zero pivot is perturbed
  * instead (DD_OK, finfo.nperturbed > 0).  After DD_ZERO_PIVOT / DD_NONFINITE a solve returns
- * DD_ERR_SINGULAR. */
+ * DD_ERR_SINGULAR.
+ * Reproducibility: the factor (and the solve) are bitwise reproducible run to run and between
+ * direct launches and CUDA-graph replays: every Schur-update tile sums its contributors in a fixed
+ * order and is subtracted from its target by exactly ONE L2 reduction per element and launch
+ * (no accumulation order to depend on, K3). */
 int dd_aux_factor(dd_aux_handle_t h, const void* d_vals, const int64_t* val_offset, void* d_factor,
                   void* d_work, void* stream, dd_aux_factor_info* finfo);
 
