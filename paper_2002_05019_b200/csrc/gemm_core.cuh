@@ -7,8 +7,11 @@
 // concatenation of a list of segments ("gathered K", SURVEY.md §8(a) a4:
 // owner-computes target tiles summing all contributors of a level in a fixed
 // order -- deterministic, no atomics).  Operands are staged into shared memory by
-// cp.async (LDGSTS, 16-byte chunks, zero-filled outside the logical shape) in a
-// STAGES-deep pipeline and fed to mma.sync.m16n8k4.f64 from registers.
+// cp.async (LDGSTS, 16-byte chunks; zero-filled along K outside the logical shape,
+// rows / columns outside it are never stored) in a STAGES-deep pipeline and fed to
+// mma.sync.m16n8k4.f64 from registers.  The copies go through per-thread running
+// pointers (the "fast loader" below); the tile can be subtracted from C by L2
+// reductions (store_tile MODE 2).
 //
 // Operand layouts (all column-major storage in HBM):
 //   A "MK": A(m,k) = a[m + col(k)*lda]   (m contiguous; optional column gather map)
@@ -372,23 +375,25 @@ struct Gemm {
     }
   }
 
-  // ---- Fast loader (MK x NK operands, no column gather).  load_stage recomputes every chunk's
-  // source address and bounds from scratch (~26 SASS instructions and a 6-deep dependent chain
-  // per cp.async: more issue slots per stage than the DMMAs themselves).  A thread's chunks of a
-  // stage all share one row offset and sit a fixed number of k-columns apart, so inside a segment
-  // the thread keeps ONE running pointer per operand (pa, pb): a full stage costs one 64-bit add
-  // per chunk.  The row predicate (bytes) is constant per tile; only a segment's last partial
-  // stage (pk + BK > K) and gathered segments go through load_stage.  The chunks of the next
-  // stage are issued in BK/4 parts between the k-steps of the current stage (part(ks)), so no
-  // warp spends a long DMMA-free stretch issuing copies.
+  // ---- Fast loader (all four operand layouts; segments without a column gather).  load_stage
+  // recomputes every chunk's source address and bounds from scratch (~26 SASS instructions and a
+  // 6-deep dependent chain per cp.async: more issue slots per stage than the DMMAs themselves,
+  // and with 16 warps per SM the kernels were bound by each warp's serial instruction latency).
+  // A thread's chunks of a stage share one row (or k) offset and sit a fixed distance apart, so
+  // inside a segment the thread keeps ONE running pointer per operand (pa, pb): a full stage
+  // costs one 64-bit add per chunk.  The row predicate is constant per tile; only a segment's
+  // last partial stage (pk + BK > K) and gathered segments go through load_stage.  The chunks of
+  // the next stage are issued in parts between the k-steps of the current stage (part<KS>).
 #ifndef DDK_FASTLD
 #define DDK_FASTLD 1
 #endif
   static constexpr int KSTEPS = BK / 4;
-  // the copies of a stage go out in the first SPREAD k-steps.  Measured on cfg2 (2-stage pipelines):
-  // K3 (MK x NK) 29.3 / 29.8 / 29.9 TF/s with SPREAD 1 / 2 / 4; the solve (.. x KN) 4,405 / 4,367 /
-  // 4,505 ms per 1000 RHS -- copies issued in the last k-steps have little time to land before
-  // the next stage's wait, which the solve's shorter stages (32-column tiles) expose.
+  static_assert(KSTEPS >= 1 && KSTEPS <= 8, "StageLd::part_rt / all() and the 4-bit k-step counts cover BK <= 32");
+  // The copies of a stage go out in the first SPREAD k-steps (0 = all KSTEPS).  Measured with
+  // 2-stage pipelines: real K3 (MK x NK) on cfg2, BK = 16: 29.3 / 29.8 / 29.9 TF/s with SPREAD
+  // 1 / 2 / 4; BK = 24: 30.1 / 30.3 / 30.4 with 4 / 3 / 6; the solve (.. x KN) 4,405 / 4,367 /
+  // 4,505 ms per 1000 RHS with 1 / 2 / 4 -- copies issued in the last k-steps have little time
+  // to land before the next stage's wait.
 #ifndef DDK_FASTLD_SPREAD
 #define DDK_FASTLD_SPREAD 0
 #endif
@@ -413,7 +418,7 @@ struct Gemm {
     static constexpr bool OK = GRP > 0 && NTHR % GRP == 0 && (KC ? R : BK) % STEP == 0 && CH >= 1 && CH <= 32;
     __device__ static int off(int tid) {  // offset of the thread's first chunk inside the operand's stage tile
       const int c = (tid % GRP) * 2, o = tid / GRP;
-      return KC ? o * LD + c : o * LD + c;
+      return o * LD + c;  // RC: k column o, row pair c; KC: row o, k pair c
     }
     static constexpr int DSTEP = STEP * LD;  // smem distance between a thread's successive chunks
   };
