@@ -401,9 +401,9 @@ struct Gemm {
 #define DDK_FASTLD_SPREAD_KN 2
 #endif
 #ifndef DDK_FASTLD_SPREAD_CPLX
-#define DDK_FASTLD_SPREAD_CPLX 1  // complex 3M K3 at 3 CTAs/SM on cfg3: 40.0 / 39.5 / 37.4 effective TF/s with SPREAD 1 / 2 / 4
+#define DDK_FASTLD_SPREAD_CPLX 1  // complex (cfg3): 3M K3 at 3 CTAs/SM 40.0 / 39.5 / 37.4 effective TF/s with SPREAD 1 / 2 / 4; solve 3,439 / 3,523 / 3,799 ms per 1000 RHS
 #endif
-  static constexpr int SPREAD_REQ = B_KN ? DDK_FASTLD_SPREAD_KN : (CPLX ? DDK_FASTLD_SPREAD_CPLX : DDK_FASTLD_SPREAD);
+  static constexpr int SPREAD_REQ = CPLX ? DDK_FASTLD_SPREAD_CPLX : (B_KN ? DDK_FASTLD_SPREAD_KN : DDK_FASTLD_SPREAD);
   static constexpr int SPREAD = (SPREAD_REQ > 0 && SPREAD_REQ < KSTEPS) ? SPREAD_REQ : KSTEPS;
   // One operand's copy pattern.  RC (row-contiguous: A "MK" / B "NK"): a thread's chunks share one
   // row pair and sit KS k-columns apart, the running pointer walks through them and through the
