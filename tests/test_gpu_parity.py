@@ -271,6 +271,38 @@ def test_cuda_graphs_bitwise_equal_direct(name, grid, sizes, tol):
     assert residual_berr(p, X, random_rhs(p.n, 3, p.is_complex, 2)).max() <= TOL_BERR
 
 
+@pytest.mark.parametrize("name,grid,sizes", [("cfg2", (3, 3, 2), lambda n, rng: rng.integers(40, 301, n)),
+                                             ("cfg3", (3, 2, 2), 90)])
+def test_factor_solve_bitwise_reproducible(name, grid, sizes):
+    """Two independent factorizations + solves of the same bytes are bitwise equal: every Schur
+    update tile sums its contributors in a fixed order and reaches its target (and the solve
+    updates reach y) through exactly ONE L2 reduction per element and launch (DESIGN.md section 7,
+    K3 / K5), so nothing depends on the order the reductions arrive in.  Ragged interface sizes:
+    edge tiles, multi-level gathered K and the split-K backward update all take part."""
+    import torch
+    import paper_2002_05019_b200 as dd
+    from tests._gpu import to_dev_colmajor
+    p = dd_inputs.config(name, grid=grid, sizes=sizes)
+    vals = torch.from_numpy(p.values).cuda()
+    B = random_rhs(p.n, 70, p.is_complex, 5)
+    outs = []
+    for rep in range(2):
+        s = dd.AuxSolver(p.blk_size, p.colptr, p.rowidx, complex_=p.is_complex)
+        rc, fi = s.factor(vals, p.val_offset)
+        assert rc == dd.DD_OK
+        Bd = to_dev_colmajor(B, torch)
+        s.solve_(Bd)
+        torch.cuda.synchronize()
+        piv = s.pivots()
+        outs.append((Bd.cpu().numpy(), piv, fi["max_abs_L"]))
+        s.close()
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert outs[0][2] == outs[1][2]
+    for k in outs[0][1]:
+        assert np.array_equal(np.asarray(outs[0][1][k]), np.asarray(outs[1][1][k])), k
+    assert residual_berr(p, outs[0][0], B).max() <= TOL_BERR
+
+
 def test_complex_4m_parity():
     """Complex Schur update with the four-real-product (4M) form (options.complex_3m = 0)."""
     import torch
