@@ -46,7 +46,10 @@ constexpr int ATY = 8;     // thread rows (256 threads: 32 x 8, 4 columns each)
 }  // namespace
 
 // One CTA per (output block, 32-column chunk); loops over 32-row tiles of the block.
-template <bool C, bool SYM>
+// ACC (SYM = false only): accumulate onto the block's current values; a template parameter so the
+// plain assembly carries no per-element branch for it (as a runtime flag it cost cfg2's assembly
+// 11.5 -> 12.3 ms).
+template <bool C, bool SYM, bool ACC = false>
 __global__ void __launch_bounds__(AT * ATY) k_assemble(AsmArgs a) {
   using E = Elem<C>;
   using T = typename E::T;
@@ -60,13 +63,13 @@ __global__ void __launch_bounds__(AT * ATY) k_assemble(AsmArgs a) {
   // S_p element of the block is then read from HBM once (the pair S[r0, c0] / S[c0, r0] is read by
   // this CTA only)
   const bool mirror = SYM && it.pad;
-  if (a.accumulate && it.k0 == it.k1) return;  // accumulate mode: blocks no clique covers keep their values
+  if (ACC && it.k0 == it.k1) return;  // accumulate mode: blocks no clique covers keep their values
   for (int r0 = mirror ? it.c0 : 0; r0 < it.rows; r0 += AT) {
     T acc[AT / ATY];
 #pragma unroll
     for (int j = 0; j < AT / ATY; ++j) {
       const int row = r0 + tx, col = it.c0 + ty + ATY * j;  // accumulate (SYM = false only): start from the block
-      acc[j] = (a.accumulate && row < it.rows && col < it.cols) ? out[row + (int64_t)col * it.rows] : E::zero();
+      acc[j] = (ACC && row < it.rows && col < it.cols) ? out[row + (int64_t)col * it.rows] : E::zero();
     }
     for (int q = it.k0; q < it.k1; ++q) {
       const AsmContrib c = a.con[q];
@@ -117,11 +120,14 @@ int asm_chunk() { return AT; }
 void launch_assemble(bool cplx, bool sym, const AsmArgs& a, int nitems, cudaStream_t st) {
   if (nitems <= 0) return;
   const dim3 grid(nitems), block(AT * ATY);
+  const bool acc = a.accumulate != 0;  // api.cu only passes accumulate with sym off
   if (cplx) {
     if (sym) k_assemble<true, true><<<grid, block, 0, st>>>(a);
+    else if (acc) k_assemble<true, false, true><<<grid, block, 0, st>>>(a);
     else k_assemble<true, false><<<grid, block, 0, st>>>(a);
   } else {
     if (sym) k_assemble<false, true><<<grid, block, 0, st>>>(a);
+    else if (acc) k_assemble<false, false, true><<<grid, block, 0, st>>>(a);
     else k_assemble<false, false><<<grid, block, 0, st>>>(a);
   }
 }
